@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""bench.py -- MoE-layer fwd+bwd tokens/s of the B200-native HEXA-MoE hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+One step = one fwd+bwd pass (routing-index build, ESMM x4, ESTMM x2, ESS x2)
+of the layer over one synthetic batch: the reference's own generators
+(make_random_params scale 0.5, x ~ N(0,1), uniform top-k routing, seed 1,
+g_y = ones as in tools/commands.cpp:220-221).
+
+value   : whole-job tokens/s with inputs resident in HBM, each step timed with
+          CUDA events on the launch stream, L2 flushed (256 MiB write) between
+          steps outside the timed events, max over ranks.
+e2e     : the same metric through the public API (paper_2411_01288_b200.LayerRunner)
+          with x, g_y and the routing in pinned HOST memory: H2D copies, fwd+bwd
+          and the D2H read of y are inside the timed region every step.
+roofline: the dominant kernel's algorithmic FLOP (or bytes) per launch over its
+          live CUDA-event duration inside the timed region, against
+          MEASURED_PEAKS.json.
+cpu_baseline: the reference's own CPU path (oracle/_ref, compiled unmodified
+          from /root/reference) on the host cores, rank 0, bounded sample.
+--impl reference: times that same reference CPU path as the reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE.json configs; N for c3/c5 is not given there
+    "c1": dict(E=8, k=1, D=96, H=384, N=3136, dtype="f32", dist="uniform",
+               desc="single MoE-MLP layer 8E top-1 d96 ffn384 3136 tok fp32"),
+    "c2": dict(E=32, k=2, D=384, H=1536, N=16384, dtype="bf16", dist="uniform",
+               desc="Swin-MoE-S stage-3 layer 32E top-2 d384 ffn1536 16384 tok bf16"),
+    "c3": dict(E=32, k=2, D=1024, H=4096, N=16384, dtype="bf16", dist="uniform",
+               desc="Swin-MoE-B stage-4 layer 32E top-2 d1024 ffn4096, 16384 tok per GPU"),
+    "c4": dict(E=64, k=2, D=1024, H=4096, N=131072, dtype="bf16", dist="uniform",
+               desc="64E top-2 d1024 ffn4096 131072 tok"),
+    "c5": dict(E=64, k=2, D=768, H=3072, N=16384, dtype="bf16", dist="skew90",
+               desc="64E top-2 d768 ffn3072, 90% of tokens to experts {0,1}"),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return dict(hbm=d["hbm_gbs"], tensor=d["bf16_tflops"],
+                    tensor_sustained=d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                    source="measured")
+    except (OSError, KeyError, ValueError):
+        return dict(hbm=6650.0, tensor=1590.0, tensor_sustained=1400.0, source="fallback")
+
+
+def skew90_routing(N, E, k, seed):
+    """c5: 90% of tokens choose {0, 1} (choice i -> expert i), the rest uniform
+    distinct pairs from the reference generator."""
+    import numpy as np
+    from paper_2411_01288_b200 import RoutingChoice, synthesize_routing
+    r = synthesize_routing(N, E, k, "uniform", seed)
+    a = r.assignments.copy()
+    rng = np.random.default_rng(seed)
+    hot = rng.random(N) < 0.9
+    for i in range(k):
+        a[i, hot] = i
+    return RoutingChoice(N, E, k, a)
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle sampling during the timed region."""
+
+    def __init__(self, index=0, period=0.1):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period, self._stop = period, threading.Event()
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N, self.h = N, N.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 - clocks are best effort
+            self.N = None
+
+    def _run(self):
+        N = self.N
+        names = {getattr(N, a): a for a in dir(N) if a.startswith("nvmlClocksThrottleReason")
+                 and isinstance(getattr(N, a), int)}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                bits = N.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for v, nm in names.items():
+                    if v and bits & v and v != N.nvmlClocksThrottleReasonGpuIdle:
+                        self.reasons.add(nm.replace("nvmlClocksThrottleReason", ""))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.N:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.N:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def dist_init(args):
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return rank, ws, local
+
+
+def max_over_ranks(v, ws):
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    import torch
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def cpu_baseline(cfg, max_seconds=25.0):
+    """Reference CPU path (oracle/_ref) on a bounded token sample, all host threads."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    if not O.ref_available():
+        return None
+    threads = max(1, min(os.cpu_count() or 1, 64))
+    E, k, D, H = cfg["E"], cfg["k"], cfg["D"], cfg["H"]
+    # probe the rate, then size the sample to ~max_seconds (never above N)
+    probe = max(threads * 8, 16)
+    t = O.ref_time_layer(E, k, D, H, D, probe, 8, threads, 1)
+    rate = probe / max(t, 1e-6)
+    n = int(min(cfg["N"], max(probe, rate * max_seconds * 0.8)))
+    n = max(threads, n // threads * threads)
+    t = O.ref_time_layer(E, k, D, H, D, n, 8, threads, 1)
+    return {"value": n / t, "unit": "tokens/s", "cores": threads, "kind": "reference",
+            "sample": f"{n} of {cfg['N']} tokens, fwd+bwd via moekit::moe_forward/"
+                      f"moe_backward, {threads} threads on disjoint token shards",
+            "seconds": t}
+
+
+def run_reference(args, cfg, rank, ws):
+    """--impl reference: the reference's CPU implementation of the same path."""
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    threads = max(1, min(os.cpu_count() or 1, 64))
+    E, k, D, H = cfg["E"], cfg["k"], cfg["D"], cfg["H"]
+    budget = 150.0 / max(1, args.steps + args.warmup)  # whole run within minutes
+    probe = max(threads * 8, 16)
+    tp = O.ref_time_layer(E, k, D, H, D, probe, 8, threads, 1)
+    rate = probe / max(tp, 1e-6)
+    n = int(min(cfg["N"], max(probe, rate * budget * 0.8)))
+    n = max(threads, n // threads * threads)
+    for _ in range(args.warmup):
+        O.ref_time_layer(E, k, D, H, D, n, 8, threads, 1)
+    times = [O.ref_time_layer(E, k, D, H, D, n, 8, threads, 1) for _ in range(args.steps)]
+    total = sum(times)
+    val = n * args.steps / total
+    sample = f"{n} of {cfg['N']} tokens per step, {threads} threads"
+    out = {
+        "impl": "reference", "metric": "MoE layer fwd+bwd tokens/sec", "value": val,
+        "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "desc": cfg["desc"], "E": E, "k": k, "d": D,
+                   "ffn": H, "tokens": cfg["N"]},
+        "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": threads,
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+
+
+def run_ours(args, cfg, rank, ws, local):
+    import numpy as np
+    import torch
+
+    import paper_2411_01288_b200 as H
+    from paper_2411_01288_b200 import _lib
+    from paper_2411_01288_b200.runner import LayerRunner
+
+    dtype = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
+    E, k, D, Hd, N = cfg["E"], cfg["k"], cfg["D"], cfg["H"], cfg["N"]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    seed = 1 + rank  # each rank its own token batch (weak scaling)
+    p, x = H.make_random_params(E, D, Hd, D, "gelu", seed=1, n_tokens=N, dtype=dtype,
+                                device=dev)
+    if rank:
+        _, x = H.make_random_params(E, D, Hd, D, "gelu", seed=seed, n_tokens=N, dtype=dtype,
+                                    device=dev)
+    r = skew90_routing(N, E, k, seed) if cfg["dist"] == "skew90" else \
+        H.synthesize_routing(N, E, k, cfg["dist"], seed)
+    a = r.to_device(dev)
+    gy = torch.ones(N, D, dtype=dtype, device=dev)
+    run = LayerRunner(p, N, k, dev, dtype)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    # warm-up (also validates routing once)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    run.forward(x, a, status=status)
+    run.backward(x, gy)
+    torch.cuda.synchronize()
+    assert int(status.item()) == 0
+    for _ in range(max(0, args.warmup - 1)):
+        run.step(x, a, gy)
+    barrier(ws)
+
+    # ---- device-resident timed region ------------------------------------
+    L = _lib.lib()
+    L.hxm_profile_reset()
+    launches0 = L.hxm_launch_count()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    barrier(ws)
+    with clocks:
+        L.hxm_profile_enable(1)
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush outside the step's events
+            evs[i][0].record(stream)
+            run.step(x, a, gy)
+            evs[i][1].record(stream)
+        L.hxm_profile_enable(0)
+        barrier(ws)
+    launches = L.hxm_launch_count() - launches0
+    step_ms = [s.elapsed_time(e) for s, e in evs]
+    total_ms = max_over_ranks(sum(step_ms), ws)
+    prof = _lib.profile_read()
+    L.hxm_profile_reset()
+    value = N * ws * args.steps / (total_ms / 1000.0)
+
+    # ---- end-to-end through the public API with host buffers --------------
+    xh = x.cpu().pin_memory()
+    gyh = gy.cpu().pin_memory()
+    ah = a.cpu().pin_memory()
+    yh = torch.empty(N, D, dtype=torch.float32).pin_memory()
+    xd, gyd, ad = torch.empty_like(x), torch.empty_like(gy), torch.empty_like(a)
+    e2e_steps = max(3, min(args.steps, 20))
+    for _ in range(2):
+        xd.copy_(xh, non_blocking=True); ad.copy_(ah, non_blocking=True)
+        gyd.copy_(gyh, non_blocking=True)
+        run.step(xd, ad, gyd)
+        yh.copy_(run.y, non_blocking=True)
+    barrier(ws)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        xd.copy_(xh, non_blocking=True)
+        ad.copy_(ah, non_blocking=True)
+        gyd.copy_(gyh, non_blocking=True)
+        run.step(xd, ad, gyd)
+        yh.copy_(run.y, non_blocking=True)
+    e1.record(stream)
+    barrier(ws)
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), ws)
+    e2e_val = N * ws * e2e_steps / (e2e_ms / 1000.0)
+    h2d = xh.numel() * xh.element_size() + gyh.numel() * gyh.element_size() + \
+        ah.numel() * ah.element_size()
+    d2h = yh.numel() * yh.element_size()
+
+    if rank != 0:
+        return
+    pk = peaks()
+    kernels = {}
+    for nm, (ms, n, work, kind) in prof.items():
+        avg_ms = ms / max(n, 1)
+        per_launch = work / max(n, 1)
+        if kind == 0:
+            ach = per_launch / (avg_ms / 1e3) / 1e12
+            kernels[nm] = {"avg_us": 1e3 * avg_ms, "launches": n, "achieved": ach,
+                           "unit": "TFLOP/s", "frac": ach / pk["tensor_sustained"]}
+        else:
+            ach = per_launch / (avg_ms / 1e3) / 1e9
+            kernels[nm] = {"avg_us": 1e3 * avg_ms, "launches": n, "achieved": ach,
+                           "unit": "GB/s", "frac": ach / pk["hbm"]}
+    dom = max(prof.items(), key=lambda kv: kv[1][0])[0] if prof else None
+    roof = None
+    if dom:
+        kd = kernels[dom]
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tf):
+            with open(tf) as f:
+                traffic = json.load(f).get(args.config, {}).get(dom)
+        tensor = kd["unit"] == "TFLOP/s"
+        roof = {"kernel": dom, "bound": "tensor" if tensor else "hbm",
+                "achieved": kd["achieved"],
+                "peak": pk["tensor_sustained"] if tensor else pk["hbm"],
+                "unit": kd["unit"], "frac": kd["frac"], "traffic": traffic,
+                "peak_source": f"{pk['source']} ({'bf16 sustained' if tensor else 'HBM copy'})",
+                "work_per_launch": prof[dom][2] / max(prof[dom][1], 1),
+                "share_of_step": prof[dom][0] / max(sum(v[0] for v in prof.values()), 1e-9)}
+    flop_step = 6.0 * k * N * (D * Hd + Hd * D)
+    cpu = None
+    if ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg)
+    out = {
+        "metric": "MoE layer fwd+bwd tokens/sec", "value": value, "unit": "tokens/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
+        "config": {"workload": args.config, "desc": cfg["desc"], "E": E, "k": k, "d": D,
+                   "ffn": Hd, "tokens_per_gpu": N, "routing": cfg["dist"],
+                   "parallelism": f"replicas{ws}" if ws > 1 else "single",
+                   "l2": "flushed between steps (256 MiB write, outside the timed events)"},
+        "layer_tflops": flop_step * args.steps * ws / (total_ms / 1e3) / 1e12,
+        "layer_frac_of_bf16_sustained": flop_step * args.steps / (total_ms / 1e3) / 1e12
+        / pk["tensor_sustained"],
+        "roofline": roof, "kernels": kernels,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_val, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "steps": e2e_steps},
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference(args, cfg, rank, int(os.environ.get("WORLD_SIZE", "1")))
+        return
+    rank, ws, local = dist_init(args)
+    try:
+        run_ours(args, cfg, rank, ws, local)
+    finally:
+        if ws > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

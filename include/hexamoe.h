@@ -1,0 +1,222 @@
+/*
+ * hexamoe.h -- C ABI of the B200-native HEXA-MoE expert-specific operators.
+ *
+ * This is the drop-in boundary for the reference `moekit` hot path
+ * (/root/reference/proj/core/include/moekit/{routing,es_ops,moe_layer}.hpp).
+ * Every entry point below names the reference function it replaces.  The
+ * signatures are plain C: device pointers, sizes and a cudaStream_t; no C++
+ * or torch types.  A host-side C++ shim that re-exposes the reference's
+ * signatures, and the ctypes binding used by the Python package, are shown in
+ * INTEGRATION.md.
+ *
+ * Conventions
+ *  - All tensor pointers are DEVICE pointers, dense row-major, with the
+ *    reference's shapes: x N x D1, weights E x D1 x D2 (dim0 = expert), bias
+ *    E x D2, ReIndex v int64[N'], idx int64[E+1] (routing.hpp:29-38).
+ *  - `dtype` selects the arithmetic: HXM_BF16 = bf16 inputs on the tcgen05
+ *    tensor cores with fp32 accumulation; HXM_F32 = fp32 inputs, fp32 FMA.
+ *    Biases, outputs and gradients are always fp32.
+ *  - Calls are asynchronous on `stream`.  Shape / argument checks run on the
+ *    host before any launch, in the reference's order, and return
+ *    HXM_ERR_SHAPE (reference ShapeError) or HXM_ERR_INVALID_ARG (reference
+ *    std::invalid_argument).  Data-dependent checks that the reference
+ *    performs while reading values (expert id out of range) are reported
+ *    through a device status word (`status_dev`, may be NULL).
+ *  - hxm_last_error() returns a thread-local message for the last failure.
+ *  - There is no CPU fallback: without a CUDA device every compute entry
+ *    point returns HXM_ERR_CUDA.
+ */
+#ifndef HEXAMOE_H
+#define HEXAMOE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* hxm_stream_t; /* == cudaStream_t */
+
+typedef enum hxm_status {
+  HXM_OK = 0,
+  HXM_ERR_SHAPE = 1,       /* moekit::ShapeError      (tensor.hpp:12-15)  */
+  HXM_ERR_INVALID_ARG = 2, /* std::invalid_argument                       */
+  HXM_ERR_CUDA = 3,
+  HXM_ERR_NCCL = 4,
+  HXM_ERR_CACHE = 5,       /* moekit::CacheError      (dist_sim.hpp:55-58) */
+  HXM_ERR_UNSUPPORTED = 6
+} hxm_status;
+
+typedef enum hxm_dtype { HXM_F32 = 0, HXM_BF16 = 1 } hxm_dtype;
+
+/* same order as moekit::ActivationKind (tensor.hpp:96) */
+typedef enum hxm_activation {
+  HXM_ACT_RELU = 0,
+  HXM_ACT_GELU = 1,
+  HXM_ACT_IDENTITY = 2
+} hxm_activation;
+
+/* moekit::EsOutputMode (es_ops.hpp:13) */
+typedef enum hxm_out_mode { HXM_WRITE = 0, HXM_ACCUMULATE = 1 } hxm_out_mode;
+
+const char* hxm_last_error(void);
+int hxm_version(void);
+/* Number of SMs of the current device, or -1 without a device. */
+int hxm_device_sm_count(void);
+
+/* ------------------------------------------------------------------------
+ * Routing index build -- replaces moekit::build_reindex (routing.hpp:42-43,
+ * routing.cpp:42-70).  Bit-exact: v is tokens grouped by expert, ascending
+ * inside each segment, segments padded with -1 to a multiple of blk;
+ * idx[0] = 0, idx[E] = N'.
+ * ---------------------------------------------------------------------- */
+/* Upper bound of N' = n + E*(blk-1): size of v. */
+size_t hxm_reindex_bound(int64_t n_tokens, int64_t n_experts, int64_t blk);
+size_t hxm_reindex_workspace_bytes(int64_t n_tokens, int64_t n_experts);
+/* assignment: device int32[n_tokens].  v: device int64[bound];
+ * idx: device int64[E+1].  status_dev (nullable, device int32): set to
+ * HXM_ERR_INVALID_ARG when an expert id is out of range (routing.cpp:47-48);
+ * the caller zeroes it.  blk == 0 -> HXM_ERR_INVALID_ARG before launch. */
+hxm_status hxm_build_reindex(const int32_t* assignment, int64_t n_tokens,
+                             int64_t n_experts, int64_t blk, int64_t* v,
+                             int64_t* idx, void* workspace,
+                             size_t workspace_bytes, int32_t* status_dev,
+                             hxm_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * Operators -- replace moekit::esmm / ess / estmm / esfk (es_ops.hpp:37-65).
+ * v/idx are a ReIndex built by hxm_build_reindex (or copied from the
+ * reference); n_padded_bound >= N' = idx[E] (hxm_reindex_bound suffices).
+ * Operator workspace: hxm_op_workspace_bytes().
+ * ---------------------------------------------------------------------- */
+size_t hxm_op_workspace_bytes(int64_t n_tokens, int64_t n_experts,
+                              int64_t n_padded_bound, int64_t d1, int64_t d2);
+
+/* esmm (es_ops.hpp:39-46): dest[t] (= | +=) bias[e(t)] + x[t] . W[e(t)].
+ * w_transposed = 0: weights is E x D1 x D2 (reference layout).
+ * w_transposed = 1: weights is E x D2 x D1 and W[e]^T is used -- this replaces
+ * materialising transpose_experts (tensor.cpp:143-153).  bias: fp32 E x D2
+ * or NULL.  dest: fp32 N x D2. */
+hxm_status hxm_esmm(hxm_dtype dtype, const void* x, int64_t n_tokens,
+                    int64_t d1, const void* weights, int64_t n_experts,
+                    int64_t d2, int w_transposed, const float* bias,
+                    const int64_t* v, const int64_t* idx,
+                    int64_t n_padded_bound, hxm_out_mode mode, float* dest,
+                    void* workspace, size_t workspace_bytes,
+                    hxm_stream_t stream);
+
+/* ess (es_ops.hpp:49): out[e] = sum of rows routed to e (fp32 E x D). */
+hxm_status hxm_ess(hxm_dtype dtype, const void* x, int64_t n_tokens, int64_t d,
+                   const int64_t* v, const int64_t* idx, int64_t n_experts,
+                   int64_t n_padded_bound, float* out, void* workspace,
+                   size_t workspace_bytes, hxm_stream_t stream);
+
+/* estmm (es_ops.hpp:52-53): out[e] = sum_{t in e} x1[t]^T x2[t]
+ * (fp32 E x D1 x D2; experts without tokens get zeros). */
+hxm_status hxm_estmm(hxm_dtype dtype, const void* x1, const void* x2,
+                     int64_t n_tokens, int64_t d1, int64_t d2,
+                     const int64_t* v, const int64_t* idx, int64_t n_experts,
+                     int64_t n_padded_bound, float* out, void* workspace,
+                     size_t workspace_bytes, hxm_stream_t stream);
+
+/* esfk (es_ops.hpp:55-65): grad_x = esmm(g, w_t, NULL) (write),
+ * grad_b = ess(g), grad_w = estmm(x, g).  w_t is E x D2 x D1 as in the
+ * reference; with w_transposed = 1 pass the un-transposed E x D1 x D2
+ * weights instead. */
+hxm_status hxm_esfk(hxm_dtype dtype, const void* x, const void* g,
+                    int64_t n_tokens, int64_t d1, int64_t d2,
+                    const void* w_t, int w_transposed, const int64_t* v,
+                    const int64_t* idx, int64_t n_experts,
+                    int64_t n_padded_bound, float* grad_x, float* grad_b,
+                    float* grad_w, void* workspace, size_t workspace_bytes,
+                    hxm_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * MoE layer -- replaces moekit::moe_forward / moe_backward
+ * (moe_layer.hpp:61-73, moe_layer.cpp:30-122).  The k routing choices are
+ * processed together: one combined expert-grouped index over the k*N
+ * (token, choice) slots, so every per-expert GEMM runs once per layer
+ * instead of once per choice.  The forward stash (ForwardStash,
+ * moe_layer.hpp:39-46) lives in `workspace` in expert-sorted row order and
+ * is consumed by hxm_moe_backward.
+ * ---------------------------------------------------------------------- */
+typedef struct hxm_layer_desc {
+  int64_t n_tokens;   /* N                                   */
+  int64_t n_experts;  /* E                                   */
+  int64_t k;          /* routing choices per token           */
+  int64_t d_in;       /* D_i                                 */
+  int64_t hidden;     /* H (this rank's slice under TP)      */
+  int64_t d_out;      /* D_o                                 */
+  int32_t activation; /* hxm_activation                      */
+  int32_t dtype;      /* hxm_dtype                           */
+  int32_t add_b2;     /* 1: add b2 (rank 0 under model-centric TP,
+                         dist_sim.cpp:486); 0: skip b2 / gb2 */
+  int32_t reserved;
+} hxm_layer_desc;
+
+size_t hxm_layer_workspace_bytes(const hxm_layer_desc* desc);
+
+/* forward: x N x D_i (dtype), w1 E x D_i x H (dtype), b1 fp32 E x H,
+ * w2 E x H x D_o (dtype), b2 fp32 E x D_o, assignments device int32 k x N
+ * (RoutingChoice::assignments, routing.hpp:14-21).  y: fp32 N x D_o
+ * (written, not accumulated).  status_dev as in hxm_build_reindex. */
+hxm_status hxm_moe_forward(const hxm_layer_desc* desc, const void* x,
+                           const void* w1, const float* b1, const void* w2,
+                           const float* b2, const int32_t* assignments,
+                           float* y, void* workspace, size_t workspace_bytes,
+                           int32_t* status_dev, hxm_stream_t stream);
+
+/* backward for the stash in `workspace`: g_y N x D_o (dtype).
+ * Gradients (fp32, written): gw1 E x D_i x H, gb1 E x H, gw2 E x H x D_o,
+ * gb2 E x D_o (skipped if add_b2 == 0; may be NULL then), gx N x D_i. */
+hxm_status hxm_moe_backward(const hxm_layer_desc* desc, const void* x,
+                            const void* w1, const void* w2, const void* g_y,
+                            void* workspace, size_t workspace_bytes,
+                            float* gw1, float* gb1, float* gw2, float* gb2,
+                            float* gx, hxm_stream_t stream);
+
+/* Debug/parity: copy the stash of choice `choice` back to token order as
+ * fp32 N x H (y1 = pre-activation, y2 = activation). */
+hxm_status hxm_moe_stash_export(const hxm_layer_desc* desc,
+                                const void* workspace, int64_t choice,
+                                float* y1, float* y2, hxm_stream_t stream);
+
+/* Algorithmic work counters of the last layer call (OpStats, es_ops.hpp:17-24):
+ * MACs on real tokens only = k*N*(D_i*H + H*D_o) per direction. */
+uint64_t hxm_layer_forward_macs(const hxm_layer_desc* desc);
+
+/* ------------------------------------------------------------------------
+ * Input generators (the reference's own seeded streams, random.hpp:13-54,
+ * routing.cpp:121-200), host memory.  Measurement inputs only.
+ * ---------------------------------------------------------------------- */
+/* dist: "uniform" | "zipf:<s>" | "fixed:<e>" | "balanced" */
+hxm_status hxm_synthesize_routing(int64_t n_tokens, int64_t n_experts,
+                                  int64_t k, const char* dist, uint64_t seed,
+                                  int32_t* assignments_host);
+/* make_random_params(E, D_i, H, D_o, ., Rng(seed), scale) followed by
+ * random_matrix(N, D_i) from the same stream (moe_layer.cpp:136-147,
+ * random.hpp:42-54; tools/commands.cpp:174-176), rounded to fp32. */
+void hxm_make_layer_inputs(uint64_t seed, int64_t n_experts, int64_t d_in,
+                           int64_t hidden, int64_t d_out, int64_t n_tokens,
+                           double scale, float* w1, float* b1, float* w2,
+                           float* b2, float* x);
+
+/* ------------------------------------------------------------------------
+ * Live kernel timing (bench.py roofline) and launch counting.  When enabled,
+ * every kernel region is bracketed by CUDA events on its launch stream.
+ * ---------------------------------------------------------------------- */
+void hxm_profile_enable(int on);
+void hxm_profile_reset(void);
+/* Aggregates recorded regions by name (synchronises on their events).
+ * names: max * name_len chars.  kind: 0 = work is FLOP, 1 = bytes.
+ * Returns the number of names written, -1 on a CUDA error. */
+int hxm_profile_read(int max, char* names, int name_len, double* total_ms,
+                     int64_t* launches, double* work, int32_t* kind);
+/* Kernels launched by this library since load. */
+uint64_t hxm_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEXAMOE_H */

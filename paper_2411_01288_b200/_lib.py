@@ -1,0 +1,130 @@
+"""ctypes binding of libhexamoe.so (the C ABI declared in include/hexamoe.h).
+
+The product path has exactly one implementation: the CUDA kernels in this
+library.  If the library is missing or the process has no CUDA device, the
+operator calls raise -- there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libhexamoe.so")
+
+HXM_OK, HXM_ERR_SHAPE, HXM_ERR_INVALID_ARG, HXM_ERR_CUDA = 0, 1, 2, 3
+HXM_ERR_NCCL, HXM_ERR_CACHE, HXM_ERR_UNSUPPORTED = 4, 5, 6
+HXM_F32, HXM_BF16 = 0, 1
+ACT = {"relu": 0, "gelu": 1, "identity": 2}
+HXM_WRITE, HXM_ACCUMULATE = 0, 1
+
+
+class ShapeError(ValueError):
+    """moekit::ShapeError (reference core/include/moekit/tensor.hpp:12-15)."""
+
+
+class CacheError(RuntimeError):
+    """moekit::CacheError (reference core/include/moekit/dist_sim.hpp:55-58)."""
+
+
+class HexaMoeCudaError(RuntimeError):
+    pass
+
+
+class LayerDesc(C.Structure):
+    """hxm_layer_desc (include/hexamoe.h)."""
+    _fields_ = [("n_tokens", C.c_int64), ("n_experts", C.c_int64), ("k", C.c_int64),
+                ("d_in", C.c_int64), ("hidden", C.c_int64), ("d_out", C.c_int64),
+                ("activation", C.c_int32), ("dtype", C.c_int32), ("add_b2", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+_p = C.c_void_p
+_i64 = C.c_int64
+_sz = C.c_size_t
+
+# name -> (restype, argtypes); every symbol include/hexamoe.h declares
+SIGNATURES = {
+    "hxm_last_error": (C.c_char_p, []),
+    "hxm_version": (C.c_int, []),
+    "hxm_device_sm_count": (C.c_int, []),
+    "hxm_reindex_bound": (_sz, [_i64, _i64, _i64]),
+    "hxm_reindex_workspace_bytes": (_sz, [_i64, _i64]),
+    "hxm_build_reindex": (C.c_int, [_p, _i64, _i64, _i64, _p, _p, _p, _sz, _p, _p]),
+    "hxm_op_workspace_bytes": (_sz, [_i64, _i64, _i64, _i64, _i64]),
+    "hxm_esmm": (C.c_int, [C.c_int, _p, _i64, _i64, _p, _i64, _i64, C.c_int, _p, _p, _p, _i64,
+                           C.c_int, _p, _p, _sz, _p]),
+    "hxm_ess": (C.c_int, [C.c_int, _p, _i64, _i64, _p, _p, _i64, _i64, _p, _p, _sz, _p]),
+    "hxm_estmm": (C.c_int, [C.c_int, _p, _p, _i64, _i64, _i64, _p, _p, _i64, _i64, _p, _p, _sz,
+                            _p]),
+    "hxm_esfk": (C.c_int, [C.c_int, _p, _p, _i64, _i64, _i64, _p, C.c_int, _p, _p, _i64, _i64,
+                           _p, _p, _p, _p, _sz, _p]),
+    "hxm_layer_workspace_bytes": (_sz, [C.POINTER(LayerDesc)]),
+    "hxm_moe_forward": (C.c_int, [C.POINTER(LayerDesc), _p, _p, _p, _p, _p, _p, _p, _p, _sz, _p,
+                                  _p]),
+    "hxm_moe_backward": (C.c_int, [C.POINTER(LayerDesc), _p, _p, _p, _p, _p, _sz, _p, _p, _p, _p,
+                                   _p, _p]),
+    "hxm_moe_stash_export": (C.c_int, [C.POINTER(LayerDesc), _p, _i64, _p, _p, _p]),
+    "hxm_layer_forward_macs": (C.c_uint64, [C.POINTER(LayerDesc)]),
+    "hxm_synthesize_routing": (C.c_int, [_i64, _i64, _i64, C.c_char_p, C.c_uint64, _p]),
+    "hxm_make_layer_inputs": (None, [C.c_uint64, _i64, _i64, _i64, _i64, _i64, C.c_double, _p,
+                                     _p, _p, _p, _p]),
+    "hxm_profile_enable": (None, [C.c_int]),
+    "hxm_profile_reset": (None, []),
+    "hxm_profile_read": (C.c_int, [C.c_int, C.c_char_p, C.c_int, _p, _p, _p, _p]),
+    "hxm_launch_count": (C.c_uint64, []),
+}
+
+
+def profile_read(max_names: int = 64, name_len: int = 64):
+    """{name: (total_ms, launches, work, kind)} for regions recorded since reset."""
+    import numpy as np
+    names = C.create_string_buffer(max_names * name_len)
+    ms = np.zeros(max_names, np.float64)
+    n = np.zeros(max_names, np.int64)
+    work = np.zeros(max_names, np.float64)
+    kind = np.zeros(max_names, np.int32)
+    cnt = lib().hxm_profile_read(max_names, names, name_len, ms.ctypes.data, n.ctypes.data,
+                                 work.ctypes.data, kind.ctypes.data)
+    if cnt < 0:
+        raise HexaMoeCudaError("hxm_profile_read failed")
+    out = {}
+    raw = names.raw
+    for i in range(cnt):
+        nm = raw[i * name_len:(i + 1) * name_len].split(b"\0", 1)[0].decode()
+        out[nm] = (float(ms[i]), int(n[i]), float(work[i]), int(kind[i]))
+    return out
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libhexamoe.so.  Raises ImportError if it was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} not built: run `python -m paper_2411_01288_b200.build` "
+                "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(status: int, what: str = "") -> None:
+    if status == HXM_OK:
+        return
+    msg = lib().hxm_last_error().decode(errors="replace")
+    if what:
+        msg = f"{what}: {msg}"
+    if status == HXM_ERR_SHAPE:
+        raise ShapeError(msg)
+    if status == HXM_ERR_INVALID_ARG:
+        raise ValueError(msg)
+    if status == HXM_ERR_CACHE:
+        raise CacheError(msg)
+    raise HexaMoeCudaError(f"[status {status}] {msg}")

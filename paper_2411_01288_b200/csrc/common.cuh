@@ -1,0 +1,150 @@
+// common.cuh -- shared host/device plumbing for the hexamoe C ABI.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "../../include/hexamoe.h"
+#include "prof.cuh"
+
+namespace hxm {
+
+// ---------------------------------------------------------------- errors --
+void set_error(const std::string& msg);
+const char* last_error();
+
+struct Err {
+  hxm_status code;
+  std::string msg;
+};
+
+#define HXM_TRY_CUDA(expr)                                                   \
+  do {                                                                       \
+    cudaError_t _e = (expr);                                                 \
+    if (_e != cudaSuccess) {                                                 \
+      ::hxm::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));  \
+      return HXM_ERR_CUDA;                                                   \
+    }                                                                        \
+  } while (0)
+
+#define HXM_CHECK_LAUNCH()                                                   \
+  do {                                                                       \
+    cudaError_t _e = cudaGetLastError();                                     \
+    if (_e != cudaSuccess) {                                                 \
+      ::hxm::set_error(std::string("kernel launch: ") +                      \
+                       cudaGetErrorString(_e));                              \
+      return HXM_ERR_CUDA;                                                   \
+    }                                                                        \
+    ::hxm::note_launch();                                                    \
+  } while (0)
+
+#define HXM_RETURN_IF(st)                                                    \
+  do {                                                                       \
+    hxm_status _s = (st);                                                    \
+    if (_s != HXM_OK) return _s;                                             \
+  } while (0)
+
+inline hxm_status shape_error(const std::string& m) {
+  set_error(m);
+  return HXM_ERR_SHAPE;
+}
+inline hxm_status invalid_arg(const std::string& m) {
+  set_error(m);
+  return HXM_ERR_INVALID_ARG;
+}
+
+int sm_count();  // cached per device
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) {
+  return (a + b - 1) / b;
+}
+__host__ __device__ inline size_t align_up(size_t a, size_t b) {
+  return (a + b - 1) / b * b;
+}
+
+// Bump allocator over a caller-provided workspace (256-byte aligned slices).
+struct Arena {
+  char* base;
+  size_t cap;
+  size_t used = 0;
+  bool overflow = false;
+  Arena(void* b, size_t c) : base(static_cast<char*>(b)), cap(c) {}
+  template <class T>
+  T* take(size_t count) {
+    size_t bytes = align_up(count * sizeof(T) + 1, 256);
+    if (used + bytes > cap) overflow = true;
+    T* p = reinterpret_cast<T*>(base ? base + used : nullptr);
+    used += bytes;
+    return p;
+  }
+};
+
+// --------------------------------------------------------------- device --
+__device__ __forceinline__ float to_f32(float v) { return v; }
+__device__ __forceinline__ float to_f32(__nv_bfloat16 v) {
+  return __bfloat162float(v);
+}
+template <class T>
+__device__ __forceinline__ T from_f32(float v);
+template <>
+__device__ __forceinline__ float from_f32<float>(float v) {
+  return v;
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+
+// Activations in fp32: GELU tanh approximation and its exact derivative
+// (reference core/src/tensor.cpp:39-53), ReLU with ReLU'(0) = 0
+// (tensor.cpp:62-72), identity.
+__device__ __forceinline__ float act_value(int act, float x) {
+  if (act == HXM_ACT_RELU) return x > 0.f ? x : 0.f;
+  if (act == HXM_ACT_GELU) {
+    const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
+    return 0.5f * x * (1.f + tanhf(u));
+  }
+  return x;
+}
+__device__ __forceinline__ float act_derivative(int act, float x) {
+  if (act == HXM_ACT_RELU) return x > 0.f ? 1.f : 0.f;
+  if (act == HXM_ACT_GELU) {
+    const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
+    const float t = tanhf(u);
+    const float du = 0.7978845608028654f * (1.f + 3.f * 0.044715f * x * x);
+    return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * du;
+  }
+  return 1.f;
+}
+
+// Row maps: padded-position p -> source row (or -1 for a padding slot).
+struct MapV64 {  // reference ReIndex v (int64 token ids, -1 pads)
+  const int64_t* v;
+  __device__ __forceinline__ int operator()(int64_t p) const {
+    return static_cast<int>(v[p]);
+  }
+};
+struct MapSlot {  // combined k-choice index: slot s = choice*N + token
+  const int32_t* v;
+  int n;
+  __device__ __forceinline__ int operator()(int64_t p) const {
+    const int s = v[p];
+    return s < 0 ? -1 : s % n;
+  }
+};
+
+// Segment tile descriptor: rows [begin, end) of expert `expert` in the
+// padded position space; `flags` bit0 = expert split across several tiles
+// (ESTMM split-K), bit1 = expert segment is empty (zero output tile).
+struct SegTile {
+  int expert;
+  int begin;
+  int end;
+  int flags;
+};
+
+}  // namespace hxm

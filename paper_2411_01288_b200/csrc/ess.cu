@@ -1,0 +1,119 @@
+// ess.cu -- expert-specific segmented sum (ESS), the bias-gradient operator.
+//
+// Replaces moekit::ess (reference core/src/es_ops.cpp:86-102, 180-191):
+// out[e] = sum of the rows routed to expert e.  HBM-bound: every routed row is
+// read once (16-byte vector loads, consecutive threads on consecutive
+// columns so a gathered row is one coalesced burst) and E x D fp32 is written.
+// Two deterministic phases, no float atomics:
+//   ess_partial : one CTA per <=128-position segment tile -> partial[tile][D]
+//   ess_combine : out[e][d] = sum of e's tile partials in tile order.
+#include "kernels.cuh"
+
+namespace hxm {
+namespace {
+
+constexpr int NT = 256;
+
+template <class T, int VEC>
+__device__ __forceinline__ void load_vec(const T* p, float (&v)[VEC]) {
+  if constexpr (sizeof(T) * VEC == 16) {
+    const uint4 raw = __ldg(reinterpret_cast<const uint4*>(p));
+    const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) v[i] = to_f32(e[i]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) v[i] = to_f32(p[i]);
+  }
+}
+
+template <class T, int VEC>
+__global__ void __launch_bounds__(NT) ess_partial(EssArgs a) {
+  const int ti = blockIdx.x;
+  if (ti >= *a.n_tiles) return;
+  const SegTile tile = a.tiles[ti];
+  const T* X = static_cast<const T*>(a.x);
+  const int64_t D = a.d;
+  const int col_groups = static_cast<int>((D + VEC - 1) / VEC);
+  int ct = col_groups < NT ? col_groups : NT;   // threads along columns
+  ct = (ct + 31) / 32 * 32;
+  const int rp = NT / ct;                        // row parallelism
+  const int cid = threadIdx.x % ct, rid = threadIdx.x / ct;
+  __shared__ int rows[kEssRows];
+  __shared__ float red[NT * VEC];
+  for (int i = threadIdx.x; i < kEssRows; i += NT) {
+    const int64_t p = tile.begin + i;
+    rows[i] = p < tile.end ? a.map(p) : -1;
+  }
+  __syncthreads();
+  const int nrows = tile.end - tile.begin;
+  for (int cg0 = 0; cg0 < col_groups; cg0 += ct) {
+    const int cg = cg0 + cid;
+    float acc[VEC];
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
+    if (rid < rp && cg < col_groups) {
+      for (int r = rid; r < nrows; r += rp) {
+        const int row = rows[r];
+        if (row < 0) continue;
+        float v[VEC];
+        load_vec<T, VEC>(X + static_cast<int64_t>(row) * D + static_cast<int64_t>(cg) * VEC, v);
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) acc[i] += v[i];
+      }
+    }
+    if (rp > 1) {
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) red[threadIdx.x * VEC + i] = acc[i];
+      __syncthreads();
+      if (rid == 0) {
+        for (int q = 1; q < rp; ++q)
+#pragma unroll
+          for (int i = 0; i < VEC; ++i) acc[i] += red[(q * ct + cid) * VEC + i];
+      }
+      __syncthreads();
+    }
+    if (rid == 0 && cg < col_groups) {
+      float* dst = a.partial + static_cast<int64_t>(ti) * D + static_cast<int64_t>(cg) * VEC;
+#pragma unroll
+      for (int i = 0; i < VEC; ++i)
+        if (static_cast<int64_t>(cg) * VEC + i < D) dst[i] = acc[i];
+    }
+  }
+}
+
+__global__ void ess_combine(EssArgs a) {
+  const int e = blockIdx.y;
+  const int64_t d = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (d >= a.d) return;
+  const int t0 = a.tile_off[e], t1 = a.tile_off[e + 1];
+  float s = 0.f;
+  for (int t = t0; t < t1; ++t) s += a.partial[static_cast<int64_t>(t) * a.d + d];
+  a.out[static_cast<int64_t>(e) * a.d + d] = s;
+}
+
+template <class T>
+hxm_status launch_typed(const EssArgs& a, cudaStream_t st) {
+  constexpr int V = 16 / sizeof(T);
+  if (a.max_tiles > 0) {
+    const bool vec_ok = (a.d % V == 0) && (reinterpret_cast<uintptr_t>(a.x) % 16 == 0);
+    if (vec_ok) ess_partial<T, V><<<a.max_tiles, NT, 0, st>>>(a);
+    else ess_partial<T, 1><<<a.max_tiles, NT, 0, st>>>(a);
+    HXM_CHECK_LAUNCH();
+  }
+  dim3 grid(static_cast<unsigned>(ceil_div(a.d, 256)), static_cast<unsigned>(a.n_experts));
+  if (a.d > 0 && a.n_experts > 0) {
+    ess_combine<<<grid, 256, 0, st>>>(a);
+    HXM_CHECK_LAUNCH();
+  }
+  return HXM_OK;
+}
+
+}  // namespace
+
+hxm_status launch_ess(hxm_dtype dt, const EssArgs& a, cudaStream_t st) {
+  ProfScope ps(st, a.label ? a.label : "ess", a.work, WORK_BYTES);
+  return dt == HXM_BF16 ? launch_typed<__nv_bfloat16>(a, st) : launch_typed<float>(a, st);
+}
+
+}  // namespace hxm

@@ -1,0 +1,119 @@
+// kernels.cuh -- argument blocks and launchers of the expert-specific kernels.
+//
+// ESMM  (es_ops.cpp:47-81)   : grouped per-expert GEMM over segment tiles.
+// ESTMM (es_ops.cpp:106-128) : per-expert transposed GEMM, K = the expert's
+//                              tokens (variable), split-K over segment chunks.
+// ESS   (es_ops.cpp:86-102)  : per-expert segmented column sums.
+// bf16 runs on the tcgen05 tensor cores (umma.cu); fp32 runs on fp32 FMA
+// (simt.cu).  Both consume the same argument blocks.
+#pragma once
+#include "common.cuh"
+
+namespace hxm {
+
+// Row map: padded position p -> source/destination row, -1 = padding slot.
+enum MapKind : int { MAP_V64 = 0, MAP_SLOT = 1, MAP_DENSE = 2 };
+struct RowMap {
+  int kind;
+  int n;  // tokens per choice (MAP_SLOT)
+  const void* v;
+  __device__ __forceinline__ int operator()(int64_t p) const {
+    if (kind == MAP_V64) return static_cast<int>(static_cast<const int64_t*>(v)[p]);
+    if (kind == MAP_SLOT) {
+      const int s = static_cast<const int32_t*>(v)[p];
+      return s < 0 ? -1 : s % n;
+    }
+    return static_cast<int>(p);
+  }
+};
+inline RowMap map_v64(const int64_t* v) { return RowMap{MAP_V64, 0, v}; }
+inline RowMap map_slot(const int32_t* v, int64_t n) {
+  return RowMap{MAP_SLOT, static_cast<int>(n), v};
+}
+inline RowMap map_dense() { return RowMap{MAP_DENSE, 0, nullptr}; }
+
+enum EpiMode : int {
+  EPI_WRITE = 0,    // out_f32[omap(p)]  = acc + bias          (esmm write)
+  EPI_ACCUM = 1,    // out_f32[omap(p)] += acc + bias          (esmm accumulate)
+  EPI_ATOMIC = 2,   // red.add out_f32[omap(p)], acc (+bias)   (k-merged y, gx)
+  EPI_FWD_ACT = 3,  // out1[p] = acc + bias, out2[p] = F(.)    (stash y1, y2)
+  EPI_BWD_ACT = 4   // out1[p] = acc * F'(y1s[p])              (g_y1)
+};
+
+struct EsmmArgs {
+  const char* label;  // profiling region name (nullable)
+  double work;        // algorithmic FLOP (GEMMs) or bytes (ESS) of the launch
+  const void* a;  // A rows, K = d1 columns
+  RowMap amap;
+  const void* w;  // w_trans == 0: E x d1 x d2 ; 1: E x d2 x d1 (use W^T)
+  int w_trans;
+  int64_t d1, d2;
+  const float* bias;  // E x d2 or null
+  const SegTile* tiles;
+  const int32_t* n_tiles;
+  int max_tiles;
+  int tile_rows;  // rows per segment tile (kSimtRows or kUmmaRows)
+  int epi;
+  int act;
+  float* out_f32;  // WRITE / ACCUM / ATOMIC destination, rows via omap
+  RowMap omap;     // scatter map, or the pad-detection map for dense outputs
+  void* out1;      // FWD_ACT / BWD_ACT dense outputs (dtype), row stride d2
+  void* out2;
+  const void* y1s;  // BWD_ACT: pre-activation stash (dtype), row stride d2
+};
+
+struct EstmmArgs {
+  const char* label;  // profiling region name (nullable)
+  double work;        // algorithmic FLOP (GEMMs) or bytes (ESS) of the launch
+  const void* x1;  // rows via m1, d1 columns
+  RowMap m1;
+  const void* x2;  // rows via m2, d2 columns
+  RowMap m2;
+  int64_t d1, d2;
+  const SegTile* tiles;  // K chunks (split flag / empty flag)
+  const int32_t* n_tiles;
+  int max_tiles;
+  int n_experts;
+  float* out;  // E x d1 x d2
+};
+
+struct EssArgs {
+  const char* label;  // profiling region name (nullable)
+  double work;        // algorithmic FLOP (GEMMs) or bytes (ESS) of the launch
+  const void* x;
+  RowMap map;
+  int64_t d;
+  const SegTile* tiles;  // <= kEssRows positions each
+  const int32_t* n_tiles;
+  const int32_t* tile_off;  // E+1
+  int max_tiles;
+  int n_experts;
+  float* partial;  // max_tiles x d
+  float* out;      // E x d
+};
+
+constexpr int kEssRows = 128;
+constexpr int kSimtRows = 64;     // SIMT ESMM tile rows
+constexpr int kUmmaRows = 128;    // tcgen05 ESMM tile rows (UMMA M)
+constexpr int kEstmmChunk = 2048; // ESTMM split-K chunk (positions)
+
+hxm_status launch_esmm(hxm_dtype dt, const EsmmArgs& a, cudaStream_t st);
+hxm_status launch_estmm(hxm_dtype dt, const EstmmArgs& a, cudaStream_t st);
+hxm_status launch_ess(hxm_dtype dt, const EssArgs& a, cudaStream_t st);
+
+// fp32 FMA kernels (simt.cu)
+hxm_status simt_esmm(hxm_dtype dt, const EsmmArgs& a, cudaStream_t st);
+hxm_status simt_estmm(hxm_dtype dt, const EstmmArgs& a, cudaStream_t st);
+// tcgen05 kernels (umma.cu); return HXM_ERR_UNSUPPORTED for shapes they
+// do not cover (d1/d2 not multiples of 64), which the caller reports.
+hxm_status umma_esmm(const EsmmArgs& a, cudaStream_t st);
+hxm_status umma_estmm(const EstmmArgs& a, cudaStream_t st);
+bool umma_supports_esmm(int64_t d1, int64_t d2);
+bool umma_supports_estmm(int64_t d1, int64_t d2);
+
+// zero out[e] for experts whose ESTMM is split over several chunks
+hxm_status zero_split_experts(const SegTile* tiles, const int32_t* n_tiles,
+                              int max_tiles, int64_t slice, float* out,
+                              cudaStream_t st);
+
+}  // namespace hxm

@@ -1,0 +1,359 @@
+// layer.cu -- MoE layer forward / backward on the device.
+//
+// Replaces moekit::moe_forward / moe_backward (reference
+// core/src/moe_layer.cpp:30-122).  Semantics kept exactly:
+//   y      = sum_i ESMM(F(ESMM(x, W1, b1, R_i)), W2, b2, R_i)   (b2 once per choice)
+//   gb2    = sum_i ESS(g_y, R_i)             gW2 = sum_i ESTMM(y2_i, g_y, R_i)
+//   g_y2_i = ESMM(g_y, W2^T, R_i)            g_y1_i = g_y2_i * F'(y1_i)
+//   gb1    = sum_i ESS(g_y1_i, R_i)          gW1 = sum_i ESTMM(x, g_y1_i, R_i)
+//   gx     = sum_i ESMM(g_y1_i, W1^T, R_i)
+// B200-first changes (not a transliteration):
+//  * the k choices share ONE expert-grouped index over k*N (token, choice)
+//    slots (hxm::build_reindex_slots), so each expert's weights are streamed
+//    once per layer and every GEMM is one launch;
+//  * the stash y1/y2 and g_y1 live in expert-sorted row order (padded to 64
+//    positions per expert, pads written as zero rows), so only x and g_y --
+//    which arrive in token order -- are gathered; the sorted operands are
+//    read with dense tiles;
+//  * W^T is never materialised (transpose_experts, moe_layer.cpp:91-92): the
+//    GEMM reads W K-major;
+//  * y and gx accumulate over choices with fp32 reductions into zeroed
+//    buffers (the memory-efficient scheme, moe_layer.cpp:61-63).
+#include "kernels.cuh"
+#include "routing.cuh"
+
+namespace hxm {
+
+int esmm_tile_rows(hxm_dtype dt, int64_t d1, int64_t d2);
+
+namespace {
+
+constexpr int64_t kSortedBlk = 64;  // internal segment padding (UMMA K-step)
+
+struct LayerWs {
+  int32_t* v;     // combined index, slot ids
+  int32_t* idx;   // E+1
+  void* rws;      // reindex scratch
+  size_t rws_bytes;
+  SegTile* tiles_a;  // ESMM tiles over in=D_i (both GEMMs share rows)
+  int32_t* tiles_a_off;
+  int32_t* n_tiles_a;
+  SegTile* ktiles;  // ESTMM chunks
+  int32_t* ktiles_off;
+  int32_t* n_ktiles;
+  SegTile* etiles;  // ESS tiles
+  int32_t* etiles_off;
+  int32_t* n_etiles;
+  float* partial;
+  void* y1s;
+  void* y2s;
+  void* g1s;
+  int64_t bound;
+  int max_tiles_a, max_ktiles, max_etiles;
+  int rows_a;
+};
+
+size_t esize(int32_t dt) { return dt == HXM_BF16 ? 2 : 4; }
+
+LayerWs carve(Arena& ar, const hxm_layer_desc& d) {
+  LayerWs w{};
+  const int64_t slots = d.k * d.n_tokens;
+  w.bound = slots + d.n_experts * (kSortedBlk - 1);
+  const hxm_dtype dt = static_cast<hxm_dtype>(d.dtype);
+  // all four layer GEMMs share one tile table, so they must agree on the
+  // tile rows: 128 (tcgen05) when every shape is TMA-describable
+  const bool umma = dt == HXM_BF16 && umma_supports_esmm(d.d_in, d.hidden) &&
+                    umma_supports_esmm(d.hidden, d.d_out) &&
+                    umma_supports_esmm(d.d_out, d.hidden) &&
+                    umma_supports_esmm(d.hidden, d.d_in);
+  w.rows_a = umma ? kUmmaRows : kSimtRows;
+  w.v = ar.take<int32_t>(w.bound);
+  w.idx = ar.take<int32_t>(d.n_experts + 1);
+  w.rws_bytes = reindex_ws_bytes(slots, d.n_experts);
+  w.rws = ar.take<char>(w.rws_bytes);
+  w.max_tiles_a = static_cast<int>(max_tiles(w.bound, d.n_experts, kSimtRows));
+  w.tiles_a = ar.take<SegTile>(w.max_tiles_a);
+  w.tiles_a_off = ar.take<int32_t>(d.n_experts + 1);
+  w.n_tiles_a = ar.take<int32_t>(1);
+  w.max_ktiles = static_cast<int>(max_tiles(w.bound, d.n_experts, kEstmmChunk));
+  w.ktiles = ar.take<SegTile>(w.max_ktiles);
+  w.ktiles_off = ar.take<int32_t>(d.n_experts + 1);
+  w.n_ktiles = ar.take<int32_t>(1);
+  w.max_etiles = static_cast<int>(max_tiles(w.bound, d.n_experts, kEssRows));
+  w.etiles = ar.take<SegTile>(w.max_etiles);
+  w.etiles_off = ar.take<int32_t>(d.n_experts + 1);
+  w.n_etiles = ar.take<int32_t>(1);
+  w.partial = ar.take<float>(static_cast<size_t>(w.max_etiles) * std::max(d.hidden, d.d_out));
+  const size_t stash = static_cast<size_t>(w.bound) * d.hidden * esize(d.dtype);
+  w.y1s = ar.take<char>(stash);
+  w.y2s = ar.take<char>(stash);
+  w.g1s = ar.take<char>(stash);
+  return w;
+}
+
+hxm_status check_desc(const hxm_layer_desc* d) {
+  if (!d) return invalid_arg("moe layer: null descriptor");
+  if (d->dtype != HXM_F32 && d->dtype != HXM_BF16) return invalid_arg("moe layer: unknown dtype");
+  if (d->activation < 0 || d->activation > 2) return invalid_arg("moe layer: unknown activation");
+  if (d->k < 1) return shape_error("RoutingChoice: expected k assignment vectors");
+  if (d->k > d->n_experts) return invalid_arg("RoutingChoice: k exceeds expert count");
+  if (d->n_tokens < 0 || d->d_in < 1 || d->hidden < 1 || d->d_out < 1)
+    return shape_error("moe layer: extents must be positive");
+  if (d->k * d->n_tokens + d->n_experts * kSortedBlk > 0x7fffffffLL)
+    return invalid_arg("moe layer: k*N exceeds int32 slot range");
+  return HXM_OK;
+}
+
+// Reference moe_layer.cpp:33-43 validates before any work; per-token
+// distinctness of the k choices (routing.cpp:30-39) is data-dependent and
+// checked on the device.
+__global__ void check_distinct(const int32_t* a, int64_t n, int k, int E, int32_t* status) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    for (int i = 0; i < k; ++i) {
+      const int ei = a[i * n + t];
+      if (ei < 0 || ei >= E) {
+        atomicExch(status, HXM_ERR_INVALID_ARG);
+        continue;
+      }
+      for (int j = i + 1; j < k; ++j)
+        if (a[j * n + t] == ei) atomicExch(status, HXM_ERR_INVALID_ARG);
+    }
+  }
+}
+
+// stash export: sorted row p (slot s = choice*N + t) -> token-order fp32
+template <class T>
+__global__ void export_kernel(const int32_t* v, const int32_t* idx, int E, int64_t n,
+                              int choice, int64_t H, const T* y1s, const T* y2s, float* y1,
+                              float* y2) {
+  const int64_t np = idx[E];
+  for (int64_t p = blockIdx.x; p < np; p += gridDim.x) {
+    const int s = v[p];
+    if (s < 0 || s / n != choice) continue;
+    const int64_t t = s % n;
+    for (int64_t h = threadIdx.x; h < H; h += blockDim.x) {
+      y1[t * H + h] = to_f32(y1s[p * H + h]);
+      y2[t * H + h] = to_f32(y2s[p * H + h]);
+    }
+  }
+}
+
+}  // namespace
+}  // namespace hxm
+
+using namespace hxm;
+
+extern "C" {
+
+size_t hxm_layer_workspace_bytes(const hxm_layer_desc* d) {
+  if (check_desc(d) != HXM_OK) return 0;
+  Arena ar(nullptr, 0);
+  carve(ar, *d);
+  return ar.used;
+}
+
+uint64_t hxm_layer_forward_macs(const hxm_layer_desc* d) {
+  return static_cast<uint64_t>(d->k) * d->n_tokens *
+         (d->d_in * d->hidden + d->hidden * d->d_out);
+}
+
+hxm_status hxm_moe_forward(const hxm_layer_desc* d, const void* x, const void* w1,
+                           const float* b1, const void* w2, const float* b2,
+                           const int32_t* assignments, float* y, void* ws, size_t ws_bytes,
+                           int32_t* status, hxm_stream_t stream) {
+  HXM_RETURN_IF(check_desc(d));
+  if (!x || !w1 || !b1 || !w2 || (d->add_b2 && !b2) || !assignments || !y)
+    return invalid_arg("moe_forward: null tensor");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Arena ar(ws, ws_bytes);
+  LayerWs w = carve(ar, *d);
+  if (ar.overflow) return invalid_arg("moe_forward: workspace too small");
+  const hxm_dtype dt = static_cast<hxm_dtype>(d->dtype);
+  const int64_t N = d->n_tokens, E = d->n_experts, slots = d->k * N;
+  HXM_TRY_CUDA(cudaMemsetAsync(y, 0, sizeof(float) * N * d->d_out, st));
+  if (status && N > 0 && d->k > 1) {
+    check_distinct<<<std::max<int64_t>(1, std::min<int64_t>(1024, ceil_div(N, 256))), 256, 0,
+                     st>>>(assignments, N, static_cast<int>(d->k), static_cast<int>(E), status);
+    HXM_CHECK_LAUNCH();
+  }
+  HXM_RETURN_IF(build_reindex_slots(assignments, slots, E, kSortedBlk, w.v, w.idx, w.rws,
+                                    w.rws_bytes, status, st));
+  HXM_RETURN_IF(launch_tiles<int32_t>(w.idx, E, w.rows_a, false, w.tiles_a, w.tiles_a_off,
+                                      w.n_tiles_a, st));
+  if (N == 0) return HXM_OK;
+  const RowMap slot = map_slot(w.v, N);
+  // (1) y1 = x W1 + b1 ; y2 = F(y1)          (moe_layer.cpp:56-57)
+  EsmmArgs a1{};
+  a1.a = x;
+  a1.amap = slot;
+  a1.w = w1;
+  a1.w_trans = 0;
+  a1.d1 = d->d_in;
+  a1.d2 = d->hidden;
+  a1.bias = b1;
+  a1.tiles = w.tiles_a;
+  a1.n_tiles = w.n_tiles_a;
+  a1.max_tiles = static_cast<int>(max_tiles(w.bound, E, w.rows_a));
+  a1.tile_rows = w.rows_a;
+  a1.epi = EPI_FWD_ACT;
+  const double kn = static_cast<double>(slots);
+  a1.label = "esmm_fwd1";
+  a1.work = 2.0 * kn * d->d_in * d->hidden;
+  a1.act = d->activation;
+  a1.omap = slot;
+  a1.out1 = w.y1s;
+  a1.out2 = w.y2s;
+  HXM_RETURN_IF(launch_esmm(dt, a1, st));
+  // (2) y += y2 W2 + b2 over all choices     (moe_layer.cpp:61-63)
+  EsmmArgs a2 = a1;
+  a2.a = w.y2s;
+  a2.amap = map_dense();
+  a2.w = w2;
+  a2.d1 = d->hidden;
+  a2.d2 = d->d_out;
+  a2.bias = d->add_b2 ? b2 : nullptr;
+  a2.epi = EPI_ATOMIC;
+  a2.label = "esmm_fwd2";
+  a2.work = 2.0 * kn * d->hidden * d->d_out;
+  a2.out_f32 = y;
+  a2.omap = slot;
+  a2.out1 = a2.out2 = nullptr;
+  return launch_esmm(dt, a2, st);
+}
+
+hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* w1,
+                            const void* w2, const void* g_y, void* ws, size_t ws_bytes,
+                            float* gw1, float* gb1, float* gw2, float* gb2, float* gx,
+                            hxm_stream_t stream) {
+  HXM_RETURN_IF(check_desc(d));
+  if (!x || !w1 || !w2 || !g_y || !gw1 || !gb1 || !gw2 || (d->add_b2 && !gb2) || !gx)
+    return invalid_arg("moe_backward: null tensor");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Arena ar(ws, ws_bytes);
+  LayerWs w = carve(ar, *d);
+  if (ar.overflow) return invalid_arg("moe_backward: workspace too small");
+  const hxm_dtype dt = static_cast<hxm_dtype>(d->dtype);
+  const int64_t N = d->n_tokens, E = d->n_experts;
+  const int64_t Di = d->d_in, H = d->hidden, Do = d->d_out;
+  HXM_TRY_CUDA(cudaMemsetAsync(gx, 0, sizeof(float) * N * Di, st));
+  HXM_RETURN_IF(launch_tiles<int32_t>(w.idx, E, kEstmmChunk, true, w.ktiles, w.ktiles_off,
+                                      w.n_ktiles, st));
+  HXM_RETURN_IF(launch_tiles<int32_t>(w.idx, E, kEssRows, false, w.etiles, w.etiles_off,
+                                      w.n_etiles, st));
+  const RowMap slot = map_slot(w.v, N > 0 ? N : 1);
+  // (4) gb2 = sum_i ESS(g_y, R_i)             (moe_layer.cpp:103)
+  EssArgs es{};
+  es.x = g_y;
+  es.map = slot;
+  es.d = Do;
+  es.tiles = w.etiles;
+  es.n_tiles = w.n_etiles;
+  es.tile_off = w.etiles_off;
+  es.max_tiles = w.max_etiles;
+  es.n_experts = static_cast<int>(E);
+  es.partial = w.partial;
+  es.out = gb2;
+  const double kn = static_cast<double>(d->k * N);
+  const double esz = static_cast<double>(esize(d->dtype));
+  es.label = "ess_gb2";
+  es.work = kn * Do * esz + static_cast<double>(E) * Do * 4.0;
+  if (d->add_b2) HXM_RETURN_IF(launch_ess(dt, es, st));
+  // (5) gW2 = sum_i ESTMM(y2_i, g_y, R_i)     (moe_layer.cpp:104)
+  EstmmArgs t2{};
+  t2.x1 = w.y2s;
+  t2.m1 = map_dense();
+  t2.x2 = g_y;
+  t2.m2 = slot;
+  t2.d1 = H;
+  t2.d2 = Do;
+  t2.tiles = w.ktiles;
+  t2.n_tiles = w.n_ktiles;
+  t2.max_tiles = w.max_ktiles;
+  t2.n_experts = static_cast<int>(E);
+  t2.out = gw2;
+  t2.label = "estmm_gw2";
+  t2.work = 2.0 * kn * H * Do;
+  HXM_RETURN_IF(launch_estmm(dt, t2, st));
+  // (6,7) g_y1 = (g_y W2^T) * F'(y1)          (moe_layer.cpp:105-108)
+  EsmmArgs b6{};
+  b6.a = g_y;
+  b6.amap = slot;
+  b6.w = w2;
+  b6.w_trans = 1;  // W2 is E x H x Do; use W2[e]^T (Do x H)
+  b6.d1 = Do;
+  b6.d2 = H;
+  b6.tiles = w.tiles_a;
+  b6.n_tiles = w.n_tiles_a;
+  b6.max_tiles = static_cast<int>(max_tiles(w.bound, E, w.rows_a));
+  b6.tile_rows = w.rows_a;
+  b6.epi = EPI_BWD_ACT;
+  b6.label = "esmm_bwd_act";
+  b6.work = 2.0 * kn * Do * H;
+  b6.act = d->activation;
+  b6.omap = slot;
+  b6.out1 = w.g1s;
+  b6.y1s = w.y1s;
+  HXM_RETURN_IF(launch_esmm(dt, b6, st));
+  // (8) gb1 = sum_i ESS(g_y1_i, R_i)          (moe_layer.cpp:116)
+  es.x = w.g1s;
+  es.map = map_dense();
+  es.d = H;
+  es.out = gb1;
+  es.label = "ess_gb1";
+  es.work = kn * H * esz + static_cast<double>(E) * H * 4.0;
+  HXM_RETURN_IF(launch_ess(dt, es, st));
+  // (9) gW1 = sum_i ESTMM(x, g_y1_i, R_i)     (moe_layer.cpp:117)
+  EstmmArgs t1 = t2;
+  t1.x1 = x;
+  t1.m1 = slot;
+  t1.x2 = w.g1s;
+  t1.m2 = map_dense();
+  t1.d1 = Di;
+  t1.d2 = H;
+  t1.out = gw1;
+  t1.label = "estmm_gw1";
+  t1.work = 2.0 * kn * Di * H;
+  HXM_RETURN_IF(launch_estmm(dt, t1, st));
+  // (10) gx += g_y1_i W1^T                    (moe_layer.cpp:118)
+  EsmmArgs b10 = b6;
+  b10.a = w.g1s;
+  b10.amap = map_dense();
+  b10.w = w1;
+  b10.w_trans = 1;  // W1 is E x Di x H; use W1[e]^T (H x Di)
+  b10.d1 = H;
+  b10.d2 = Di;
+  b10.epi = EPI_ATOMIC;
+  b10.label = "esmm_bwd_gx";
+  b10.work = 2.0 * kn * H * Di;
+  b10.out_f32 = gx;
+  b10.out1 = nullptr;
+  b10.y1s = nullptr;
+  return launch_esmm(dt, b10, st);
+}
+
+hxm_status hxm_moe_stash_export(const hxm_layer_desc* d, const void* ws, int64_t choice,
+                                float* y1, float* y2, hxm_stream_t stream) {
+  HXM_RETURN_IF(check_desc(d));
+  if (choice < 0 || choice >= d->k) return invalid_arg("stash_export: choice out of range");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Arena ar(const_cast<void*>(ws), SIZE_MAX);
+  LayerWs w = carve(ar, *d);
+  const int64_t N = d->n_tokens;
+  if (N == 0) return HXM_OK;
+  const int grid = static_cast<int>(std::min<int64_t>(4096, w.bound));
+  if (d->dtype == HXM_BF16)
+    export_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
+        w.v, w.idx, static_cast<int>(d->n_experts), N, static_cast<int>(choice), d->hidden,
+        static_cast<const __nv_bfloat16*>(w.y1s), static_cast<const __nv_bfloat16*>(w.y2s), y1,
+        y2);
+  else
+    export_kernel<float><<<grid, 256, 0, st>>>(w.v, w.idx, static_cast<int>(d->n_experts), N,
+                                               static_cast<int>(choice), d->hidden,
+                                               static_cast<const float*>(w.y1s),
+                                               static_cast<const float*>(w.y2s), y1, y2);
+  HXM_CHECK_LAUNCH();
+  return HXM_OK;
+}
+
+}  // extern "C"

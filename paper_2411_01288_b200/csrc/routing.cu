@@ -1,0 +1,303 @@
+// routing.cu -- device routing-index build and segment tilers.
+//
+// Replaces moekit::build_reindex (reference core/src/routing.cpp:42-70):
+//   count[e]  -> ceil-to-blk padding -> exclusive scan (idx) -> -1 fill ->
+//   stable, in-token-order placement with per-expert cursors.
+// The GPU version is bit-exact with it.  Tokens are cut into fixed chunks of
+// CHUNK consecutive tokens, one warp per chunk:
+//   K1 count_chunks   : per-chunk expert histograms (smem, per warp)
+//   K2 scan_experts   : per expert, exclusive scan of its chunk counts
+//   K3 scatter        : idx (all blocks recompute it in smem; block 0 stores),
+//                       -1 padding, and each warp places its chunk in token
+//                       order: __match_any_sync gives the in-warp rank among
+//                       equal experts, so the order inside a segment is the
+//                       token order exactly as the reference's cursor loop.
+// Traffic is read 4 B/token + write 8 B/slot: it is launch/latency bound at
+// every BASELINE.json size.
+#include <cub/block/block_scan.cuh>
+
+#include "common.cuh"
+#include "routing.cuh"
+
+namespace hxm {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+__global__ void count_chunks(const int32_t* __restrict__ a, int64_t n, int E,
+                             int chunk, int nchunks, int32_t* __restrict__ cnt,
+                             int32_t* status) {
+  extern __shared__ int32_t hist[];  // [kWarps][E]
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  int32_t* h = hist + warp * E;
+  for (int e = lane; e < E; e += 32) h[e] = 0;
+  __syncwarp();
+  const int c = blockIdx.x * kWarps + warp;
+  if (c < nchunks) {
+    const int64_t t0 = static_cast<int64_t>(c) * chunk;
+    const int64_t t1 = min(n, t0 + chunk);
+    for (int64_t t = t0 + lane; t < t1; t += 32) {
+      const int e = a[t];
+      if (e < 0 || e >= E) {
+        if (status) atomicExch(status, HXM_ERR_INVALID_ARG);
+        continue;
+      }
+      atomicAdd(&h[e], 1);
+    }
+    __syncwarp();
+    for (int e = lane; e < E; e += 32) cnt[static_cast<int64_t>(c) * E + e] = h[e];
+  }
+}
+
+// One block per expert: base[c][e] = sum_{c' < c} cnt[c'][e]; total[e].
+__global__ void scan_experts(const int32_t* __restrict__ cnt, int E, int nchunks,
+                             int32_t* __restrict__ base, int32_t* __restrict__ total) {
+  using Scan = cub::BlockScan<int32_t, kThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int32_t carry;
+  const int e = blockIdx.x;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int c0 = 0; c0 < nchunks; c0 += kThreads) {
+    const int c = c0 + threadIdx.x;
+    int32_t val = c < nchunks ? cnt[static_cast<int64_t>(c) * E + e] : 0;
+    int32_t excl, agg;
+    Scan(tmp).ExclusiveSum(val, excl, agg);
+    if (c < nchunks) base[static_cast<int64_t>(c) * E + e] = carry + excl;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += agg;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) total[e] = carry;
+}
+
+// Exclusive scan of padded segment sizes into smem idx[0..E].
+template <class IdxT>
+__device__ void block_idx(const int32_t* __restrict__ total, int E, int64_t blk,
+                          IdxT* sidx) {
+  using Scan = cub::BlockScan<int64_t, kThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int e0 = 0; e0 < E; e0 += kThreads) {
+    const int e = e0 + threadIdx.x;
+    int64_t padded = 0;
+    if (e < E) padded = blk * ((static_cast<int64_t>(total[e]) + blk - 1) / blk);
+    int64_t excl, agg;
+    Scan(tmp).ExclusiveSum(padded, excl, agg);
+    if (e < E) sidx[e] = static_cast<IdxT>(carry + excl);
+    __syncthreads();
+    if (threadIdx.x == 0) carry += agg;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) sidx[E] = static_cast<IdxT>(carry);
+  __syncthreads();
+}
+
+// value written into v for token t of the (flattened) assignment:
+// reference API -> t itself; combined k-choice index -> slot id t (the
+// assignment array is k x N row-major, so the flat position IS the slot).
+template <class IdxT, class VT>
+__global__ void scatter(const int32_t* __restrict__ a, int64_t n, int E,
+                        int64_t blk, int chunk, int nchunks,
+                        const int32_t* __restrict__ base,
+                        const int32_t* __restrict__ total, VT* __restrict__ v,
+                        IdxT* __restrict__ idx_out) {
+  extern __shared__ unsigned char smem_raw[];
+  IdxT* sidx = reinterpret_cast<IdxT*>(smem_raw);                     // E+1
+  int64_t* cursor = reinterpret_cast<int64_t*>(
+      smem_raw + align_up((E + 1) * sizeof(IdxT), 16));             // [kWarps][E]
+  block_idx<IdxT>(total, E, blk, sidx);
+  if (blockIdx.x == 0) {
+    for (int e = threadIdx.x; e <= E; e += kThreads) idx_out[e] = sidx[e];
+  }
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // -1 padding of segment tails (routing.cpp:62)
+  for (int e = blockIdx.x * kWarps + warp; e < E; e += gridDim.x * kWarps) {
+    const int64_t s0 = static_cast<int64_t>(sidx[e]) + total[e];
+    const int64_t s1 = sidx[e + 1];
+    for (int64_t p = s0 + lane; p < s1; p += 32) v[p] = static_cast<VT>(-1);
+  }
+  const int c = blockIdx.x * kWarps + warp;
+  if (c >= nchunks) return;
+  int64_t* cur = cursor + static_cast<int64_t>(warp) * E;
+  for (int e = lane; e < E; e += 32)
+    cur[e] = static_cast<int64_t>(sidx[e]) + base[static_cast<int64_t>(c) * E + e];
+  __syncwarp();
+  const int64_t t0 = static_cast<int64_t>(c) * chunk;
+  const int64_t t1 = min(n, t0 + chunk);
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t tb = t0; tb < t1; tb += 32) {
+    const int64_t t = tb + lane;
+    const bool live = t < t1;
+    int e = live ? a[t] : -1;
+    if (e >= E) e = -1;  // out of range: reported by count_chunks, skipped
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    if (e >= 0) {
+      const int64_t pos = cur[e] + __popc(peers & lt);
+      v[pos] = static_cast<VT>(t);
+    }
+    __syncwarp();
+    if (e >= 0 && (__ffs(peers) - 1) == lane) cur[e] += __popc(peers);
+    __syncwarp();
+  }
+}
+
+int pick_chunk(int64_t n) {
+  // at most ~1024 chunks so K2's per-expert scan stays short
+  int64_t c = 256;
+  while (ceil_div(n, c) > 1024) c *= 2;
+  return static_cast<int>(c);
+}
+
+template <class IdxT, class VT>
+hxm_status build_impl(const int32_t* a, int64_t n, int64_t E, int64_t blk,
+                      VT* v, IdxT* idx, void* ws, size_t ws_bytes,
+                      int32_t* status, cudaStream_t st) {
+  const int chunk = pick_chunk(n);
+  const int nchunks = static_cast<int>(ceil_div(n, chunk));
+  Arena ar(ws, ws_bytes);
+  int32_t* cnt = ar.take<int32_t>(static_cast<size_t>(nchunks) * E + 1);
+  int32_t* base = ar.take<int32_t>(static_cast<size_t>(nchunks) * E + 1);
+  int32_t* total = ar.take<int32_t>(E + 1);
+  if (ar.overflow) return invalid_arg("build_reindex: workspace too small");
+  const int blocks = static_cast<int>(std::max<int64_t>(1, ceil_div(nchunks, kWarps)));
+  const size_t hist_smem = static_cast<size_t>(kWarps) * E * sizeof(int32_t);
+  if (nchunks > 0) {
+    count_chunks<<<blocks, kThreads, hist_smem, st>>>(a, n, static_cast<int>(E), chunk,
+                                                      nchunks, cnt, status);
+    HXM_CHECK_LAUNCH();
+  }
+  scan_experts<<<static_cast<int>(E), kThreads, 0, st>>>(cnt, static_cast<int>(E),
+                                                         nchunks, base, total);
+  HXM_CHECK_LAUNCH();
+  const size_t sc_smem = align_up((E + 1) * sizeof(IdxT), 16) +
+                         static_cast<size_t>(kWarps) * E * sizeof(int64_t);
+  if (sc_smem > 48 * 1024) {
+    HXM_TRY_CUDA(cudaFuncSetAttribute(scatter<IdxT, VT>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(sc_smem)));
+  }
+  scatter<IdxT, VT><<<blocks, kThreads, sc_smem, st>>>(a, n, static_cast<int>(E), blk,
+                                                        chunk, nchunks, base, total,
+                                                        v, idx);
+  HXM_CHECK_LAUNCH();
+  return HXM_OK;
+}
+
+// ----------------------------------------------------------- tilers -----
+// tiles of at most `rows` positions per expert segment; min_one: experts
+// with an empty segment still get one (empty) tile -- used by ESTMM so that
+// their zero gradient is written (es_ops.cpp:202 zero-initialised output).
+template <class IdxT>
+__global__ void build_tiles(const IdxT* __restrict__ idx, int E, int rows,
+                            int min_one, SegTile* __restrict__ tiles,
+                            int32_t* __restrict__ tile_off,
+                            int32_t* __restrict__ n_tiles) {
+  using Scan = cub::BlockScan<int32_t, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int e0 = 0; e0 < E; e0 += 1024) {
+    const int e = e0 + threadIdx.x;
+    int32_t nt = 0;
+    int64_t b = 0, len = 0;
+    if (e < E) {
+      b = idx[e];
+      len = static_cast<int64_t>(idx[e + 1]) - b;
+      nt = static_cast<int32_t>((len + rows - 1) / rows);
+      if (nt == 0 && min_one) nt = 1;
+    }
+    int32_t excl, agg;
+    Scan(tmp).ExclusiveSum(nt, excl, agg);
+    if (e < E) {
+      const int32_t off = carry + excl;
+      tile_off[e] = off;
+      const int split = nt > 1 ? 1 : 0;
+      const int empty = len == 0 ? 2 : 0;
+      for (int j = 0; j < nt; ++j) {
+        SegTile t;
+        t.expert = e;
+        t.begin = static_cast<int>(b + static_cast<int64_t>(j) * rows);
+        const int64_t hi = b + static_cast<int64_t>(j + 1) * rows;
+        t.end = static_cast<int>(hi < b + len ? hi : b + len);
+        if (len == 0) t.end = t.begin;
+        t.flags = split | empty;
+        tiles[off + j] = t;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += agg;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    tile_off[E] = carry;
+    *n_tiles = carry;
+  }
+}
+
+}  // namespace
+
+size_t reindex_ws_bytes(int64_t n, int64_t E) {
+  const int chunk = pick_chunk(n);
+  const int64_t nchunks = ceil_div(n, chunk);
+  Arena ar(nullptr, 0);
+  ar.take<int32_t>(static_cast<size_t>(nchunks) * E + 1);
+  ar.take<int32_t>(static_cast<size_t>(nchunks) * E + 1);
+  ar.take<int32_t>(E + 1);
+  return ar.used;
+}
+
+hxm_status build_reindex_slots(const int32_t* a, int64_t n_slots, int64_t E,
+                               int64_t blk, int32_t* v, int32_t* idx, void* ws,
+                               size_t ws_bytes, int32_t* status, cudaStream_t st) {
+  return build_impl<int32_t, int32_t>(a, n_slots, E, blk, v, idx, ws, ws_bytes, status, st);
+}
+
+template <class IdxT>
+hxm_status launch_tiles(const IdxT* idx, int64_t E, int rows, bool min_one,
+                        SegTile* tiles, int32_t* tile_off, int32_t* n_tiles,
+                        cudaStream_t st) {
+  build_tiles<IdxT><<<1, 1024, 0, st>>>(idx, static_cast<int>(E), rows, min_one ? 1 : 0,
+                                        tiles, tile_off, n_tiles);
+  HXM_CHECK_LAUNCH();
+  return HXM_OK;
+}
+template hxm_status launch_tiles<int32_t>(const int32_t*, int64_t, int, bool, SegTile*,
+                                          int32_t*, int32_t*, cudaStream_t);
+template hxm_status launch_tiles<int64_t>(const int64_t*, int64_t, int, bool, SegTile*,
+                                          int32_t*, int32_t*, cudaStream_t);
+
+int64_t max_tiles(int64_t n_padded_bound, int64_t E, int rows) {
+  return ceil_div(n_padded_bound, rows) + E + 1;
+}
+
+}  // namespace hxm
+
+extern "C" {
+
+size_t hxm_reindex_bound(int64_t n, int64_t E, int64_t blk) {
+  if (n < 0 || E < 0) return 0;
+  return static_cast<size_t>(n + E * (blk > 0 ? blk - 1 : 0));
+}
+
+size_t hxm_reindex_workspace_bytes(int64_t n, int64_t E) {
+  return hxm::reindex_ws_bytes(n, E);
+}
+
+hxm_status hxm_build_reindex(const int32_t* a, int64_t n, int64_t E, int64_t blk,
+                             int64_t* v, int64_t* idx, void* ws, size_t ws_bytes,
+                             int32_t* status, hxm_stream_t stream) {
+  // routing.cpp:44 -- checked before any device work
+  if (blk <= 0) return hxm::invalid_arg("build_reindex: blk must be >= 1");
+  if (n < 0 || E <= 0) return hxm::invalid_arg("build_reindex: need n >= 0 and E >= 1");
+  if (n > 0x7fffffffLL) return hxm::invalid_arg("build_reindex: n exceeds int32 range");
+  return hxm::build_impl<int64_t, int64_t>(a, n, E, blk, v, idx, ws, ws_bytes, status,
+                                           reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,24 @@
+// routing.cuh -- internal routing / tiling entry points (see routing.cu).
+#pragma once
+#include "common.cuh"
+
+namespace hxm {
+
+size_t reindex_ws_bytes(int64_t n, int64_t E);
+
+// Combined k-choice index: `a` is the k x N assignment matrix viewed as k*N
+// slots; v receives slot ids grouped by expert (choice-major, token-ascending
+// inside a segment), segments padded with -1 to a multiple of blk.
+hxm_status build_reindex_slots(const int32_t* a, int64_t n_slots, int64_t E,
+                               int64_t blk, int32_t* v, int32_t* idx, void* ws,
+                               size_t ws_bytes, int32_t* status, cudaStream_t st);
+
+// Cut every expert segment [idx[e], idx[e+1]) into tiles of <= rows positions.
+template <class IdxT>
+hxm_status launch_tiles(const IdxT* idx, int64_t E, int rows, bool min_one,
+                        SegTile* tiles, int32_t* tile_off, int32_t* n_tiles,
+                        cudaStream_t st);
+
+int64_t max_tiles(int64_t n_padded_bound, int64_t E, int rows);
+
+}  // namespace hxm

@@ -1,0 +1,61 @@
+"""LayerRunner: a preallocated, low-overhead fwd+bwd driver of one MoE layer.
+
+Holds the workspace, outputs and gradients for a fixed (N, E, k, D_i, H, D_o,
+dtype) and calls the C ABI (hxm_moe_forward / hxm_moe_backward) directly with
+cached pointers, so a training loop (or bench.py) issues a step with a few
+microseconds of host work.  All buffers are laid out once in HBM.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from ._lib import check, lib
+from .moe_layer import MoeGrads, MoeLayerParams, layer_workspace, make_desc
+
+
+class LayerRunner:
+    def __init__(self, p: MoeLayerParams, n_tokens: int, k: int, device="cuda",
+                 dtype=torch.bfloat16, add_b2: bool = True):
+        p.validate()
+        self.p = p
+        self.dtype = dtype
+        self.desc = make_desc(n_tokens, p.experts(), k, p.d_in(), p.hidden(), p.d_out(),
+                              p.activation, dtype, add_b2 and p.b2 is not None)
+        self.ws = layer_workspace(self.desc, device)
+        f = dict(dtype=torch.float32, device=device)
+        E, Di, H, Do = p.experts(), p.d_in(), p.hidden(), p.d_out()
+        self.y = torch.empty(n_tokens, Do, **f)
+        self.grads = MoeGrads(torch.empty(E, Di, H, **f), torch.empty(E, H, **f),
+                              torch.empty(E, H, Do, **f),
+                              torch.empty(E, Do, **f) if self.desc.add_b2 else None,
+                              torch.empty(n_tokens, Di, **f))
+        self.b1 = p.b1.to(torch.float32).contiguous()
+        self.b2 = p.b2.to(torch.float32).contiguous() if p.b2 is not None else None
+        self._pd = C.byref(self.desc)
+        self._L = lib()
+
+    def forward(self, x: torch.Tensor, assignments: torch.Tensor, stream=None,
+                status: torch.Tensor | None = None) -> torch.Tensor:
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        check(self._L.hxm_moe_forward(
+            self._pd, x.data_ptr(), self.p.w1.data_ptr(), self.b1.data_ptr(),
+            self.p.w2.data_ptr(), None if self.b2 is None else self.b2.data_ptr(),
+            assignments.data_ptr(), self.y.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
+            None if status is None else status.data_ptr(), st), "moe_forward")
+        return self.y
+
+    def backward(self, x: torch.Tensor, g_y: torch.Tensor, stream=None) -> MoeGrads:
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        g = self.grads
+        check(self._L.hxm_moe_backward(
+            self._pd, x.data_ptr(), self.p.w1.data_ptr(), self.p.w2.data_ptr(), g_y.data_ptr(),
+            self.ws.data_ptr(), self.ws.numel(), g.gw1.data_ptr(), g.gb1.data_ptr(),
+            g.gw2.data_ptr(), None if g.gb2 is None else g.gb2.data_ptr(), g.gx.data_ptr(), st),
+            "moe_backward")
+        return g
+
+    def step(self, x, assignments, g_y, stream=None):
+        self.forward(x, assignments, stream)
+        return self.backward(x, g_y, stream)

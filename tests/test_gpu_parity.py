@@ -1,0 +1,314 @@
+"""GPU parity: the CUDA path (through the C ABI) against the pinned CPU oracle.
+
+Bars (BASELINE.json north_star; scaled error = max|a-b| / (1 + max|ref|),
+reference tests/support/test_oracles.hpp:60-62):
+  * routing index: bit-exact;
+  * integer-valued known-answer tests: exact in fp32 and bf16;
+  * fp32 path: scaled error <= 1e-4;
+  * bf16 path: scaled error <= 2e-2, with the oracle fed the same
+    bf16-rounded inputs so only accumulation / stash rounding is measured.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+RTOL_F32 = 1e-4
+RTOL_BF16 = 2e-2
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def hx():
+    import paper_2411_01288_b200 as H
+    return H
+
+
+def dev(a, dtype=torch.float32):
+    return torch.as_tensor(np.asarray(a, dtype=np.float64)).to("cuda", dtype)
+
+
+def host(t):
+    return t.detach().to(torch.float64).cpu().numpy()
+
+
+def rounded(a, dtype):
+    """The values the device sees, as float64 for the oracle."""
+    return host(dev(a, dtype))
+
+
+def kat():
+    with open(os.path.join(os.path.dirname(__file__), "golden", "kat.json")) as f:
+        return json.load(f)
+
+
+# ----------------------------------------------------------------- routing --
+def test_reindex_kats_bitexact():
+    H = hx()
+    for c in kat()["reindex"]:
+        rx = H.build_reindex(c["assignment"], c["E"], c["blk"])
+        assert rx.idx.cpu().tolist() == c["idx"], c["cite"]
+        assert rx.v.cpu().tolist() == c["v"], c["cite"]
+
+
+def test_reindex_errors():
+    H = hx()
+    for c in kat()["reindex_errors"]:
+        with pytest.raises(ValueError):
+            H.build_reindex(c["assignment"], c["E"], c["blk"])
+
+
+def test_reindex_reference_fixtures_bitexact(golden_dir):
+    H = hx()
+    d = np.load(os.path.join(golden_dir, "ref_reindex.npz"))
+    for i in range(40):
+        E, blk = d[f"r{i}_meta"].tolist()
+        rx = H.build_reindex(d[f"r{i}_a"], E, blk)
+        assert np.array_equal(rx.v.cpu().numpy(), d[f"r{i}_v"]), i
+        assert np.array_equal(rx.idx.cpu().numpy(), d[f"r{i}_idx"]), i
+    for c in range(2):
+        rx = H.build_reindex(d["c2_assign"][c], 32, 8)
+        assert np.array_equal(rx.v.cpu().numpy(), d[f"c2_v{c}"])
+        assert np.array_equal(rx.idx.cpu().numpy(), d[f"c2_idx{c}"])
+
+
+@pytest.mark.parametrize("n,E,blk,dist", [
+    (131072, 64, 8, "uniform"),      # c4 routing size
+    (16384, 64, 1, "zipf:1.5"),
+    (100000, 7, 128, "uniform"),
+    (5000, 300, 3, "uniform"),       # many experts, odd blk
+    (1, 1, 1, "uniform"),
+    (3000, 16, 16, "fixed:0"),       # all tokens to one expert
+])
+def test_reindex_random_bitexact(n, E, blk, dist):
+    H = hx()
+    a = O.synthesize_routing(n, E, 1, dist, n + E)[0]
+    want = O.build_reindex(a, E, blk)
+    rx = H.build_reindex(a, E, blk)
+    assert np.array_equal(rx.idx.cpu().numpy(), want.idx)
+    assert np.array_equal(rx.v.cpu().numpy(), want.v)
+
+
+def test_reindex_500_random_instances():
+    """acceptance criterion 7 style (verify_suites.cpp:166-218)."""
+    H = hx()
+    rng = np.random.default_rng(20240607)
+    for _ in range(500):
+        n = int(rng.integers(1, 65)); E = int(rng.integers(1, 9))
+        blk = int(rng.choice([2, 4, 8]))
+        a = rng.integers(0, E, size=n).astype(np.int32)
+        want = O.build_reindex(a, E, blk)
+        rx = H.build_reindex(a, E, blk)
+        assert np.array_equal(rx.v.cpu().numpy(), want.v)
+        assert np.array_equal(rx.idx.cpu().numpy(), want.idx)
+
+
+# ---------------------------------------------------------------- operators --
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_operator_kats_exact(dtype):
+    H = hx()
+    k = kat()
+    for c in k["esmm"]:
+        rx = H.build_reindex(c["assignment"], c["E"], c["blk"])
+        y = H.esmm(dev(c["x"], dtype), dev(c["w"], dtype), dev(c["b"]), rx)
+        assert host(y).tolist() == c["y"], c["cite"]
+    for c in k["ess"]:
+        rx = H.build_reindex(c["assignment"], c["E"], c["blk"])
+        assert host(H.ess(dev(c["x"], dtype), rx)).tolist() == c["out"], c["cite"]
+    for c in k["estmm"]:
+        rx = H.build_reindex(c["assignment"], c["E"], c["blk"])
+        got = H.estmm(dev(c["x1"], dtype), dev(c["x2"], dtype), rx)
+        assert host(got).tolist() == c["out"], c["cite"]
+
+
+def test_esmm_accumulate_and_errors():
+    H = hx()
+    rng = np.random.default_rng(6)
+    x = rng.standard_normal((10, 3)); w = rng.standard_normal((2, 3, 4))
+    b = rng.standard_normal((2, 4))
+    rx_a = H.build_reindex([0, 1, 0, 1, 0, 1, 0, 1, 0, 1], 2, 2)
+    rx_b = H.build_reindex([1, 1, 1, 0, 0, 0, 1, 1, 0, 0], 2, 2)
+    pa = H.esmm(dev(x), dev(w), dev(b), rx_a)
+    pb = H.esmm(dev(x), dev(w), dev(b), rx_b)
+    dest = pa.clone()
+    H.esmm(dev(x), dev(w), dev(b), rx_b, H.ACCUMULATE, dest)
+    assert torch.equal(dest, pa + pb)  # test_es_ops.cpp:60-77
+    with pytest.raises(ValueError):
+        H.esmm(dev(x), dev(w), None, rx_a, H.ACCUMULATE, None)
+    with pytest.raises(H.ShapeError):
+        H.esmm(dev(x), dev(w), None, rx_a, H.ACCUMULATE, torch.zeros(3, 4, device="cuda"))
+    with pytest.raises(H.ShapeError):  # test_es_ops.cpp:289-298
+        H.esmm(dev(np.zeros((2, 3))), dev(np.zeros((2, 4, 2))), None,
+               H.build_reindex([0, 1], 2, 2))
+    with pytest.raises(H.ShapeError):
+        H.estmm(dev(np.zeros((2, 3))), dev(np.zeros((3, 2))), H.build_reindex([0, 1], 2, 2))
+    with pytest.raises(H.ShapeError):
+        H.ess(dev(np.zeros((5, 2))), H.build_reindex([0, 1], 2, 2))
+
+
+@pytest.mark.parametrize("dtype,rtol", [(torch.float32, RTOL_F32), (torch.bfloat16, RTOL_BF16)])
+def test_operators_vs_reference_fixtures(golden_dir, dtype, rtol):
+    H = hx()
+    d = np.load(os.path.join(golden_dir, "ref_ops.npz"))
+    for i in range(16):
+        g = lambda k: d[f"o{i}_{k}"]
+        E, blk = g("meta").tolist()
+        rx = H.build_reindex(g("a"), E, blk)
+        x, x2, w, b = (rounded(g(k), dtype) for k in ("x", "x2", "w", "b"))
+        orx = O.build_reindex(g("a"), E, blk)
+        if dtype == torch.float32:  # fixtures are the reference's own outputs
+            want_mm, want_ss, want_tm = g("esmm"), g("ess"), g("estmm")
+        else:                        # oracle on the bf16-rounded inputs
+            want_mm = O.esmm(x, w, g("b"), orx)
+            want_ss, want_tm = O.ess(x, orx), O.estmm(x, x2, orx)
+        got = H.esmm(dev(x, dtype), dev(w, dtype), dev(g("b")), rx)
+        assert O.scaled_err(host(got), want_mm) <= rtol, (i, "esmm")
+        assert O.scaled_err(host(H.ess(dev(x, dtype), rx)), want_ss) <= rtol, (i, "ess")
+        got_tm = H.estmm(dev(x, dtype), dev(x2, dtype), rx)
+        assert O.scaled_err(host(got_tm), want_tm) <= rtol, (i, "estmm")
+        f = H.esfk(dev(x, dtype), dev(x2, dtype), dev(w, dtype), rx, w_transposed=True)
+        want_gx = O.esmm(x2, np.ascontiguousarray(np.transpose(w, (0, 2, 1))), None, orx)
+        assert O.scaled_err(host(f.grad_x), want_gx) <= rtol, (i, "esfk")
+
+
+@pytest.mark.parametrize("E,n,d1,d2,blk", [
+    (32, 4096, 384, 1536, 8),    # c2 first GEMM shape (token subsample)
+    (32, 4096, 1536, 384, 8),    # c2 second GEMM shape
+    (8, 1000, 128, 256, 3),      # ragged segments, odd blk
+    (64, 3000, 64, 192, 8),      # many experts, some empty
+])
+def test_bf16_operators_at_scale(E, n, d1, d2, blk):
+    H = hx()
+    rng = np.random.default_rng(E * n)
+    a = O.synthesize_routing(n, E, 1, "zipf:1.1", 5)[0]
+    x = rounded(rng.standard_normal((n, d1)), torch.bfloat16)
+    x2 = rounded(rng.standard_normal((n, d2)), torch.bfloat16)
+    w = rounded(0.5 * rng.standard_normal((E, d1, d2)), torch.bfloat16)
+    b = rng.standard_normal((E, d2))
+    orx = O.build_reindex(a, E, blk)
+    rx = H.build_reindex(a, E, blk)
+    bf = torch.bfloat16
+    got = H.esmm(dev(x, bf), dev(w, bf), dev(b), rx)
+    assert O.scaled_err(host(got), O.esmm(x, w, b, orx)) <= RTOL_BF16
+    gt = H.esmm(dev(x2, bf), dev(w, bf), None, rx, w_transposed=True)
+    want_t = O.esmm(x2, np.ascontiguousarray(np.transpose(w, (0, 2, 1))), None, orx)
+    assert O.scaled_err(host(gt), want_t) <= RTOL_BF16
+    assert O.scaled_err(host(H.estmm(dev(x, bf), dev(x2, bf), rx)), O.estmm(x, x2, orx)) <= RTOL_BF16
+    assert O.scaled_err(host(H.ess(dev(x, bf), rx)), O.ess(x, orx)) <= RTOL_BF16
+
+
+# -------------------------------------------------------------------- layer --
+def _layer_case(E, k, din, hid, dout, n, act, dtype, seed, dist="uniform"):
+    H = hx()
+    p, x = H.make_random_params(E, din, hid, dout, act, seed=seed, n_tokens=n, dtype=dtype)
+    r = H.synthesize_routing(n, E, k, dist, seed + 1)
+    gy = torch.as_tensor(np.random.default_rng(seed).standard_normal((n, dout))).to("cuda", dtype)
+    return p, x, r, gy
+
+
+def _check_layer(p, x, r, gy, rtol, act):
+    H = hx()
+    fw = H.moe_forward(x, p, r)
+    g = H.moe_backward(fw.stash, p, gy)
+    y_ref, y1_ref, y2_ref = O.moe_forward(host(x), host(p.w1), host(p.b1), host(p.w2),
+                                          host(p.b2), r.assignments, 8, act)
+    go = O.moe_backward(host(x), host(p.w1), host(p.w2), r.assignments, y1_ref, y2_ref,
+                        host(gy), 8, act)
+    errs = {"y": O.scaled_err(host(fw.y), y_ref)}
+    for i in range(r.k):
+        y1, y2 = fw.stash.export(i)
+        errs[f"y1_{i}"] = O.scaled_err(host(y1), y1_ref[i])
+        errs[f"y2_{i}"] = O.scaled_err(host(y2), y2_ref[i])
+    for key in ("gw1", "gb1", "gw2", "gb2", "gx"):
+        errs[key] = O.scaled_err(host(getattr(g, key)), go[key])
+    bad = {k: v for k, v in errs.items() if not v <= rtol}
+    assert not bad, bad
+    return errs
+
+
+def test_layer_chain_rule_kat():
+    H = hx()
+    c = kat()["layer_chain_rule"]
+    for dtype in (torch.float32, torch.bfloat16):
+        p = H.MoeLayerParams(dev(c["w1"], dtype), dev(c["b1"]), dev(c["w2"], dtype),
+                             dev(c["b2"]), c["act"])
+        r = H.RoutingChoice(1, 1, 1, np.array(c["assignments"], np.int32))
+        fw = H.moe_forward(dev(c["x"], dtype), p, r, c["blk"])
+        assert host(fw.y).tolist() == c["y"]
+        g = H.moe_backward(fw.stash, p, dev(c["g_y"], dtype))
+        for key in ("gx", "gw1", "gw2", "gb1", "gb2"):
+            assert host(getattr(g, key)).tolist() == c[key], (dtype, key)
+
+
+def test_layer_reference_fixtures_fp32(golden_dir):
+    H = hx()
+    d = np.load(os.path.join(golden_dir, "ref_layer.npz"))
+    for i in range(5):
+        g = lambda k: d[f"l{i}_{k}"]
+        E, k, din, hid, dout, n, blk, act = g("meta").tolist()
+        actn = {v: kk for kk, v in O.ACT.items()}[act]
+        p = H.MoeLayerParams(dev(g("w1")), dev(g("b1")), dev(g("w2")), dev(g("b2")), actn)
+        r = H.RoutingChoice(n, E, k, g("a"))
+        fw = H.moe_forward(dev(g("x")), p, r, blk)
+        assert O.scaled_err(host(fw.y), g("y")) <= RTOL_F32, i
+        gr = H.moe_backward(fw.stash, p, dev(g("gy")))
+        for key in ("gw1", "gb1", "gw2", "gb2", "gx"):
+            assert O.scaled_err(host(getattr(gr, key)), g(key)) <= RTOL_F32, (i, key)
+
+
+def test_layer_c1_fp32_full_size():
+    """BASELINE.json configs[0]: 8 experts top-1, d=96, ffn=384, 3136 tokens, fp32."""
+    p, x, r, gy = _layer_case(8, 1, 96, 384, 96, 3136, "gelu", torch.float32, 1)
+    _check_layer(p, x, r, gy, RTOL_F32, "gelu")
+
+
+@pytest.mark.parametrize("E,k,din,hid,dout,n,act,dist", [
+    (32, 2, 384, 1536, 384, 1024, "gelu", "uniform"),  # c2 dims, token subsample
+    (8, 2, 64, 128, 64, 777, "relu", "uniform"),
+    (16, 3, 128, 256, 192, 500, "identity", "zipf:1.3"),
+    (64, 2, 128, 192, 128, 600, "gelu", "uniform"),    # many empty experts
+    (4, 2, 12, 20, 6, 50, "gelu", "uniform"),          # unaligned dims
+])
+def test_layer_bf16_vs_oracle(E, k, din, hid, dout, n, act, dist):
+    p, x, r, gy = _layer_case(E, k, din, hid, dout, n, act, torch.bfloat16, E + n, dist)
+    _check_layer(p, x, r, gy, RTOL_BF16, act)
+
+
+def test_layer_c2_full_size_properties():
+    """c2 at full N: exact integer properties that do not need the CPU oracle.
+    With g_y = ones, gb2[e] = number of (token, choice) slots routed to e
+    exactly, and two runs give bit-identical outputs (k = 2 reductions
+    commute)."""
+    H = hx()
+    E, k, D, Hd, N = 32, 2, 384, 1536, 16384
+    p, x = H.make_random_params(E, D, Hd, D, "gelu", seed=1, n_tokens=N)
+    r = H.synthesize_routing(N, E, k, "uniform", 1)
+    ones = torch.ones(N, D, dtype=torch.bfloat16, device="cuda")
+    fw = H.moe_forward(x, p, r)
+    g = H.moe_backward(fw.stash, p, ones)
+    counts = np.bincount(r.assignments.ravel(), minlength=E).astype(np.float64)
+    assert np.array_equal(host(g.gb2), np.repeat(counts[:, None], D, axis=1))
+    fw2 = H.moe_forward(x, p, r)
+    assert torch.equal(fw.y, fw2.y)
+    assert torch.isfinite(g.gw1).all() and torch.isfinite(g.gx).all()
+
+
+def test_layer_routing_validation():
+    H = hx()
+    p, x = H.make_random_params(2, 8, 16, 8, "gelu", seed=28, n_tokens=4)
+    bad = H.RoutingChoice(4, 2, 3, np.zeros((3, 4), np.int32))  # k > E
+    with pytest.raises(ValueError):
+        H.moe_forward(x, p, bad)
+    ok = H.synthesize_routing(4, 2, 1, "uniform", 1)
+    with pytest.raises(H.ShapeError):
+        H.moe_forward(x[:3], p, ok)
