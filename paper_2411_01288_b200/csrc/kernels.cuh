@@ -45,6 +45,8 @@ struct EsmmArgs {
   double work;        // algorithmic FLOP (GEMMs) or bytes (ESS) of the launch
   const void* a;  // A rows, K = d1 columns
   RowMap amap;
+  int64_t a_rows;  // rows of the tensor behind `a` (TMA bounds)
+  int64_t n_experts;
   const void* w;  // w_trans == 0: E x d1 x d2 ; 1: E x d2 x d1 (use W^T)
   int w_trans;
   int64_t d1, d2;
@@ -69,6 +71,7 @@ struct EstmmArgs {
   RowMap m1;
   const void* x2;  // rows via m2, d2 columns
   RowMap m2;
+  int64_t x1_rows, x2_rows;  // rows of the tensors behind x1 / x2
   int64_t d1, d2;
   const SegTile* tiles;  // K chunks (split flag / empty flag)
   const int32_t* n_tiles;

@@ -187,6 +187,8 @@ hxm_status hxm_moe_forward(const hxm_layer_desc* d, const void* x, const void* w
   EsmmArgs a1{};
   a1.a = x;
   a1.amap = slot;
+  a1.a_rows = N;
+  a1.n_experts = E;
   a1.w = w1;
   a1.w_trans = 0;
   a1.d1 = d->d_in;
@@ -209,6 +211,7 @@ hxm_status hxm_moe_forward(const hxm_layer_desc* d, const void* x, const void* w
   EsmmArgs a2 = a1;
   a2.a = w.y2s;
   a2.amap = map_dense();
+  a2.a_rows = w.bound;
   a2.w = w2;
   a2.d1 = d->hidden;
   a2.d2 = d->d_out;
@@ -265,6 +268,8 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
   t2.m1 = map_dense();
   t2.x2 = g_y;
   t2.m2 = slot;
+  t2.x1_rows = w.bound;
+  t2.x2_rows = N;
   t2.d1 = H;
   t2.d2 = Do;
   t2.tiles = w.ktiles;
@@ -279,6 +284,8 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
   EsmmArgs b6{};
   b6.a = g_y;
   b6.amap = slot;
+  b6.a_rows = N;
+  b6.n_experts = E;
   b6.w = w2;
   b6.w_trans = 1;  // W2 is E x H x Do; use W2[e]^T (Do x H)
   b6.d1 = Do;
@@ -309,6 +316,8 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
   t1.m1 = slot;
   t1.x2 = w.g1s;
   t1.m2 = map_dense();
+  t1.x1_rows = N;
+  t1.x2_rows = w.bound;
   t1.d1 = Di;
   t1.d2 = H;
   t1.out = gw1;
@@ -319,6 +328,7 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
   EsmmArgs b10 = b6;
   b10.a = w.g1s;
   b10.amap = map_dense();
+  b10.a_rows = w.bound;
   b10.w = w1;
   b10.w_trans = 1;  // W1 is E x Di x H; use W1[e]^T (H x Di)
   b10.d1 = H;

@@ -107,6 +107,8 @@ hxm_status hxm_esmm(hxm_dtype dt, const void* x, int64_t n, int64_t d1, const vo
   EsmmArgs a{};
   a.a = x;
   a.amap = map_v64(v);
+  a.a_rows = n;
+  a.n_experts = E;
   a.w = w;
   a.w_trans = w_trans;
   a.d1 = d1;
@@ -170,6 +172,8 @@ hxm_status hxm_estmm(hxm_dtype dt, const void* x1, const void* x2, int64_t n, in
   a.m1 = map_v64(v);
   a.x2 = x2;
   a.m2 = map_v64(v);
+  a.x1_rows = n;
+  a.x2_rows = n;
   a.d1 = d1;
   a.d2 = d2;
   a.tiles = o.ktiles;

@@ -1,12 +1,686 @@
-// umma.cu -- tcgen05 (5th-gen tensor core) expert-specific GEMMs, bf16 in,
-// fp32 accumulate in TMEM.  (placeholder: filled in by the next milestone)
+// umma.cu -- tcgen05 (5th-gen tensor core) expert-specific GEMMs for sm_100a:
+// bf16 operands staged by TMA (tile and tile::gather4), fp32 accumulators in
+// TMEM, one persistent warp-specialised kernel per operator.
+//
+//   ESMM  (es_ops.cpp:47-81):   out[p] = A[row(p)] . W[e] (+ b[e]) over 128-row
+//          segment tiles of one expert; A rows gathered by TMA gather4 straight
+//          from the token-order tensor (no dispatch copy), or read as dense
+//          tiles from the expert-sorted stash.  W read MN-major (W[e] is D1 x D2
+//          row-major) or K-major (W^T use: no transpose_experts copy).
+//   ESTMM (es_ops.cpp:106-128): out[e] = X1^T X2 over the expert's token
+//          positions (K = tokens, variable), both operands MN-major, split-K
+//          over <= kEstmmChunk-position chunks with fp32 red.add for split
+//          experts.
+//
+// Warp roles (192 threads): warp 0 = TMA producer (all 32 lanes issue gather4),
+// warp 1 = TMEM allocator + single-thread tcgen05.mma issuer, warps 2..5 =
+// epilogue (TMEM -> registers -> bias / activation / stores).  Pipelines:
+// smem ring full/empty (TMA <-> MMA) and a double-buffered TMEM accumulator
+// full/empty (MMA <-> epilogue), so tile i's epilogue overlaps tile i+1's MMA.
+#include <cuda.h>
+
 #include "kernels.cuh"
 
 namespace hxm {
 
-bool umma_supports_esmm(int64_t, int64_t) { return false; }
-bool umma_supports_estmm(int64_t, int64_t) { return false; }
-hxm_status umma_esmm(const EsmmArgs&, cudaStream_t) { return HXM_ERR_UNSUPPORTED; }
-hxm_status umma_estmm(const EstmmArgs&, cudaStream_t) { return HXM_ERR_UNSUPPORTED; }
+namespace {
+
+constexpr int BM = 128;  // UMMA M (rows per tile, TMEM lanes)
+constexpr int BK = 64;   // one 128-byte swizzle atom of bf16 per k-block
+constexpr int UK = 16;   // UMMA K for kind::f16
+constexpr int kThreads = 192;
+constexpr uint32_t kTmemCols = 512;
+constexpr int kABytes = BM * BK * 2;  // 16 KB
+
+// ------------------------------------------------------------- PTX layer --
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 10000000;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(a),
+      "r"(parity));
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)));
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                       int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                       int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+// 4 rows (r0..r3, -1 = out of bounds -> zero fill) x 64 columns from col.
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int col, int r0, int r1, int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db,
+                                          uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
+}
+
+// UMMA shared-memory descriptor (sm100): start>>4 [0,14), LBO>>4 [16,30),
+// SBO>>4 [32,46), version=1 [46,48), layout SWIZZLE_128B=2 [61,64).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) |
+         (static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
+}
+// Instruction descriptor kind::f16: D=f32, A=B=bf16, majors, N>>3, M>>4.
+__host__ __device__ constexpr uint32_t idesc_bf16(int n, int a_mn, int b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(a_mn) << 15) |
+         (static_cast<uint32_t>(b_mn) << 16) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ float gelu_fast(float x) {
+  const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
+  return 0.5f * x * (1.f + t);
+}
+__device__ __forceinline__ float act_fwd(int act, float x) {
+  if (act == HXM_ACT_GELU) return gelu_fast(x);
+  if (act == HXM_ACT_RELU) return x > 0.f ? x : 0.f;
+  return x;
+}
+__device__ __forceinline__ float act_bwd(int act, float x) {
+  if (act == HXM_ACT_GELU) {
+    const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
+    const float du = 0.7978845608028654f * (1.f + 3.f * 0.044715f * x * x);
+    return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * du;
+  }
+  if (act == HXM_ACT_RELU) return x > 0.f ? 1.f : 0.f;
+  return 1.f;
+}
+
+struct UParams {
+  CUtensorMap tmA;  // ESMM A / ESTMM X1
+  CUtensorMap tmB;  // ESMM W / ESTMM X2
+  RowMap amap;      // gather map of A (ESMM rows / ESTMM X1 rows)
+  RowMap bmap;      // ESTMM X2 rows
+  int a_gather, b_gather, b_kmajor;
+  int K, N, M;  // ESMM: K=d1, N=d2 ; ESTMM: M=d1, N=d2
+  int n_nt, n_mt;
+  const SegTile* tiles;
+  const int32_t* n_tiles;
+  int epi, act;
+  const float* bias;
+  float* out_f32;
+  RowMap omap;
+  void* out1;
+  void* out2;
+  const void* y1s;
+  float* est_out;
+};
+
+template <int BN>
+struct Cfg {
+  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kStage = kABytes + kBBytes;
+  static constexpr int kStages = (200 * 1024) / kStage > 8 ? 8 : (200 * 1024) / kStage;
+  static constexpr int kSmem = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int BN, bool ESTMM>
+__global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant__ UParams p) {
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStage);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int n_items = *p.n_tiles;
+  const int per_item = ESTMM ? p.n_mt * p.n_nt : p.n_nt;
+  const int total = n_items * per_item;
+
+  if (warp == 0) {
+    // ================================ TMA producer =======================
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&p.tmA) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&p.tmB) : "memory");
+    }
+    int s = 0;
+    uint32_t ph = 0;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      const SegTile t = p.tiles[w / per_item];
+      const int rem = w % per_item;
+      if (!ESTMM) {
+        const int n0 = rem * BN;
+        const int nk = p.K / BK;
+        int rows[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int q = t.begin + 4 * lane + i;
+          rows[i] = (p.a_gather && q < t.end) ? p.amap(q) : -1;
+        }
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* sa = smem + s * C::kStage;
+          uint8_t* sb = sa + kABytes;
+          if (lane == 0) mbar_arrive_tx(&full[s], C::kStage);
+          __syncwarp();
+          if (p.a_gather) {
+            tma_gather4(sa + lane * 512, &p.tmA, &full[s], kb * BK, rows[0], rows[1], rows[2],
+                        rows[3]);
+          } else if (lane == 0) {
+            tma_2d(sa, &p.tmA, &full[s], kb * BK, t.begin);
+          }
+          if (lane == 0) {
+            if (p.b_kmajor) {
+              tma_3d(sb, &p.tmB, &full[s], kb * BK, n0, t.expert);
+            } else {
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j)
+                tma_3d(sb + j * 8192, &p.tmB, &full[s], n0 + 64 * j, kb * BK, t.expert);
+            }
+          }
+          __syncwarp();
+          if (++s == C::kStages) { s = 0; ph ^= 1; }
+        }
+      } else {
+        const int mt = rem / p.n_nt, nt = rem % p.n_nt;
+        const int m0 = mt * BM, n0 = nt * BN;
+        const int nk = (t.end - t.begin + BK - 1) / BK;
+        for (int kb = 0; kb < nk; ++kb) {
+          const int p0 = t.begin + kb * BK;
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* sa = smem + s * C::kStage;
+          uint8_t* sb = sa + kABytes;
+          if (lane == 0) mbar_arrive_tx(&full[s], C::kStage);
+          __syncwarp();
+          // A = X1^T: two 64-column chunks of the 64 k-rows
+          if (p.a_gather) {
+            const int rg = lane % 16, ch = lane / 16;
+            int r[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int q = p0 + 4 * rg + i;
+              r[i] = q < t.end ? p.amap(q) : -1;
+            }
+            tma_gather4(sa + ch * 8192 + rg * 512, &p.tmA, &full[s], m0 + 64 * ch, r[0], r[1],
+                        r[2], r[3]);
+          } else if (lane == 0) {
+            tma_2d(sa, &p.tmA, &full[s], m0, p0);
+            tma_2d(sa + 8192, &p.tmA, &full[s], m0 + 64, p0);
+          }
+          // B = X2: BN/64 chunks of the 64 k-rows
+          if (p.b_gather) {
+            for (int g = lane; g < (BN / 64) * 16; g += 32) {
+              const int rg = g % 16, ch = g / 16;
+              int r[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int q = p0 + 4 * rg + i;
+                r[i] = q < t.end ? p.bmap(q) : -1;
+              }
+              tma_gather4(sb + ch * 8192 + rg * 512, &p.tmB, &full[s], n0 + 64 * ch, r[0], r[1],
+                          r[2], r[3]);
+            }
+          } else if (lane == 0) {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) tma_2d(sb + j * 8192, &p.tmB, &full[s], n0 + 64 * j, p0);
+          }
+          __syncwarp();
+          if (++s == C::kStages) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================================ MMA issuer ==========================
+    constexpr uint32_t kIdescEsmmMN = idesc_bf16(BN, 0, 1);
+    constexpr uint32_t kIdescEsmmK = idesc_bf16(BN, 0, 0);
+    constexpr uint32_t kIdescEst = idesc_bf16(BN, 1, 1);
+    const uint32_t idesc = ESTMM ? kIdescEst : (p.b_kmajor ? kIdescEsmmK : kIdescEsmmMN);
+    int s = 0, acc = 0;
+    uint32_t ph = 0, aph = 0;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      const SegTile t = p.tiles[w / per_item];
+      const int nk = ESTMM ? (t.end - t.begin + BK - 1) / BK : p.K / BK;
+      mbar_wait(&tempty[acc], aph ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem + acc * BN;
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sa = smem_u32(smem + s * C::kStage);
+          const uint32_t sb = sa + kABytes;
+#pragma unroll
+          for (int kk = 0; kk < BK / UK; ++kk) {
+            uint64_t da, db;
+            if (ESTMM) {  // both MN-major: 16 k-rows = 2 x 1024 B per UMMA_K
+              da = sdesc(sa + kk * 2048, 8192, 1024);
+              db = sdesc(sb + kk * 2048, 8192, 1024);
+            } else {      // A K-major: 32 B per UMMA_K inside the swizzle atom
+              da = sdesc(sa + kk * 32, 16, 1024);
+              db = p.b_kmajor ? sdesc(sb + kk * 32, 16, 1024) : sdesc(sb + kk * 2048, 8192, 1024);
+            }
+            umma_bf16(d, da, db, idesc, (kb | kk) != 0);
+          }
+          umma_commit(&empty[s]);
+        }
+        __syncwarp();
+        if (++s == C::kStages) { s = 0; ph ^= 1; }
+      }
+      if (lane == 0) umma_commit(&tfull[acc]);
+      __syncwarp();
+      if (++acc == 2) { acc = 0; aph ^= 1; }
+    }
+  } else {
+    // ================================ epilogue ============================
+    const int lg = warp & 3;  // TMEM lane group this warp may access
+    const int row = lg * 32 + lane;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      const SegTile t = p.tiles[w / per_item];
+      const int rem = w % per_item;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(lg * 32) << 16) + acc * BN;
+      if (!ESTMM) {
+        const int n0 = rem * BN;
+        const int q = t.begin + row;
+        const bool valid = q < t.end;
+        const int orow = valid ? p.omap(q) : -1;
+        const int N = p.N;
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(taddr + c0, r);
+          if (c0 + 32 == BN) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+          }
+          if (!valid) continue;
+          const int n = n0 + c0;
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+          if (p.bias && p.epi != EPI_BWD_ACT) {
+            const float4* b4 = reinterpret_cast<const float4*>(p.bias + static_cast<int64_t>(t.expert) * N + n);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 b = __ldg(b4 + i);
+              v[4 * i] += b.x; v[4 * i + 1] += b.y; v[4 * i + 2] += b.z; v[4 * i + 3] += b.w;
+            }
+          }
+          if (p.epi == EPI_FWD_ACT || p.epi == EPI_BWD_ACT) {
+            const int64_t off = static_cast<int64_t>(q) * N + n;
+            uint4* o1 = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out1) + off);
+            if (orow < 0) {  // padding slot: zero rows in the sorted stash
+#pragma unroll
+              for (int i = 0; i < 4; ++i) o1[i] = make_uint4(0, 0, 0, 0);
+              if (p.epi == EPI_FWD_ACT) {
+                uint4* o2 = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out2) + off);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) o2[i] = make_uint4(0, 0, 0, 0);
+              }
+              continue;
+            }
+            if (p.epi == EPI_FWD_ACT) {
+              uint4* o2 = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out2) + off);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                o1[i] = make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                                   pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+                float a[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) a[j] = act_fwd(p.act, v[8 * i + j]);
+                o2[i] = make_uint4(pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]),
+                                   pack_bf16(a[4], a[5]), pack_bf16(a[6], a[7]));
+              }
+            } else {
+              const uint4* y4 = reinterpret_cast<const uint4*>(
+                  static_cast<const __nv_bfloat16*>(p.y1s) + off);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const uint4 yy = y4[i];
+                const __nv_bfloat16* yb = reinterpret_cast<const __nv_bfloat16*>(&yy);
+                float g[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) g[j] = v[8 * i + j] * act_bwd(p.act, __bfloat162float(yb[j]));
+                o1[i] = make_uint4(pack_bf16(g[0], g[1]), pack_bf16(g[2], g[3]),
+                                   pack_bf16(g[4], g[5]), pack_bf16(g[6], g[7]));
+              }
+            }
+          } else {
+            if (orow < 0) continue;
+            float* o = p.out_f32 + static_cast<int64_t>(orow) * N + n;
+            float4* o4 = reinterpret_cast<float4*>(o);
+            if (p.epi == EPI_WRITE) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                o4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            } else if (p.epi == EPI_ACCUM) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                float4 c = o4[i];
+                c.x += v[4 * i]; c.y += v[4 * i + 1]; c.z += v[4 * i + 2]; c.w += v[4 * i + 3];
+                o4[i] = c;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                red_add_v4(o + 4 * i, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            }
+          }
+        }
+      } else {
+        const int mt = rem / p.n_nt, nt = rem % p.n_nt;
+        const int m = mt * BM + row;
+        const int n0 = nt * BN;
+        const bool valid = m < p.M;
+        const bool split = t.flags & 1;
+        const bool empty_seg = t.end <= t.begin;
+        float* o = p.est_out + (static_cast<int64_t>(t.expert) * p.M + m) * p.N + n0;
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t r[32];
+          if (!empty_seg) tmem_ld32(taddr + c0, r);
+          if (c0 + 32 == BN) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+          }
+          if (!valid) continue;
+          float4* o4 = reinterpret_cast<float4*>(o + c0);
+          if (empty_seg) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) o4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            continue;
+          }
+          if (split) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              red_add_v4(o + c0 + 4 * i, __uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                         __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              o4[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                                  __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+          }
+        }
+      }
+      if (++acc == 2) { acc = 0; aph ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(kTmemCols));
+  }
+}
+
+// ----------------------------------------------------------- host side ---
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encoder() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  }
+  return fn;
+}
+
+// bf16 tensor of `rank` dims (dims[0] innermost, element counts), row pitch
+// strides in bytes for dims 1.., box sizes, 128B swizzle, OOB -> zeros.
+bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
+              const uint64_t* strides_bytes, const uint32_t* box) {
+  EncodeFn enc = encoder();
+  if (!enc) return false;
+  cuuint64_t gd[3], gs[2];
+  cuuint32_t bx[3], es[3] = {1, 1, 1};
+  for (int i = 0; i < rank; ++i) {
+    gd[i] = dims[i];
+    bx[i] = box[i];
+  }
+  for (int i = 0; i + 1 < rank; ++i) gs[i] = strides_bytes[i];
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), gd, gs,
+                   bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int pick_bn(int64_t n) {
+  for (int bn : {256, 192, 128, 64})
+    if (n % bn == 0) return bn;
+  return 0;
+}
+
+template <int BN, bool ESTMM>
+hxm_status launch_bn(const UParams& prm, int max_work, cudaStream_t st) {
+  using C = Cfg<BN>;
+  auto kern = umma_kernel<BN, ESTMM>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    HXM_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+    attr_set = true;
+  }
+  const int sms = sm_count();
+  if (sms <= 0) return invalid_arg("tcgen05 path: no CUDA device");
+  const int grid = std::max(1, std::min(sms, max_work));
+  kern<<<grid, kThreads, C::kSmem, st>>>(prm);
+  HXM_CHECK_LAUNCH();
+  return HXM_OK;
+}
+
+template <bool ESTMM>
+hxm_status launch_any(int bn, const UParams& prm, int max_work, cudaStream_t st) {
+  switch (bn) {
+    case 256: return launch_bn<256, ESTMM>(prm, max_work, st);
+    case 192: return launch_bn<192, ESTMM>(prm, max_work, st);
+    case 128: return launch_bn<128, ESTMM>(prm, max_work, st);
+    default: return launch_bn<64, ESTMM>(prm, max_work, st);
+  }
+}
+
+// rows of the tensor behind a row map: gathered sources are bounded by the
+// largest valid row (n_rows), dense sorted buffers by the padded bound.
+}  // namespace
+
+bool umma_supports_esmm(int64_t d1, int64_t d2) {
+  return d1 > 0 && d2 > 0 && d1 % 64 == 0 && d2 % 64 == 0 && d1 < (1 << 30) && d2 < (1 << 30);
+}
+bool umma_supports_estmm(int64_t d1, int64_t d2) { return umma_supports_esmm(d1, d2); }
+
+hxm_status umma_esmm(const EsmmArgs& a, cudaStream_t st) {
+  if (a.max_tiles <= 0) return HXM_OK;
+  if (a.tile_rows != kUmmaRows) return invalid_arg("umma_esmm: tiles must have 128 rows");
+  const int bn = pick_bn(a.d2);
+  UParams prm{};
+  const bool gather = a.amap.kind != MAP_DENSE;
+  // A: gathered token rows (n_rows = a_rows) or the dense sorted stash
+  {
+    const uint64_t dims[2] = {static_cast<uint64_t>(a.d1), static_cast<uint64_t>(a.a_rows)};
+    const uint64_t strides[1] = {static_cast<uint64_t>(a.d1) * 2};
+    const uint32_t box[2] = {64, gather ? 1u : 128u};
+    if (!make_map(&prm.tmA, a.a, 2, dims, strides, box))
+      return invalid_arg("umma_esmm: cannot encode the A tensor map");
+  }
+  // B: W[e] (E x d1 x d2, MN-major) or W^T use (E x d2 x d1, K-major)
+  {
+    const int64_t E = a.n_experts;
+    if (!a.w_trans) {
+      const uint64_t dims[3] = {static_cast<uint64_t>(a.d2), static_cast<uint64_t>(a.d1),
+                                static_cast<uint64_t>(E)};
+      const uint64_t strides[2] = {static_cast<uint64_t>(a.d2) * 2,
+                                   static_cast<uint64_t>(a.d1 * a.d2) * 2};
+      const uint32_t box[3] = {64, 64, 1};
+      if (!make_map(&prm.tmB, a.w, 3, dims, strides, box))
+        return invalid_arg("umma_esmm: cannot encode the W tensor map");
+    } else {
+      const uint64_t dims[3] = {static_cast<uint64_t>(a.d1), static_cast<uint64_t>(a.d2),
+                                static_cast<uint64_t>(E)};
+      const uint64_t strides[2] = {static_cast<uint64_t>(a.d1) * 2,
+                                   static_cast<uint64_t>(a.d1 * a.d2) * 2};
+      const uint32_t box[3] = {64, static_cast<uint32_t>(bn), 1};
+      if (!make_map(&prm.tmB, a.w, 3, dims, strides, box))
+        return invalid_arg("umma_esmm: cannot encode the W^T tensor map");
+    }
+  }
+  prm.amap = a.amap;
+  prm.a_gather = gather;
+  prm.b_kmajor = a.w_trans;
+  prm.K = static_cast<int>(a.d1);
+  prm.N = static_cast<int>(a.d2);
+  prm.n_nt = static_cast<int>(a.d2 / bn);
+  prm.n_mt = 1;
+  prm.tiles = a.tiles;
+  prm.n_tiles = a.n_tiles;
+  prm.epi = a.epi;
+  prm.act = a.act;
+  prm.bias = a.bias;
+  prm.out_f32 = a.out_f32;
+  prm.omap = a.omap;
+  prm.out1 = a.out1;
+  prm.out2 = a.out2;
+  prm.y1s = a.y1s;
+  return launch_any<false>(bn, prm, a.max_tiles * prm.n_nt, st);
+}
+
+hxm_status umma_estmm(const EstmmArgs& a, cudaStream_t st) {
+  if (a.max_tiles <= 0) return HXM_OK;
+  const int bn = pick_bn(a.d2);
+  UParams prm{};
+  const bool ga = a.m1.kind != MAP_DENSE, gb = a.m2.kind != MAP_DENSE;
+  {
+    const uint64_t dims[2] = {static_cast<uint64_t>(a.d1), static_cast<uint64_t>(a.x1_rows)};
+    const uint64_t strides[1] = {static_cast<uint64_t>(a.d1) * 2};
+    const uint32_t box[2] = {64, ga ? 1u : 64u};
+    if (!make_map(&prm.tmA, a.x1, 2, dims, strides, box))
+      return invalid_arg("umma_estmm: cannot encode the X1 tensor map");
+  }
+  {
+    const uint64_t dims[2] = {static_cast<uint64_t>(a.d2), static_cast<uint64_t>(a.x2_rows)};
+    const uint64_t strides[1] = {static_cast<uint64_t>(a.d2) * 2};
+    const uint32_t box[2] = {64, gb ? 1u : 64u};
+    if (!make_map(&prm.tmB, a.x2, 2, dims, strides, box))
+      return invalid_arg("umma_estmm: cannot encode the X2 tensor map");
+  }
+  prm.amap = a.m1;
+  prm.bmap = a.m2;
+  prm.a_gather = ga;
+  prm.b_gather = gb;
+  prm.M = static_cast<int>(a.d1);
+  prm.N = static_cast<int>(a.d2);
+  prm.n_mt = static_cast<int>(ceil_div(a.d1, BM));
+  prm.n_nt = static_cast<int>(a.d2 / bn);
+  prm.tiles = a.tiles;
+  prm.n_tiles = a.n_tiles;
+  prm.est_out = a.out;
+  return launch_any<true>(bn, prm, a.max_tiles * prm.n_mt * prm.n_nt, st);
+}
 
 }  // namespace hxm
