@@ -1,0 +1,345 @@
+"""Tensor parallelism along the FFN hidden dimension H (one process per GPU).
+
+Re-designs the reference's in-process simulator (core/src/dist_sim.cpp) as real
+collectives over torch.distributed (NCCL over NVLink on B200; gloo for the
+CPU tests).  The numerics follow the reference exactly:
+
+* ``shard_params`` / ``unshard_params`` (dist_sim.cpp:29-102): rank r owns
+  W1[:, :, h_r], b1[:, h_r], W2[:, h_r, :]; b2 is owned by rank 0
+  (dist_sim.hpp:33-36).  Shards are stored contiguous per rank.
+* ``PipelineSharedCache`` (dist_sim.hpp:60-82, dist_sim.cpp:104-125): one
+  layer's full parameters per device; CacheError on overflow or
+  read-before-fill.
+* ``data_centric_step`` (dist_sim.cpp:352-452): the parameter shards are
+  all-gathered into the cache -- on a side stream, so the gather of the
+  next layer overlaps the current compute -- every rank runs the full layer on
+  its own tokens, then parameter gradients are summed across ranks
+  (all-reduce as in the reference, or reduce-scatter to the owners).
+* ``model_centric_step`` (dist_sim.cpp:454-601): tokens (and routing, and in
+  backward g_y) are all-gathered, every rank computes the global batch on its
+  H-slice (rank 0 alone adds b2 and computes gb2, dist_sim.cpp:486, 520-522),
+  the partial y and partial gx are all-reduce-summed (or reduce-scattered back
+  to the token owners).
+
+Compute is injected as a ``LocalCompute`` so the same choreography runs with
+the CUDA layer in production and with a CPU reference in the gloo tests.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional, Sequence
+
+import torch
+import torch.distributed as dist
+
+from ._lib import CacheError
+
+
+# ------------------------------------------------------------ sharding ----
+@dataclass
+class ParamShard:
+    w1: torch.Tensor  # E x D_i x h_r
+    b1: torch.Tensor  # E x h_r
+    w2: torch.Tensor  # E x h_r x D_o
+    hidden_offset: int
+
+    def elements(self) -> int:
+        return self.w1.numel() + self.b1.numel() + self.w2.numel()
+
+
+@dataclass
+class ShardedParams:
+    shards: List[ParamShard]
+    b2: Optional[torch.Tensor]  # owned by rank 0
+    activation: str
+    hidden_sizes: List[int]
+
+    def n_devices(self) -> int:
+        return len(self.shards)
+
+    def full_param_elements(self) -> int:
+        s = self.shards[0]
+        E, Di, Do = s.w1.shape[0], s.w1.shape[1], s.w2.shape[2]
+        H = sum(self.hidden_sizes)
+        return E * (Di * H + H + H * Do + Do)
+
+    def shard_elements(self, d: int) -> int:
+        n = self.shards[d].elements()
+        return n + (self.b2.numel() if d == 0 and self.b2 is not None else 0)
+
+
+def even_split(hidden: int, n: int) -> List[int]:
+    base, rem = divmod(hidden, n)
+    return [base + (1 if i < rem else 0) for i in range(n)]
+
+
+def shard_params(p, hidden_alloc: Sequence[int]) -> ShardedParams:
+    """dist_sim.cpp:29-78 (same checks and messages)."""
+    p.validate()
+    if len(hidden_alloc) == 0:
+        raise ValueError("shard_params: need at least one device")
+    if sum(hidden_alloc) != p.hidden():
+        raise ValueError("shard_params: hidden allocation does not sum to the hidden size")
+    if any(h <= 0 for h in hidden_alloc):
+        raise ValueError("shard_params: hidden shares must be > 0")
+    shards, off = [], 0
+    for h in hidden_alloc:
+        shards.append(ParamShard(p.w1[:, :, off:off + h].contiguous(),
+                                 p.b1[:, off:off + h].contiguous(),
+                                 p.w2[:, off:off + h, :].contiguous(), off))
+        off += h
+    return ShardedParams(shards, p.b2, p.activation, list(hidden_alloc))
+
+
+def unshard_params(s: ShardedParams):
+    """dist_sim.cpp:80-102: exact inverse of shard_params."""
+    from .moe_layer import MoeLayerParams
+    w1 = torch.cat([sh.w1 for sh in s.shards], dim=2)
+    b1 = torch.cat([sh.b1 for sh in s.shards], dim=1)
+    w2 = torch.cat([sh.w2 for sh in s.shards], dim=1)
+    return MoeLayerParams(w1, b1, w2, s.b2, s.activation)
+
+
+class PipelineSharedCache:
+    """One full-layer parameter buffer per device (dist_sim.hpp:60-82)."""
+
+    def __init__(self, capacity_elements: int):
+        self.capacity = capacity_elements
+        self._params = None
+        self.layer = -1
+        self.fills = 0
+
+    def fill(self, layer_id: int, params) -> None:
+        n = params.param_elements()
+        if n > self.capacity:
+            raise CacheError(f"pipeline-shared cache: layer parameters ({n} elements) exceed "
+                             f"cache capacity ({self.capacity})")
+        self._params, self.layer = params, layer_id
+        self.fills += 1
+
+    def clear(self) -> None:
+        self._params, self.layer = None, -1
+
+    def filled(self) -> bool:
+        return self._params is not None
+
+    def params(self):
+        if self._params is None:
+            raise CacheError("pipeline-shared cache: read before fill")
+        return self._params
+
+
+# ------------------------------------------------------------- compute ----
+@dataclass
+class LocalCompute:
+    """forward(x, params, assignments, add_b2) -> (y fp32, stash);
+    backward(stash, params, g_y) -> MoeGrads-like object (gw1, gb1, gw2, gb2, gx)."""
+    forward: Callable
+    backward: Callable
+
+
+def cuda_compute() -> LocalCompute:
+    from .moe_layer import moe_backward, moe_forward
+
+    def fwd(x, params, assignments, add_b2):
+        p = params if add_b2 else _without_b2(params)
+        res = moe_forward(x, p, assignments, validate=False)
+        return res.y, res.stash
+
+    def bwd(stash, params, g_y):
+        return moe_backward(stash, params if stash.desc.add_b2 else _without_b2(params), g_y)
+
+    return LocalCompute(fwd, bwd)
+
+
+def _without_b2(p):
+    from .moe_layer import MoeLayerParams
+    return MoeLayerParams(p.w1, p.b1, p.w2, None, p.activation)
+
+
+# ---------------------------------------------------------- collectives ---
+def _ws(group) -> int:
+    return dist.get_world_size(group)
+
+
+def _rank(group) -> int:
+    return dist.get_rank(group)
+
+
+def all_gather_rows(local: torch.Tensor, counts: Sequence[int], group=None) -> torch.Tensor:
+    """Rank-order row concatenation (dist_sim.cpp:127-145) for uneven row
+    counts: pad to the largest count, all_gather_into_tensor, drop padding."""
+    P = _ws(group)
+    m = max(counts)
+    if local.shape[0] < m:
+        pad = torch.zeros((m - local.shape[0],) + tuple(local.shape[1:]), dtype=local.dtype,
+                          device=local.device)
+        local = torch.cat([local, pad])
+    out = torch.empty((P * m,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(out, local.contiguous(), group=group)
+    if all(c == m for c in counts):
+        return out
+    return torch.cat([out[r * m:r * m + counts[r]] for r in range(P)])
+
+
+def _row_counts(n_local: int, group=None, device=None) -> List[int]:
+    t = torch.tensor([n_local], dtype=torch.int64, device=device)
+    out = torch.empty(_ws(group), dtype=torch.int64, device=device)
+    dist.all_gather_into_tensor(out, t, group=group)
+    return [int(v) for v in out.tolist()]
+
+
+def gather_params(shard: ParamShard, b2, hidden_sizes: Sequence[int], activation: str,
+                  group=None, stream: Optional[torch.cuda.Stream] = None):
+    """All-gather every rank's hidden-slice into full parameters (the cache
+    fill of dist_sim.cpp:367-368).  Shards are padded to the largest share so
+    one all_gather_into_tensor moves them; b2 is broadcast from rank 0."""
+    from .moe_layer import MoeLayerParams
+    P = _ws(group)
+    hmax = max(hidden_sizes)
+    E, Di, hr = shard.w1.shape
+    Do = shard.w2.shape[2]
+
+    def padded(t, dim):
+        if t.shape[dim] == hmax:
+            return t.contiguous()
+        shp = list(t.shape)
+        shp[dim] = hmax - t.shape[dim]
+        return torch.cat([t, torch.zeros(shp, dtype=t.dtype, device=t.device)], dim=dim)
+
+    ctx = torch.cuda.stream(stream) if stream is not None else _nullctx()
+    with ctx:
+        # rank-major flat outputs (gloo requires dim-0 concatenation)
+        w1g = torch.empty((P * E, Di, hmax), dtype=shard.w1.dtype, device=shard.w1.device)
+        w2g = torch.empty((P * E, hmax, Do), dtype=shard.w2.dtype, device=shard.w2.device)
+        b1g = torch.empty((P * E, hmax), dtype=shard.b1.dtype, device=shard.b1.device)
+        dist.all_gather_into_tensor(w1g, padded(shard.w1, 2), group=group)
+        dist.all_gather_into_tensor(w2g, padded(shard.w2, 1), group=group)
+        dist.all_gather_into_tensor(b1g, padded(shard.b1, 1), group=group)
+        w1g, w2g = w1g.view(P, E, Di, hmax), w2g.view(P, E, hmax, Do)
+        b1g = b1g.view(P, E, hmax)
+        b2f = b2
+        if b2f is None or _rank(group) != 0:
+            b2f = torch.empty((E, Do), dtype=shard.b1.dtype, device=shard.w1.device) \
+                if b2 is None else b2
+        b2f = b2f.contiguous()
+        dist.broadcast(b2f, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                       group=group)
+        w1 = torch.cat([w1g[r, :, :, :hidden_sizes[r]] for r in range(P)], dim=2)
+        w2 = torch.cat([w2g[r, :, :hidden_sizes[r], :] for r in range(P)], dim=1)
+        b1 = torch.cat([b1g[r, :, :hidden_sizes[r]] for r in range(P)], dim=1)
+    return MoeLayerParams(w1, b1, w2, b2f, activation)
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+# -------------------------------------------------------------- steps -----
+@dataclass
+class DistStepResult:
+    y: torch.Tensor            # local rows (data-centric / reduce-scatter) or global (all-reduce)
+    grads: object              # gw1, gb1, gw2, gb2, gx
+    collectives: List[str] = field(default_factory=list)
+
+
+def data_centric_step(local_x, local_assign, local_gy, shard: ParamShard, b2, hidden_sizes,
+                      activation: str, cache: PipelineSharedCache, compute: LocalCompute,
+                      group=None, grad_reduce: str = "all_reduce",
+                      side_stream: Optional[torch.cuda.Stream] = None) -> DistStepResult:
+    """dist_sim.cpp:352-452 with real collectives.  Returns this rank's y
+    rows and the summed parameter gradients (all_reduce: full tensors on every
+    rank, as the reference; reduce_scatter: each rank's H-slice of gw1 / gb1 /
+    gw2, and gb2 on rank 0)."""
+    log = ["param_all_gather"]
+    full = gather_params(shard, b2, hidden_sizes, activation, group, side_stream)
+    if side_stream is not None:
+        torch.cuda.current_stream().wait_stream(side_stream)
+    cache.fill(0, full)
+    p = cache.params()
+    y, stash = compute.forward(local_x, p, local_assign, True)
+    g = compute.backward(stash, p, local_gy)
+    if grad_reduce == "all_reduce":
+        for t in (g.gw1, g.gb1, g.gw2, g.gb2):
+            dist.all_reduce(t, group=group)
+        log.append("grad_all_reduce")
+        return DistStepResult(y, g, log)
+    # reduce-scatter along H to the shard owners (half the traffic)
+    P, r = _ws(group), _rank(group)
+    off = shard.hidden_offset
+    h = hidden_sizes[r]
+    hmax = max(hidden_sizes)
+    from .moe_layer import MoeGrads
+    outs = []
+    for t, dim in ((g.gw1, 2), (g.gb1, 1), (g.gw2, 1)):
+        parts = []
+        o = 0
+        for hr in hidden_sizes:
+            sl = t.narrow(dim, o, hr)
+            if hr < hmax:
+                shp = list(sl.shape)
+                shp[dim] = hmax - hr
+                sl = torch.cat([sl, torch.zeros(shp, dtype=t.dtype, device=t.device)], dim=dim)
+            parts.append(sl.movedim(dim, 0).contiguous())
+            o += hr
+        inp = torch.cat(parts)  # [P*hmax, ...] rank-major
+        out = torch.empty_like(parts[0])
+        dist.reduce_scatter_tensor(out, inp, group=group)
+        outs.append(out[:h].movedim(0, dim).contiguous())
+    dist.reduce(g.gb2, dst=dist.get_global_rank(group, 0) if group is not None else 0,
+                group=group)
+    log.append("grad_reduce_scatter")
+    del off
+    return DistStepResult(y, MoeGrads(outs[0], outs[1], outs[2], g.gb2 if r == 0 else None,
+                                      g.gx), log)
+
+
+def model_centric_step(local_x, local_assign, local_gy, shard: ParamShard, b2, activation: str,
+                       compute: LocalCompute, group=None,
+                       reduce: str = "all_reduce") -> DistStepResult:
+    """dist_sim.cpp:454-601 with real collectives.  ``reduce`` = "all_reduce"
+    returns global y / gx on every rank (reference semantics);
+    "reduce_scatter" returns this rank's token rows only."""
+    from .moe_layer import MoeGrads, MoeLayerParams
+    r = _rank(group)
+    log = []
+    counts = _row_counts(local_x.shape[0], group, local_x.device)
+    x = all_gather_rows(local_x, counts, group)
+    a = all_gather_rows(local_assign.t().contiguous(), counts, group).t().contiguous()
+    log.append("token_all_gather")
+    p = MoeLayerParams(shard.w1, shard.b1, shard.w2, b2 if r == 0 else None, activation)
+    y_part, stash = compute.forward(x, p, a, r == 0)
+    y = _reduce_rows(y_part, counts, group, reduce)
+    log.append("output_" + reduce)
+    gy = all_gather_rows(local_gy, counts, group)
+    log.append("grad_all_gather")
+    g = compute.backward(stash, p, gy)
+    gx = _reduce_rows(g.gx, counts, group, reduce)
+    log.append("input_grad_" + reduce)
+    return DistStepResult(y, MoeGrads(g.gw1, g.gb1, g.gw2, g.gb2 if r == 0 else None, gx), log)
+
+
+def _reduce_rows(t: torch.Tensor, counts: Sequence[int], group, how: str) -> torch.Tensor:
+    if how == "all_reduce":
+        dist.all_reduce(t, group=group)
+        return t
+    P, r, m = _ws(group), _rank(group), max(counts)
+    if all(c == m for c in counts):
+        out = torch.empty((m,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        dist.reduce_scatter_tensor(out, t.contiguous(), group=group)
+        return out
+    parts, o = [], 0
+    for c in counts:
+        sl = t[o:o + c]
+        if c < m:
+            sl = torch.cat([sl, torch.zeros((m - c,) + tuple(t.shape[1:]), dtype=t.dtype,
+                                            device=t.device)])
+        parts.append(sl)
+        o += c
+    out = torch.empty((m,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    dist.reduce_scatter_tensor(out, torch.cat(parts), group=group)
+    return out[:counts[r]]
