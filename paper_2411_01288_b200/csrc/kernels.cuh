@@ -92,8 +92,16 @@ struct EssArgs {
   int max_tiles;
   int n_experts;
   float* partial;  // max_tiles x d
-  float* out;      // E x d
+  float* out;      // E x d, or null: no reduction (copy only)
+  void* copy_out;  // optional: rows also copied to expert-sorted order
+                   // (copy_out[p] = x[map(p)], padding slots -> zero rows)
 };
+
+// dst[p] = src[map(p)] for p < idx[E] (padding slots -> zero rows): the
+// expert-sorted copy of a token-order tensor, bandwidth-bound.
+hxm_status launch_gather_rows(hxm_dtype dt, const void* src, RowMap map, int64_t d,
+                              const int32_t* idx, int n_experts, int64_t bound, void* dst,
+                              cudaStream_t st);
 
 constexpr int kEssRows = 128;
 constexpr int kSimtRows = 64;     // SIMT ESMM tile rows

@@ -45,6 +45,8 @@ struct LayerWs {
   int32_t* etiles_off;
   int32_t* n_etiles;
   float* partial;
+  void* xs;   // x in expert-sorted slot order (forward stash)
+  void* gys;  // g_y in expert-sorted slot order (backward scratch)
   void* y1s;
   void* y2s;
   void* g1s;
@@ -85,6 +87,8 @@ LayerWs carve(Arena& ar, const hxm_layer_desc& d) {
   w.n_etiles = ar.take<int32_t>(1);
   w.partial = ar.take<float>(static_cast<size_t>(w.max_etiles) * std::max(d.hidden, d.d_out));
   const size_t stash = static_cast<size_t>(w.bound) * d.hidden * esize(d.dtype);
+  w.xs = ar.take<char>(static_cast<size_t>(w.bound) * d.d_in * esize(d.dtype));
+  w.gys = ar.take<char>(static_cast<size_t>(w.bound) * d.d_out * esize(d.dtype));
   w.y1s = ar.take<char>(stash);
   w.y2s = ar.take<char>(stash);
   w.g1s = ar.take<char>(stash);
@@ -183,11 +187,14 @@ hxm_status hxm_moe_forward(const hxm_layer_desc* d, const void* x, const void* w
                                       w.n_tiles_a, st));
   if (N == 0) return HXM_OK;
   const RowMap slot = map_slot(w.v, N);
+  // (0) expert-sorted copy of x: every later GEMM reads dense tiles
+  HXM_RETURN_IF(launch_gather_rows(dt, x, slot, d->d_in, w.idx, static_cast<int>(E), w.bound,
+                                   w.xs, st));
   // (1) y1 = x W1 + b1 ; y2 = F(y1)          (moe_layer.cpp:56-57)
   EsmmArgs a1{};
-  a1.a = x;
-  a1.amap = slot;
-  a1.a_rows = N;
+  a1.a = w.xs;
+  a1.amap = map_dense();
+  a1.a_rows = w.bound;
   a1.n_experts = E;
   a1.w = w1;
   a1.w_trans = 0;
@@ -256,20 +263,22 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
   es.max_tiles = w.max_etiles;
   es.n_experts = static_cast<int>(E);
   es.partial = w.partial;
-  es.out = gb2;
+  es.out = d->add_b2 ? gb2 : nullptr;
+  es.copy_out = w.gys;  // fused: expert-sorted copy of g_y
   const double kn = static_cast<double>(d->k * N);
   const double esz = static_cast<double>(esize(d->dtype));
   es.label = "ess_gb2";
   es.work = kn * Do * esz + static_cast<double>(E) * Do * 4.0;
-  if (d->add_b2) HXM_RETURN_IF(launch_ess(dt, es, st));
+  HXM_RETURN_IF(launch_ess(dt, es, st));
+  es.copy_out = nullptr;
   // (5) gW2 = sum_i ESTMM(y2_i, g_y, R_i)     (moe_layer.cpp:104)
   EstmmArgs t2{};
   t2.x1 = w.y2s;
   t2.m1 = map_dense();
-  t2.x2 = g_y;
-  t2.m2 = slot;
+  t2.x2 = w.gys;
+  t2.m2 = map_dense();
   t2.x1_rows = w.bound;
-  t2.x2_rows = N;
+  t2.x2_rows = w.bound;
   t2.d1 = H;
   t2.d2 = Do;
   t2.tiles = w.ktiles;
@@ -282,9 +291,9 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
   HXM_RETURN_IF(launch_estmm(dt, t2, st));
   // (6,7) g_y1 = (g_y W2^T) * F'(y1)          (moe_layer.cpp:105-108)
   EsmmArgs b6{};
-  b6.a = g_y;
-  b6.amap = slot;
-  b6.a_rows = N;
+  b6.a = w.gys;
+  b6.amap = map_dense();
+  b6.a_rows = w.bound;
   b6.n_experts = E;
   b6.w = w2;
   b6.w_trans = 1;  // W2 is E x H x Do; use W2[e]^T (Do x H)
@@ -312,11 +321,11 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
   HXM_RETURN_IF(launch_ess(dt, es, st));
   // (9) gW1 = sum_i ESTMM(x, g_y1_i, R_i)     (moe_layer.cpp:117)
   EstmmArgs t1 = t2;
-  t1.x1 = x;
-  t1.m1 = slot;
+  t1.x1 = w.xs;
+  t1.m1 = map_dense();
   t1.x2 = w.g1s;
   t1.m2 = map_dense();
-  t1.x1_rows = N;
+  t1.x1_rows = w.bound;
   t1.x2_rows = w.bound;
   t1.d1 = Di;
   t1.d2 = H;
