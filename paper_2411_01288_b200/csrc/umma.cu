@@ -12,8 +12,8 @@
 //          over <= kEstmmChunk-position chunks with fp32 red.add for split
 //          experts.
 //
-// Warp roles (192 threads): warp 0 = TMA producer (all 32 lanes issue gather4),
-// warp 1 = TMEM allocator + single-thread tcgen05.mma issuer, warps 2..5 =
+// Warp roles (320 threads): warp 0 = TMA producer (all 32 lanes issue gather4),
+// warp 1 = TMEM allocator + single-thread tcgen05.mma issuer, warps 2..9 =
 // epilogue (TMEM -> registers -> bias / activation / stores).  Pipelines:
 // smem ring full/empty (TMA <-> MMA) and a double-buffered TMEM accumulator
 // full/empty (MMA <-> epilogue), so tile i's epilogue overlaps tile i+1's MMA.
@@ -28,7 +28,8 @@ namespace {
 constexpr int BM = 128;  // UMMA M (rows per tile, TMEM lanes)
 constexpr int BK = 64;   // one 128-byte swizzle atom of bf16 per k-block
 constexpr int UK = 16;   // UMMA K for kind::f16
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;  // producer, MMA, 8 epilogue warps
 constexpr uint32_t kTmemCols = 512;
 constexpr int kABytes = BM * BK * 2;  // 16 KB
 
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -381,26 +382,43 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
     }
   } else {
     // ================================ epilogue ============================
-    const int lg = warp & 3;  // TMEM lane group this warp may access
+    // 8 warps: warp w reads TMEM lane group (w % 4) -- the hardware rule --
+    // and column half (w - 2) / 4 of the accumulator, so two warps per SMSP
+    // overlap TMEM loads, math and global traffic.
+    constexpr int HB = BN / 2;
+    const int lg = warp & 3;
+    const int half = (warp - 2) / 4;
     const int row = lg * 32 + lane;
     int acc = 0;
     uint32_t aph = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
       const SegTile t = p.tiles[w / per_item];
       const int rem = w % per_item;
-      mbar_wait(&tfull[acc], aph);
-      tc_fence_after();
-      const uint32_t taddr = tmem + (static_cast<uint32_t>(lg * 32) << 16) + acc * BN;
       if (!ESTMM) {
-        const int n0 = rem * BN;
+        const int n0 = rem * BN + half * HB;
         const int q = t.begin + row;
         const bool valid = q < t.end;
         const int orow = valid ? p.omap(q) : -1;
         const int N = p.N;
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        const bool bwd = p.epi == EPI_BWD_ACT;
+        // F'(y1) operand: issued before the accumulator wait so the loads
+        // overlap this tile's MMA
+        uint4 yv[HB / 8];
+        if (bwd && valid) {
+          const uint4* y4 = reinterpret_cast<const uint4*>(
+              static_cast<const __nv_bfloat16*>(p.y1s) + static_cast<int64_t>(q) * N + n0);
+#pragma unroll
+          for (int i = 0; i < HB / 8; ++i) yv[i] = __ldg(y4 + i);
+        }
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+        const uint32_t taddr =
+            tmem + (static_cast<uint32_t>(lg * 32) << 16) + acc * BN + half * HB;
+#pragma unroll
+        for (int c0 = 0; c0 < HB; c0 += 32) {
           uint32_t r[32];
           tmem_ld32(taddr + c0, r);
-          if (c0 + 32 == BN) {
+          if (c0 + 32 == HB) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -410,28 +428,29 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-          if (p.bias && p.epi != EPI_BWD_ACT) {
-            const float4* b4 = reinterpret_cast<const float4*>(p.bias + static_cast<int64_t>(t.expert) * N + n);
+          if (p.bias && !bwd) {
+            const float4* b4 =
+                reinterpret_cast<const float4*>(p.bias + static_cast<int64_t>(t.expert) * N + n);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const float4 b = __ldg(b4 + i);
               v[4 * i] += b.x; v[4 * i + 1] += b.y; v[4 * i + 2] += b.z; v[4 * i + 3] += b.w;
             }
           }
-          if (p.epi == EPI_FWD_ACT || p.epi == EPI_BWD_ACT) {
+          if (p.epi == EPI_FWD_ACT || bwd) {
             const int64_t off = static_cast<int64_t>(q) * N + n;
             uint4* o1 = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out1) + off);
             if (orow < 0) {  // padding slot: zero rows in the sorted stash
 #pragma unroll
               for (int i = 0; i < 4; ++i) o1[i] = make_uint4(0, 0, 0, 0);
-              if (p.epi == EPI_FWD_ACT) {
+              if (!bwd) {
                 uint4* o2 = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out2) + off);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) o2[i] = make_uint4(0, 0, 0, 0);
               }
               continue;
             }
-            if (p.epi == EPI_FWD_ACT) {
+            if (!bwd) {
               uint4* o2 = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out2) + off);
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
@@ -444,11 +463,9 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
                                    pack_bf16(a[4], a[5]), pack_bf16(a[6], a[7]));
               }
             } else {
-              const uint4* y4 = reinterpret_cast<const uint4*>(
-                  static_cast<const __nv_bfloat16*>(p.y1s) + off);
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
-                const uint4 yy = y4[i];
+                const uint4 yy = yv[c0 / 8 + i];
                 const __nv_bfloat16* yb = reinterpret_cast<const __nv_bfloat16*>(&yy);
                 float g[8];
 #pragma unroll
@@ -482,15 +499,20 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
       } else {
         const int mt = rem / p.n_nt, nt = rem % p.n_nt;
         const int m = mt * BM + row;
-        const int n0 = nt * BN;
+        const int n0 = nt * BN + half * HB;
         const bool valid = m < p.M;
         const bool split = t.flags & 1;
         const bool empty_seg = t.end <= t.begin;
         float* o = p.est_out + (static_cast<int64_t>(t.expert) * p.M + m) * p.N + n0;
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+        const uint32_t taddr =
+            tmem + (static_cast<uint32_t>(lg * 32) << 16) + acc * BN + half * HB;
+#pragma unroll
+        for (int c0 = 0; c0 < HB; c0 += 32) {
           uint32_t r[32];
           if (!empty_seg) tmem_ld32(taddr + c0, r);
-          if (c0 + 32 == BN) {
+          if (c0 + 32 == HB) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
