@@ -204,8 +204,12 @@ template <int BN>
 struct Cfg {
   static constexpr int kBBytes = BN * BK * 2;
   static constexpr int kStage = kABytes + kBBytes;
-  static constexpr int kStages = (200 * 1024) / kStage > 8 ? 8 : (200 * 1024) / kStage;
-  static constexpr int kSmem = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/;
+  // 227 KB opt-in smem = stages + per-epilogue-warp staging (4 KB each) +
+  // 1 KB alignment slack + barriers
+  static constexpr int kStaging = kEpiWarps * 4096;
+  static constexpr int kBudget = 232448 - 1024 - 256 - kStaging;
+  static constexpr int kStages = kBudget / kStage > 8 ? 8 : kBudget / kStage;
+  static constexpr int kSmem = kStages * kStage + kStaging + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 template <int BN, bool ESTMM>
@@ -214,7 +218,8 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStage);
+  uint8_t* staging = smem + C::kStages * C::kStage;  // kEpiWarps x 4 KB
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + C::kStaging);
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + 2;
@@ -384,11 +389,14 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
     // ================================ epilogue ============================
     // 8 warps: warp w reads TMEM lane group (w % 4) -- the hardware rule --
     // and column half (w - 2) / 4 of the accumulator, so two warps per SMSP
-    // overlap TMEM loads, math and global traffic.
+    // overlap TMEM loads, math and global traffic.  Each 32-row x 32-column
+    // chunk is transposed through a 4 KB per-warp staging buffer (16-byte
+    // chunks XOR-swizzled, conflict-free) so global stores / reductions
+    // cover whole row segments instead of 32 rows x 16 B per instruction.
     constexpr int HB = BN / 2;
     const int lg = warp & 3;
     const int half = (warp - 2) / 4;
-    const int row = lg * 32 + lane;
+    uint8_t* stg = staging + (warp - 2) * 4096;
     int acc = 0;
     uint32_t aph = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
@@ -396,19 +404,23 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
       const int rem = w % per_item;
       if (!ESTMM) {
         const int n0 = rem * BN + half * HB;
-        const int q = t.begin + row;
+        const int q0 = t.begin + lg * 32;  // first position of this warp's rows
+        const int q = q0 + lane;
         const bool valid = q < t.end;
         const int orow = valid ? p.omap(q) : -1;
         const int N = p.N;
         const bool bwd = p.epi == EPI_BWD_ACT;
+        const bool dense_out = p.epi == EPI_FWD_ACT || bwd;
         // F'(y1) operand: issued before the accumulator wait so the loads
         // overlap this tile's MMA
+        // (two 32-column chunks ahead; later chunks are fetched two ahead
+        // inside the loop to bound register pressure)
         uint4 yv[HB / 8];
+        const uint4* y4 = reinterpret_cast<const uint4*>(
+            static_cast<const __nv_bfloat16*>(p.y1s) + static_cast<int64_t>(q) * N + n0);
         if (bwd && valid) {
-          const uint4* y4 = reinterpret_cast<const uint4*>(
-              static_cast<const __nv_bfloat16*>(p.y1s) + static_cast<int64_t>(q) * N + n0);
 #pragma unroll
-          for (int i = 0; i < HB / 8; ++i) yv[i] = __ldg(y4 + i);
+          for (int i = 0; i < (HB / 8 < 8 ? HB / 8 : 8); ++i) yv[i] = __ldg(y4 + i);
         }
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
@@ -423,7 +435,10 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
           }
-          if (!valid) continue;
+          if (bwd && valid && c0 + 64 < HB) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) yv[(c0 + 64) / 8 + i] = __ldg(y4 + (c0 + 64) / 8 + i);
+          }
           const int n = n0 + c0;
           float v[32];
 #pragma unroll
@@ -437,73 +452,85 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
               v[4 * i] += b.x; v[4 * i + 1] += b.y; v[4 * i + 2] += b.z; v[4 * i + 3] += b.w;
             }
           }
-          if (p.epi == EPI_FWD_ACT || bwd) {
-            const int64_t off = static_cast<int64_t>(q) * N + n;
-            uint4* o1 = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out1) + off);
-            if (orow < 0) {  // padding slot: zero rows in the sorted stash
+          if (dense_out) {
+            // bf16 rows of the sorted stash: stage 2 KB per output
+            const bool pad = orow < 0;  // padding slot -> zero row
+            __syncwarp();
 #pragma unroll
-              for (int i = 0; i < 4; ++i) o1[i] = make_uint4(0, 0, 0, 0);
+            for (int j = 0; j < 4; ++j) {
+              uint32_t a1[4], a2[4];
               if (!bwd) {
-                uint4* o2 = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out2) + off);
 #pragma unroll
-                for (int i = 0; i < 4; ++i) o2[i] = make_uint4(0, 0, 0, 0);
-              }
-              continue;
-            }
-            if (!bwd) {
-              uint4* o2 = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out2) + off);
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                o1[i] = make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
-                                   pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
-                float a[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) a[j] = act_fwd(p.act, v[8 * i + j]);
-                o2[i] = make_uint4(pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]),
-                                   pack_bf16(a[4], a[5]), pack_bf16(a[6], a[7]));
-              }
-            } else {
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const uint4 yy = yv[c0 / 8 + i];
+                for (int i = 0; i < 4; ++i) {
+                  const float x0 = v[8 * j + 2 * i], x1 = v[8 * j + 2 * i + 1];
+                  a1[i] = pad ? 0u : pack_bf16(x0, x1);
+                  a2[i] = pad ? 0u : pack_bf16(act_fwd(p.act, x0), act_fwd(p.act, x1));
+                }
+              } else {
+                const uint4 yy = yv[c0 / 8 + j];
                 const __nv_bfloat16* yb = reinterpret_cast<const __nv_bfloat16*>(&yy);
-                float g[8];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) g[j] = v[8 * i + j] * act_bwd(p.act, __bfloat162float(yb[j]));
-                o1[i] = make_uint4(pack_bf16(g[0], g[1]), pack_bf16(g[2], g[3]),
-                                   pack_bf16(g[4], g[5]), pack_bf16(g[6], g[7]));
+                for (int i = 0; i < 4; ++i) {
+                  const float g0 = v[8 * j + 2 * i] * act_bwd(p.act, __bfloat162float(yb[2 * i]));
+                  const float g1 = v[8 * j + 2 * i + 1] * act_bwd(p.act, __bfloat162float(yb[2 * i + 1]));
+                  a1[i] = pad ? 0u : pack_bf16(g0, g1);
+                }
+              }
+              const int sw = (j ^ (lane & 3)) * 16;
+              *reinterpret_cast<uint4*>(stg + lane * 64 + sw) = make_uint4(a1[0], a1[1], a1[2], a1[3]);
+              if (!bwd)
+                *reinterpret_cast<uint4*>(stg + 2048 + lane * 64 + sw) =
+                    make_uint4(a2[0], a2[1], a2[2], a2[3]);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int rr = i * 8 + lane / 4, cc = lane % 4;
+              const bool ok = q0 + rr < t.end;
+              const int so = rr * 64 + ((cc ^ (rr & 3)) * 16);
+              const int64_t off = static_cast<int64_t>(q0 + rr) * N + n + cc * 8;
+              if (ok) {
+                *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out1) + off) =
+                    *reinterpret_cast<const uint4*>(stg + so);
+                if (!bwd)
+                  *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out2) + off) =
+                      *reinterpret_cast<const uint4*>(stg + 2048 + so);
               }
             }
           } else {
-            if (orow < 0) continue;
-            float* o = p.out_f32 + static_cast<int64_t>(orow) * N + n;
-            float4* o4 = reinterpret_cast<float4*>(o);
-            if (p.epi == EPI_WRITE) {
+            // fp32 rows scattered to token order: stage 4 KB (32 x 128 B)
+            __syncwarp();
 #pragma unroll
-              for (int i = 0; i < 8; ++i)
-                o4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-            } else if (p.epi == EPI_ACCUM) {
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<float4*>(stg + lane * 128 + ((j ^ (lane & 7)) * 16)) =
+                  make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            __syncwarp();
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                float4 c = o4[i];
-                c.x += v[4 * i]; c.y += v[4 * i + 1]; c.z += v[4 * i + 2]; c.w += v[4 * i + 3];
-                o4[i] = c;
+            for (int i = 0; i < 8; ++i) {
+              const int rr = i * 4 + lane / 8, cc = lane % 8;
+              const int orr = __shfl_sync(0xffffffffu, orow, rr);
+              const float4 val = *reinterpret_cast<const float4*>(stg + rr * 128 + ((cc ^ (rr & 7)) * 16));
+              if (orr < 0) continue;
+              float* o = p.out_f32 + static_cast<int64_t>(orr) * N + n + cc * 4;
+              if (p.epi == EPI_WRITE) {
+                *reinterpret_cast<float4*>(o) = val;
+              } else if (p.epi == EPI_ACCUM) {
+                float4 c = *reinterpret_cast<float4*>(o);
+                c.x += val.x; c.y += val.y; c.z += val.z; c.w += val.w;
+                *reinterpret_cast<float4*>(o) = c;
+              } else {
+                red_add_v4(o, val.x, val.y, val.z, val.w);
               }
-            } else {
-#pragma unroll
-              for (int i = 0; i < 8; ++i)
-                red_add_v4(o + 4 * i, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
             }
           }
         }
       } else {
         const int mt = rem / p.n_nt, nt = rem % p.n_nt;
-        const int m = mt * BM + row;
+        const int m0 = mt * BM + lg * 32;  // first output row of this warp
         const int n0 = nt * BN + half * HB;
-        const bool valid = m < p.M;
         const bool split = t.flags & 1;
         const bool empty_seg = t.end <= t.begin;
-        float* o = p.est_out + (static_cast<int64_t>(t.expert) * p.M + m) * p.N + n0;
+        float* obase = p.est_out + static_cast<int64_t>(t.expert) * p.M * p.N;
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
         const uint32_t taddr =
@@ -511,29 +538,31 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
 #pragma unroll
         for (int c0 = 0; c0 < HB; c0 += 32) {
           uint32_t r[32];
-          if (!empty_seg) tmem_ld32(taddr + c0, r);
+          if (!empty_seg) {
+            tmem_ld32(taddr + c0, r);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = 0u;
+          }
           if (c0 + 32 == HB) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
           }
-          if (!valid) continue;
-          float4* o4 = reinterpret_cast<float4*>(o + c0);
-          if (empty_seg) {
+          __syncwarp();
 #pragma unroll
-            for (int i = 0; i < 8; ++i) o4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-            continue;
-          }
-          if (split) {
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<uint4*>(stg + lane * 128 + ((j ^ (lane & 7)) * 16)) =
+                make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+          __syncwarp();
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-              red_add_v4(o + c0 + 4 * i, __uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
-                         __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
-          } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              o4[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
-                                  __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+          for (int i = 0; i < 8; ++i) {
+            const int rr = i * 4 + lane / 8, cc = lane % 8;
+            const float4 val = *reinterpret_cast<const float4*>(stg + rr * 128 + ((cc ^ (rr & 7)) * 16));
+            if (m0 + rr >= p.M) continue;
+            float* o = obase + static_cast<int64_t>(m0 + rr) * p.N + n0 + c0 + cc * 4;
+            if (split && !empty_seg) red_add_v4(o, val.x, val.y, val.z, val.w);
+            else *reinterpret_cast<float4*>(o) = val;
           }
         }
       }
