@@ -133,6 +133,23 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+// same load without the completion wait (pair with tmem_wait)
+__device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c),
                "f"(d)
@@ -212,8 +229,13 @@ struct Cfg {
   static constexpr int kSmem = kStages * kStage + kStaging + 1024 /*align*/ + 256 /*barriers*/;
 };
 
-template <int BN, bool ESTMM>
+// MODE: 0 = ESMM, fp32 write / accumulate / reduce epilogue; 1 = ESMM with
+// bias + activation into the bf16 stash (y1, y2); 2 = ESMM times F'(y1) into
+// the bf16 g_y1 stash; 3 = ESTMM.  One instantiation per mode keeps each
+// epilogue's register footprint to what it uses.
+template <int BN, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant__ UParams p) {
+  constexpr bool ESTMM = MODE == 3;
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -409,8 +431,8 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
         const bool valid = q < t.end;
         const int orow = valid ? p.omap(q) : -1;
         const int N = p.N;
-        const bool bwd = p.epi == EPI_BWD_ACT;
-        const bool dense_out = p.epi == EPI_FWD_ACT || bwd;
+        constexpr bool bwd = MODE == 2;
+        constexpr bool dense_out = MODE == 1 || MODE == 2;
         // F'(y1) operand: issued before the accumulator wait so the loads
         // overlap this tile's MMA
         // (two 32-column chunks ahead; later chunks are fetched two ahead
@@ -422,19 +444,30 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
 #pragma unroll
           for (int i = 0; i < (HB / 8 < 8 ? HB / 8 : 8); ++i) yv[i] = __ldg(y4 + i);
         }
+        // bias of this warp's HB columns: lane l holds columns 4l..4l+3,
+        // broadcast by shuffles (loaded before the wait)
+        float4 bl = make_float4(0.f, 0.f, 0.f, 0.f);
+        const bool has_bias = p.bias && !bwd;
+        if (has_bias && lane * 4 < HB)
+          bl = __ldg(reinterpret_cast<const float4*>(p.bias + static_cast<int64_t>(t.expert) * N +
+                                                     n0) + lane);
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
         const uint32_t taddr =
             tmem + (static_cast<uint32_t>(lg * 32) << 16) + acc * BN + half * HB;
+        uint32_t rbuf[2][32];
+        tmem_ld32_async(taddr, rbuf[0]);
+        tmem_wait();
+        if (HB == 32) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
 #pragma unroll
         for (int c0 = 0; c0 < HB; c0 += 32) {
-          uint32_t r[32];
-          tmem_ld32(taddr + c0, r);
-          if (c0 + 32 == HB) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
-          }
+          uint32_t (&r)[32] = rbuf[(c0 / 32) & 1];
+          // next chunk's TMEM load overlaps this chunk's math
+          if (c0 + 32 < HB) tmem_ld32_async(taddr + c0 + 32, rbuf[((c0 / 32) + 1) & 1]);
           if (bwd && valid && c0 + 64 < HB) {
 #pragma unroll
             for (int i = 0; i < 4; ++i) yv[(c0 + 64) / 8 + i] = __ldg(y4 + (c0 + 64) / 8 + i);
@@ -443,13 +476,14 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-          if (p.bias && !bwd) {
-            const float4* b4 =
-                reinterpret_cast<const float4*>(p.bias + static_cast<int64_t>(t.expert) * N + n);
+          if (has_bias) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const float4 b = __ldg(b4 + i);
-              v[4 * i] += b.x; v[4 * i + 1] += b.y; v[4 * i + 2] += b.z; v[4 * i + 3] += b.w;
+            for (int i = 0; i < 32; i += 4) {
+              const int src = (c0 + i) / 4;
+              v[i] += __shfl_sync(0xffffffffu, bl.x, src);
+              v[i + 1] += __shfl_sync(0xffffffffu, bl.y, src);
+              v[i + 2] += __shfl_sync(0xffffffffu, bl.z, src);
+              v[i + 3] += __shfl_sync(0xffffffffu, bl.w, src);
             }
           }
           if (dense_out) {
@@ -521,6 +555,14 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
               } else {
                 red_add_v4(o, val.x, val.y, val.z, val.w);
               }
+            }
+          }
+          if (c0 + 32 < HB) {
+            tmem_wait();
+            if (c0 + 64 >= HB) {  // last TMEM load landed: free the accumulator
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&tempty[acc]);
             }
           }
         }
@@ -622,10 +664,10 @@ int pick_bn(int64_t n) {
   return 0;
 }
 
-template <int BN, bool ESTMM>
+template <int BN, int MODE>
 hxm_status launch_bn(const UParams& prm, int max_work, cudaStream_t st) {
   using C = Cfg<BN>;
-  auto kern = umma_kernel<BN, ESTMM>;
+  auto kern = umma_kernel<BN, MODE>;
   static bool attr_set = false;
   if (!attr_set) {
     HXM_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
@@ -639,13 +681,13 @@ hxm_status launch_bn(const UParams& prm, int max_work, cudaStream_t st) {
   return HXM_OK;
 }
 
-template <bool ESTMM>
-hxm_status launch_any(int bn, const UParams& prm, int max_work, cudaStream_t st) {
+template <int MODE>
+hxm_status launch_bn_any(int bn, const UParams& prm, int max_work, cudaStream_t st) {
   switch (bn) {
-    case 256: return launch_bn<256, ESTMM>(prm, max_work, st);
-    case 192: return launch_bn<192, ESTMM>(prm, max_work, st);
-    case 128: return launch_bn<128, ESTMM>(prm, max_work, st);
-    default: return launch_bn<64, ESTMM>(prm, max_work, st);
+    case 256: return launch_bn<256, MODE>(prm, max_work, st);
+    case 192: return launch_bn<192, MODE>(prm, max_work, st);
+    case 128: return launch_bn<128, MODE>(prm, max_work, st);
+    default: return launch_bn<64, MODE>(prm, max_work, st);
   }
 }
 
@@ -710,7 +752,10 @@ hxm_status umma_esmm(const EsmmArgs& a, cudaStream_t st) {
   prm.out1 = a.out1;
   prm.out2 = a.out2;
   prm.y1s = a.y1s;
-  return launch_any<false>(bn, prm, a.max_tiles * prm.n_nt, st);
+  const int work = a.max_tiles * prm.n_nt;
+  if (a.epi == EPI_FWD_ACT) return launch_bn_any<1>(bn, prm, work, st);
+  if (a.epi == EPI_BWD_ACT) return launch_bn_any<2>(bn, prm, work, st);
+  return launch_bn_any<0>(bn, prm, work, st);
 }
 
 hxm_status umma_estmm(const EstmmArgs& a, cudaStream_t st) {
@@ -743,7 +788,7 @@ hxm_status umma_estmm(const EstmmArgs& a, cudaStream_t st) {
   prm.tiles = a.tiles;
   prm.n_tiles = a.n_tiles;
   prm.est_out = a.out;
-  return launch_any<true>(bn, prm, a.max_tiles * prm.n_mt * prm.n_nt, st);
+  return launch_bn_any<3>(bn, prm, a.max_tiles * prm.n_mt * prm.n_nt, st);
 }
 
 }  // namespace hxm
