@@ -312,3 +312,16 @@ def test_layer_routing_validation():
     ok = H.synthesize_routing(4, 2, 1, "uniform", 1)
     with pytest.raises(H.ShapeError):
         H.moe_forward(x[:3], p, ok)
+
+
+def test_cpp_dropin():
+    """The reference's own C++ types and KATs through include/hexamoe_moekit.hpp
+    (C++ shim over the C ABI) -- built by oracle/Makefile from the reference
+    headers, see INTEGRATION.md."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(__file__)), "oracle", "_ref", "dropin_test")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/dropin_test not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failures" in r.stdout
