@@ -133,6 +133,27 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+// TMA tile store smem -> global (bulk-group completion)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0,
+                                             int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map),
+      "r"(c0), "r"(c1), "r"(smem_u32(src))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // same load without the completion wait (pair with tmem_wait)
 __device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
@@ -200,6 +221,8 @@ __device__ __forceinline__ float act_bwd(int act, float x) {
 struct UParams {
   CUtensorMap tmA;  // ESMM A / ESTMM X1
   CUtensorMap tmB;  // ESMM W / ESTMM X2
+  CUtensorMap tmO1;  // MODE 1/2: dense bf16 stash output(s), 32 x 32 boxes
+  CUtensorMap tmO2;
   RowMap amap;      // gather map of A (ESMM rows / ESTMM X1 rows)
   RowMap bmap;      // ESTMM X2 rows
   int a_gather, b_gather, b_kmajor;
@@ -489,6 +512,10 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
           if (dense_out) {
             // bf16 rows of the sorted stash: stage 2 KB per output
             const bool pad = orow < 0;  // padding slot -> zero row
+            // all 32 rows of this warp inside the segment (always, for the
+            // layer's 64-aligned segments): TMA-store the staged 32 x 32 box
+            const bool full_warp = q0 + 31 < t.end;
+            if (lane == 0) bulk_wait_read0();  // staging free again
             __syncwarp();
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -510,11 +537,23 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
                   a1[i] = pad ? 0u : pack_bf16(g0, g1);
                 }
               }
-              const int sw = (j ^ (lane & 3)) * 16;
+              // 64B swizzle (TMA pattern: chunk ^= (row >> 1) & 3) for the
+              // TMA store; plain XOR for the LDS read-back path
+              const int sw = (full_warp ? (j ^ ((lane >> 1) & 3)) : (j ^ (lane & 3))) * 16;
               *reinterpret_cast<uint4*>(stg + lane * 64 + sw) = make_uint4(a1[0], a1[1], a1[2], a1[3]);
               if (!bwd)
                 *reinterpret_cast<uint4*>(stg + 2048 + lane * 64 + sw) =
                     make_uint4(a2[0], a2[1], a2[2], a2[3]);
+            }
+            if (full_warp) {
+              fence_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_2d(&p.tmO1, stg, n, q0);
+                if (!bwd) tma_store_2d(&p.tmO2, stg + 2048, n, q0);
+                bulk_commit();
+              }
+              goto chunk_done;
             }
             __syncwarp();
 #pragma unroll
@@ -557,6 +596,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
               }
             }
           }
+        chunk_done:
           if (c0 + 32 < HB) {
             tmem_wait();
             if (c0 + 64 >= HB) {  // last TMEM load landed: free the accumulator
@@ -610,6 +650,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
       }
       if (++acc == 2) { acc = 0; aph ^= 1; }
     }
+    if (lane == 0) bulk_wait0();  // this warp's TMA stores are complete
   }
   tc_fence_before();
   __syncthreads();
@@ -640,9 +681,11 @@ EncodeFn encoder() {
 }
 
 // bf16 tensor of `rank` dims (dims[0] innermost, element counts), row pitch
-// strides in bytes for dims 1.., box sizes, 128B swizzle, OOB -> zeros.
+// strides in bytes for dims 1.., box sizes, 128B (default) or 64B swizzle,
+// OOB -> zeros.
 bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
-              const uint64_t* strides_bytes, const uint32_t* box) {
+              const uint64_t* strides_bytes, const uint32_t* box,
+              CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeFn enc = encoder();
   if (!enc) return false;
   cuuint64_t gd[3], gs[2];
@@ -653,7 +696,7 @@ bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
   }
   for (int i = 0; i + 1 < rank; ++i) gs[i] = strides_bytes[i];
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), gd, gs,
-                   bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -752,6 +795,18 @@ hxm_status umma_esmm(const EsmmArgs& a, cudaStream_t st) {
   prm.out1 = a.out1;
   prm.out2 = a.out2;
   prm.y1s = a.y1s;
+  if (a.epi == EPI_FWD_ACT || a.epi == EPI_BWD_ACT) {
+    // dense bf16 stash outputs (same row space as the dense A operand):
+    // 32 x 32 boxes stored by TMA from the epilogue's 64B-swizzled staging
+    const uint64_t dims[2] = {static_cast<uint64_t>(a.d2), static_cast<uint64_t>(a.a_rows)};
+    const uint64_t strides[1] = {static_cast<uint64_t>(a.d2) * 2};
+    const uint32_t box[2] = {32, 32};
+    if (!make_map(&prm.tmO1, a.out1, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B))
+      return invalid_arg("umma_esmm: cannot encode the output tensor map");
+    if (a.epi == EPI_FWD_ACT &&
+        !make_map(&prm.tmO2, a.out2, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B))
+      return invalid_arg("umma_esmm: cannot encode the output tensor map");
+  }
   const int work = a.max_tiles * prm.n_nt;
   if (a.epi == EPI_FWD_ACT) return launch_bn_any<1>(bn, prm, work, st);
   if (a.epi == EPI_BWD_ACT) return launch_bn_any<2>(bn, prm, work, st);
