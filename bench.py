@@ -252,7 +252,7 @@ def run_ours(args, cfg, rank, ws, local):
     launches0 = L.hxm_launch_count()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local, period=0.005)
     barrier(ws)
     with clocks:
         L.hxm_profile_enable(1)

@@ -193,8 +193,8 @@ hxm_status gather_typed(const void* src, RowMap map, int64_t d, const int32_t* i
 
 hxm_status launch_gather_rows(hxm_dtype dt, const void* src, RowMap map, int64_t d,
                               const int32_t* idx, int n_experts, int64_t bound, void* dst,
-                              cudaStream_t st) {
-  ProfScope ps(st, "gather_rows", 0.0, WORK_BYTES);
+                              cudaStream_t st, double work_bytes) {
+  ProfScope ps(st, "gather_rows", work_bytes, WORK_BYTES);
   return dt == HXM_BF16 ? gather_typed<__nv_bfloat16>(src, map, d, idx, n_experts, bound, dst, st)
                         : gather_typed<float>(src, map, d, idx, n_experts, bound, dst, st);
 }

@@ -101,7 +101,7 @@ struct EssArgs {
 // expert-sorted copy of a token-order tensor, bandwidth-bound.
 hxm_status launch_gather_rows(hxm_dtype dt, const void* src, RowMap map, int64_t d,
                               const int32_t* idx, int n_experts, int64_t bound, void* dst,
-                              cudaStream_t st);
+                              cudaStream_t st, double work_bytes = 0.0);
 
 constexpr int kEssRows = 128;
 constexpr int kSimtRows = 64;     // SIMT ESMM tile rows

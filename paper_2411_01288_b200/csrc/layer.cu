@@ -188,8 +188,11 @@ hxm_status hxm_moe_forward(const hxm_layer_desc* d, const void* x, const void* w
   if (N == 0) return HXM_OK;
   const RowMap slot = map_slot(w.v, N);
   // (0) expert-sorted copy of x: every later GEMM reads dense tiles
+  // algorithmic bytes: every routed slot's row read once and written once
   HXM_RETURN_IF(launch_gather_rows(dt, x, slot, d->d_in, w.idx, static_cast<int>(E), w.bound,
-                                   w.xs, st));
+                                   w.xs, st,
+                                   2.0 * static_cast<double>(slots) * d->d_in *
+                                       static_cast<double>(esize(d->dtype))));
   // (1) y1 = x W1 + b1 ; y2 = F(y1)          (moe_layer.cpp:56-57)
   EsmmArgs a1{};
   a1.a = w.xs;
