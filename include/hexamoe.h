@@ -177,10 +177,12 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* desc, const void* x,
                             float* gx, hxm_stream_t stream);
 
 /* Debug/parity: copy the stash of choice `choice` back to token order as
- * fp32 N x H (y1 = pre-activation, y2 = activation). */
+ * fp32 N x H.  The device stash keeps what the backward needs of the
+ * reference's (y1, y2) pair (moe_layer.hpp:39-46): dact = F'(y1) and
+ * y2 = F(y1). */
 hxm_status hxm_moe_stash_export(const hxm_layer_desc* desc,
                                 const void* workspace, int64_t choice,
-                                float* y1, float* y2, hxm_stream_t stream);
+                                float* dact, float* y2, hxm_stream_t stream);
 
 /* Algorithmic work counters of the last layer call (OpStats, es_ops.hpp:17-24):
  * MACs on real tokens only = k*N*(D_i*H + H*D_o) per direction. */

@@ -43,76 +43,71 @@ __device__ __forceinline__ void store_vec(T* p, const float (&v)[VEC]) {
 
 template <class T, int VEC>
 __global__ void __launch_bounds__(NT) ess_partial(EssArgs a) {
+  // grid: x = segment tile (<= 128 positions), y = column slab of 32 vector
+  // groups (one per lane); the 8 warps split the tile's rows, each keeping
+  // U = 4 row loads in flight, and are combined in fixed order through smem.
   const int ti = blockIdx.x;
   if (ti >= *a.n_tiles) return;
   const SegTile tile = a.tiles[ti];
   const T* X = static_cast<const T*>(a.x);
   const int64_t D = a.d;
   const int col_groups = static_cast<int>((D + VEC - 1) / VEC);
-  int ct = col_groups < NT ? col_groups : NT;   // threads along columns
-  ct = (ct + 31) / 32 * 32;
-  const int rp = NT / ct;                        // row parallelism
-  const int cid = threadIdx.x % ct, rid = threadIdx.x / ct;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  constexpr int W = NT / 32;
+  const int cg = blockIdx.y * 32 + lane;
   __shared__ int rows[kEssRows];
-  __shared__ float red[NT * VEC];
+  __shared__ float red[W][32 * VEC];
   for (int i = threadIdx.x; i < kEssRows; i += NT) {
     const int64_t p = tile.begin + i;
     rows[i] = p < tile.end ? a.map(p) : -1;
   }
   __syncthreads();
   const int nrows = tile.end - tile.begin;
-  for (int cg0 = 0; cg0 < col_groups; cg0 += ct) {
-    const int cg = cg0 + cid;
-    float acc[VEC];
+  float acc[VEC];
 #pragma unroll
-    for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
-    if (rid < rp && cg < col_groups) {
-      constexpr int U = 4;  // rows in flight per thread
-      for (int r0 = rid; r0 < nrows; r0 += rp * U) {
-        float v[U][VEC];
-        int rr[U];
+  for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
+  if (cg < col_groups) {
+    constexpr int U = 4;  // rows in flight per thread
+    for (int r0 = warp; r0 < nrows; r0 += W * U) {
+      float v[U][VEC];
+      int rr[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int r = r0 + u * rp;
-          rr[u] = r < nrows ? rows[r] : -2;
-          if (rr[u] >= 0) {
-            load_vec<T, VEC>(X + static_cast<int64_t>(rr[u]) * D + static_cast<int64_t>(cg) * VEC,
-                             v[u]);
-          } else {
+      for (int u = 0; u < U; ++u) {
+        const int r = r0 + u * W;
+        rr[u] = r < nrows ? rows[r] : -2;
+        if (rr[u] >= 0) {
+          load_vec<T, VEC>(X + static_cast<int64_t>(rr[u]) * D + static_cast<int64_t>(cg) * VEC,
+                           v[u]);
+        } else {
 #pragma unroll
-            for (int i = 0; i < VEC; ++i) v[u][i] = 0.f;
-          }
+          for (int i = 0; i < VEC; ++i) v[u][i] = 0.f;
         }
+      }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
+      for (int u = 0; u < U; ++u) {
 #pragma unroll
-          for (int i = 0; i < VEC; ++i) acc[i] += v[u][i];
-          if (a.copy_out && rr[u] != -2) {  // padding slots copy as zero rows
-            T* dst = static_cast<T*>(a.copy_out) +
-                     (static_cast<int64_t>(tile.begin) + r0 + u * rp) * D +
-                     static_cast<int64_t>(cg) * VEC;
-            store_vec<T, VEC>(dst, v[u]);
-          }
+        for (int i = 0; i < VEC; ++i) acc[i] += v[u][i];
+        if (a.copy_out && rr[u] != -2) {  // padding slots copy as zero rows
+          T* dst = static_cast<T*>(a.copy_out) +
+                   (static_cast<int64_t>(tile.begin) + r0 + u * W) * D +
+                   static_cast<int64_t>(cg) * VEC;
+          store_vec<T, VEC>(dst, v[u]);
         }
       }
     }
-    if (rp > 1) {
+  }
+  if (!a.partial) return;
 #pragma unroll
-      for (int i = 0; i < VEC; ++i) red[threadIdx.x * VEC + i] = acc[i];
-      __syncthreads();
-      if (rid == 0) {
-        for (int q = 1; q < rp; ++q)
+  for (int i = 0; i < VEC; ++i) red[warp][lane * VEC + i] = acc[i];
+  __syncthreads();
+  // column sums in a fixed warp order (deterministic)
+  for (int c = threadIdx.x; c < 32 * VEC; c += NT) {
+    const int64_t col = static_cast<int64_t>(blockIdx.y) * 32 * VEC + c;
+    if (col >= D) continue;
+    float s = 0.f;
 #pragma unroll
-          for (int i = 0; i < VEC; ++i) acc[i] += red[(q * ct + cid) * VEC + i];
-      }
-      __syncthreads();
-    }
-    if (rid == 0 && cg < col_groups && a.partial) {
-      float* dst = a.partial + static_cast<int64_t>(ti) * D + static_cast<int64_t>(cg) * VEC;
-#pragma unroll
-      for (int i = 0; i < VEC; ++i)
-        if (static_cast<int64_t>(cg) * VEC + i < D) dst[i] = acc[i];
-    }
+    for (int w = 0; w < W; ++w) s += red[w][c];
+    a.partial[static_cast<int64_t>(ti) * D + col] = s;
   }
 }
 
@@ -132,8 +127,10 @@ hxm_status launch_typed(const EssArgs& a, cudaStream_t st) {
   if (a.max_tiles > 0) {
     const bool vec_ok = (a.d % V == 0) && (reinterpret_cast<uintptr_t>(a.x) % 16 == 0) &&
                         (reinterpret_cast<uintptr_t>(a.copy_out) % 16 == 0);
-    if (vec_ok) ess_partial<T, V><<<a.max_tiles, NT, 0, st>>>(a);
-    else ess_partial<T, 1><<<a.max_tiles, NT, 0, st>>>(a);
+    const int64_t groups = vec_ok ? ceil_div(a.d, V) : a.d;
+    dim3 grid(static_cast<unsigned>(a.max_tiles), static_cast<unsigned>(ceil_div(groups, 32)));
+    if (vec_ok) ess_partial<T, V><<<grid, NT, 0, st>>>(a);
+    else ess_partial<T, 1><<<grid, NT, 0, st>>>(a);
     HXM_CHECK_LAUNCH();
   }
   dim3 grid(static_cast<unsigned>(ceil_div(a.d, 256)), static_cast<unsigned>(a.n_experts));

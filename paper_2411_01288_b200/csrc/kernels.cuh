@@ -36,8 +36,8 @@ enum EpiMode : int {
   EPI_WRITE = 0,    // out_f32[omap(p)]  = acc + bias          (esmm write)
   EPI_ACCUM = 1,    // out_f32[omap(p)] += acc + bias          (esmm accumulate)
   EPI_ATOMIC = 2,   // red.add out_f32[omap(p)], acc (+bias)   (k-merged y, gx)
-  EPI_FWD_ACT = 3,  // out1[p] = acc + bias, out2[p] = F(.)    (stash y1, y2)
-  EPI_BWD_ACT = 4   // out1[p] = acc * F'(y1s[p])              (g_y1)
+  EPI_FWD_ACT = 3,  // y1 = acc + bias: out1[p] = F'(y1), out2[p] = F(y1)  (stash)
+  EPI_BWD_ACT = 4   // out1[p] = acc * y1s[p]  (y1s holds F'(y1))         (g_y1)
 };
 
 struct EsmmArgs {

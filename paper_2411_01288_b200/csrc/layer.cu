@@ -183,8 +183,13 @@ hxm_status hxm_moe_forward(const hxm_layer_desc* d, const void* x, const void* w
   }
   HXM_RETURN_IF(build_reindex_slots(assignments, slots, E, kSortedBlk, w.v, w.idx, w.rws,
                                     w.rws_bytes, status, st));
-  HXM_RETURN_IF(launch_tiles<int32_t>(w.idx, E, w.rows_a, false, w.tiles_a, w.tiles_a_off,
-                                      w.n_tiles_a, st));
+  // the three tilings of the index (ESMM tiles, ESTMM chunks, ESS tiles) in
+  // one launch; the backward reuses them from the stash
+  const TileSpec specs[3] = {
+      {w.rows_a, 0, w.tiles_a, w.tiles_a_off, w.n_tiles_a},
+      {kEstmmChunk, 1, w.ktiles, w.ktiles_off, w.n_ktiles},
+      {kEssRows, 0, w.etiles, w.etiles_off, w.n_etiles}};
+  HXM_RETURN_IF(launch_tiles3<int32_t>(w.idx, E, specs, 3, st));
   if (N == 0) return HXM_OK;
   const RowMap slot = map_slot(w.v, N);
   // (0) expert-sorted copy of x: every later GEMM reads dense tiles
@@ -250,10 +255,7 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
   const int64_t N = d->n_tokens, E = d->n_experts;
   const int64_t Di = d->d_in, H = d->hidden, Do = d->d_out;
   HXM_TRY_CUDA(cudaMemsetAsync(gx, 0, sizeof(float) * N * Di, st));
-  HXM_RETURN_IF(launch_tiles<int32_t>(w.idx, E, kEstmmChunk, true, w.ktiles, w.ktiles_off,
-                                      w.n_ktiles, st));
-  HXM_RETURN_IF(launch_tiles<int32_t>(w.idx, E, kEssRows, false, w.etiles, w.etiles_off,
-                                      w.n_etiles, st));
+  // tile tables were built by hxm_moe_forward (they live in the stash)
   const RowMap slot = map_slot(w.v, N > 0 ? N : 1);
   // (4) gb2 = sum_i ESS(g_y, R_i)             (moe_layer.cpp:103)
   EssArgs es{};

@@ -147,9 +147,10 @@ __global__ void scatter(const int32_t* __restrict__ a, int64_t n, int E,
 }
 
 int pick_chunk(int64_t n) {
-  // at most ~1024 chunks so K2's per-expert scan stays short
-  int64_t c = 256;
-  while (ceil_div(n, c) > 1024) c *= 2;
+  // >= 64 tokens per warp-chunk (enough warps to fill the GPU at the
+  // BASELINE sizes), at most ~2048 chunks so K2's per-expert scan stays short
+  int64_t c = 64;
+  while (ceil_div(n, c) > 2048) c *= 2;
   return static_cast<int>(c);
 }
 
@@ -193,13 +194,13 @@ hxm_status build_impl(const int32_t* a, int64_t n, int64_t E, int64_t blk,
 // with an empty segment still get one (empty) tile -- used by ESTMM so that
 // their zero gradient is written (es_ops.cpp:202 zero-initialised output).
 template <class IdxT>
-__global__ void build_tiles(const IdxT* __restrict__ idx, int E, int rows,
-                            int min_one, SegTile* __restrict__ tiles,
-                            int32_t* __restrict__ tile_off,
-                            int32_t* __restrict__ n_tiles) {
+__device__ void tile_pass(const IdxT* __restrict__ idx, int E, int rows, int min_one,
+                          SegTile* __restrict__ tiles, int32_t* __restrict__ tile_off,
+                          int32_t* __restrict__ n_tiles) {
   using Scan = cub::BlockScan<int32_t, 1024>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int32_t carry;
+  __syncthreads();
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   for (int e0 = 0; e0 < E; e0 += 1024) {
@@ -240,7 +241,28 @@ __global__ void build_tiles(const IdxT* __restrict__ idx, int E, int rows,
   }
 }
 
+template <class IdxT>
+__global__ void build_tiles(const IdxT* __restrict__ idx, int E, TileSpec a, TileSpec b,
+                            TileSpec c, int count) {
+  tile_pass<IdxT>(idx, E, a.rows, a.min_one, a.tiles, a.tile_off, a.n_tiles);
+  if (count > 1) tile_pass<IdxT>(idx, E, b.rows, b.min_one, b.tiles, b.tile_off, b.n_tiles);
+  if (count > 2) tile_pass<IdxT>(idx, E, c.rows, c.min_one, c.tiles, c.tile_off, c.n_tiles);
+}
+
 }  // namespace
+
+template <class IdxT>
+hxm_status launch_tiles3(const IdxT* idx, int64_t E, const TileSpec* specs, int count,
+                         cudaStream_t st) {
+  if (count < 1 || count > 3) return invalid_arg("launch_tiles3: 1..3 specs");
+  build_tiles<IdxT><<<1, 1024, 0, st>>>(idx, static_cast<int>(E), specs[0],
+                                        specs[count > 1 ? 1 : 0], specs[count > 2 ? 2 : 0],
+                                        count);
+  HXM_CHECK_LAUNCH();
+  return HXM_OK;
+}
+template hxm_status launch_tiles3<int32_t>(const int32_t*, int64_t, const TileSpec*, int,
+                                           cudaStream_t);
 
 size_t reindex_ws_bytes(int64_t n, int64_t E) {
   const int chunk = pick_chunk(n);
@@ -262,8 +284,8 @@ template <class IdxT>
 hxm_status launch_tiles(const IdxT* idx, int64_t E, int rows, bool min_one,
                         SegTile* tiles, int32_t* tile_off, int32_t* n_tiles,
                         cudaStream_t st) {
-  build_tiles<IdxT><<<1, 1024, 0, st>>>(idx, static_cast<int>(E), rows, min_one ? 1 : 0,
-                                        tiles, tile_off, n_tiles);
+  const TileSpec s{rows, min_one ? 1 : 0, tiles, tile_off, n_tiles};
+  build_tiles<IdxT><<<1, 1024, 0, st>>>(idx, static_cast<int>(E), s, s, s, 1);
   HXM_CHECK_LAUNCH();
   return HXM_OK;
 }

@@ -19,6 +19,19 @@ hxm_status launch_tiles(const IdxT* idx, int64_t E, int rows, bool min_one,
                         SegTile* tiles, int32_t* tile_off, int32_t* n_tiles,
                         cudaStream_t st);
 
+// Up to three tilings of the same index in one launch (the layer builds its
+// ESMM, ESTMM-chunk and ESS tables together).
+struct TileSpec {
+  int rows;
+  int min_one;
+  SegTile* tiles;
+  int32_t* tile_off;
+  int32_t* n_tiles;
+};
+template <class IdxT>
+hxm_status launch_tiles3(const IdxT* idx, int64_t E, const TileSpec* specs, int count,
+                         cudaStream_t st);
+
 int64_t max_tiles(int64_t n_padded_bound, int64_t E, int rows);
 
 }  // namespace hxm

@@ -99,15 +99,16 @@ __global__ void __launch_bounds__(NT) esmm_simt_kernel(EsmmArgs a) {
           T* o1 = static_cast<T*>(a.out1);
           T* o2 = static_cast<T*>(a.out2);
           const bool pad = orow < 0;
-          o1[p * N + n] = from_f32<T>(pad ? 0.f : v);
+          // stash (F'(y1), F(y1)) -- all the backward needs of y1
+          o1[p * N + n] = from_f32<T>(pad ? 0.f : act_derivative(a.act, v));
           o2[p * N + n] = from_f32<T>(pad ? 0.f : act_value(a.act, v));
           break;
         }
-        default: {  // EPI_BWD_ACT (no bias)
+        default: {  // EPI_BWD_ACT (no bias): g_y1 = g_y2 * F'(y1)
           T* o1 = static_cast<T*>(a.out1);
-          const T* y1 = static_cast<const T*>(a.y1s);
+          const T* dact = static_cast<const T*>(a.y1s);
           const bool pad = orow < 0;
-          const float g = acc[i][j] * act_derivative(a.act, to_f32(y1[p * N + n]));
+          const float g = acc[i][j] * to_f32(dact[p * N + n]);
           o1[p * N + n] = from_f32<T>(pad ? 0.f : g);
           break;
         }
@@ -220,7 +221,8 @@ hxm_status simt_estmm(hxm_dtype dt, const EstmmArgs& a, cudaStream_t st) {
 hxm_status zero_split_experts(const SegTile* tiles, const int32_t* n_tiles, int max_tiles,
                               int64_t slice, float* out, cudaStream_t st) {
   if (max_tiles <= 0) return HXM_OK;
-  dim3 grid(static_cast<unsigned>(std::min<int64_t>(64, ceil_div(slice, 1024))),
+  // blocks of non-split tiles exit at once; 16 blocks zero a split expert
+  dim3 grid(static_cast<unsigned>(std::min<int64_t>(16, ceil_div(slice, 1024))),
             static_cast<unsigned>(max_tiles));
   zero_split_kernel<<<grid, 256, 0, st>>>(tiles, n_tiles, slice, out);
   HXM_CHECK_LAUNCH();

@@ -195,27 +195,25 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
 }
-__device__ __forceinline__ float gelu_fast(float x) {
-  const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
-  float t;
-  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
-  return 0.5f * x * (1.f + t);
-}
-__device__ __forceinline__ float act_fwd(int act, float x) {
-  if (act == HXM_ACT_GELU) return gelu_fast(x);
-  if (act == HXM_ACT_RELU) return x > 0.f ? x : 0.f;
-  return x;
-}
-__device__ __forceinline__ float act_bwd(int act, float x) {
+// F(x) and F'(x) together (tensor.cpp:39-53, 62-72): GELU-tanh shares one
+// tanh.approx between the value and its exact derivative.
+__device__ __forceinline__ void act_both(int act, float x, float& f, float& df) {
   if (act == HXM_ACT_GELU) {
-    const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
+    const float x2 = x * x;
+    const float u = x * fmaf(0.7978845608028654f * 0.044715f, x2, 0.7978845608028654f);
     float t;
     asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
-    const float du = 0.7978845608028654f * (1.f + 3.f * 0.044715f * x * x);
-    return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * du;
+    const float hx = 0.5f * x;
+    f = fmaf(hx, t, hx);
+    const float du = fmaf(0.7978845608028654f * 3.f * 0.044715f, x2, 0.7978845608028654f);
+    df = fmaf(0.5f, t, 0.5f) + hx * fmaf(-t, t, 1.f) * du;
+  } else if (act == HXM_ACT_RELU) {
+    f = x > 0.f ? x : 0.f;
+    df = x > 0.f ? 1.f : 0.f;
+  } else {
+    f = x;
+    df = 1.f;
   }
-  if (act == HXM_ACT_RELU) return x > 0.f ? 1.f : 0.f;
-  return 1.f;
 }
 
 struct UParams {
@@ -237,6 +235,7 @@ struct UParams {
   void* out1;
   void* out2;
   const void* y1s;
+  float* colsum;  // MODE 2: per-(tile, lane group) column sums of the output
   float* est_out;
 };
 
@@ -456,10 +455,10 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
         const int N = p.N;
         constexpr bool bwd = MODE == 2;
         constexpr bool dense_out = MODE == 1 || MODE == 2;
-        // F'(y1) operand: issued before the accumulator wait so the loads
-        // overlap this tile's MMA
-        // (two 32-column chunks ahead; later chunks are fetched two ahead
-        // inside the loop to bound register pressure)
+        // F'(y1) operand (MODE 2, from the stash): issued before the
+        // accumulator wait so the loads overlap this tile's MMA (two 32-column
+        // chunks ahead; later chunks are fetched two ahead inside the loop to
+        // bound register pressure)
         uint4 yv[HB / 8];
         const uint4* y4 = reinterpret_cast<const uint4*>(
             static_cast<const __nv_bfloat16*>(p.y1s) + static_cast<int64_t>(q) * N + n0);
@@ -521,19 +520,23 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
             for (int j = 0; j < 4; ++j) {
               uint32_t a1[4], a2[4];
               if (!bwd) {
+                // stash = (F'(y1), F(y1)): everything the backward needs
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                  const float x0 = v[8 * j + 2 * i], x1 = v[8 * j + 2 * i + 1];
-                  a1[i] = pad ? 0u : pack_bf16(x0, x1);
-                  a2[i] = pad ? 0u : pack_bf16(act_fwd(p.act, x0), act_fwd(p.act, x1));
+                  float f0, d0, f1, d1;
+                  act_both(p.act, v[8 * j + 2 * i], f0, d0);
+                  act_both(p.act, v[8 * j + 2 * i + 1], f1, d1);
+                  a1[i] = pad ? 0u : pack_bf16(d0, d1);
+                  a2[i] = pad ? 0u : pack_bf16(f0, f1);
                 }
               } else {
+                // g_y1 = g_y2 * F'(y1), F'(y1) read from the stash
                 const uint4 yy = yv[c0 / 8 + j];
                 const __nv_bfloat16* yb = reinterpret_cast<const __nv_bfloat16*>(&yy);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                  const float g0 = v[8 * j + 2 * i] * act_bwd(p.act, __bfloat162float(yb[2 * i]));
-                  const float g1 = v[8 * j + 2 * i + 1] * act_bwd(p.act, __bfloat162float(yb[2 * i + 1]));
+                  const float g0 = v[8 * j + 2 * i] * __bfloat162float(yb[2 * i]);
+                  const float g1 = v[8 * j + 2 * i + 1] * __bfloat162float(yb[2 * i + 1]);
                   a1[i] = pad ? 0u : pack_bf16(g0, g1);
                 }
               }

@@ -78,7 +78,9 @@ class ForwardStash:
     blk: int
 
     def export(self, choice: int):
-        """(y1_i, y2_i) in token order, fp32 N x H (for parity checks)."""
+        """(F'(y1_i), y2_i) in token order, fp32 N x H (for parity checks).
+        The device stash keeps F'(y1) instead of y1: it is all the backward
+        needs of y1 (moe_layer.cpp:108) and saves recomputing F'."""
         d = self.desc
         y1 = torch.empty(d.n_tokens, d.hidden, dtype=torch.float32, device=self.x.device)
         y2 = torch.empty_like(y1)

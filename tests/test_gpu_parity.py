@@ -52,6 +52,18 @@ def kat():
         return json.load(f)
 
 
+def dact_ref(act, y1):
+    """F'(y1) of the reference activations (tensor.cpp:48-53, 72), fp64."""
+    y1 = np.asarray(y1, dtype=np.float64)
+    if act == "gelu":
+        c = 0.7978845608028654
+        t = np.tanh(c * (y1 + 0.044715 * y1 ** 3))
+        return 0.5 * (1 + t) + 0.5 * y1 * (1 - t * t) * c * (1 + 3 * 0.044715 * y1 * y1)
+    if act == "relu":
+        return (y1 > 0).astype(np.float64)
+    return np.ones_like(y1)
+
+
 # ----------------------------------------------------------------- routing --
 def test_reindex_kats_bitexact():
     H = hx()
@@ -226,8 +238,8 @@ def _check_layer(p, x, r, gy, rtol, act):
                         host(gy), 8, act)
     errs = {"y": O.scaled_err(host(fw.y), y_ref)}
     for i in range(r.k):
-        y1, y2 = fw.stash.export(i)
-        errs[f"y1_{i}"] = O.scaled_err(host(y1), y1_ref[i])
+        dact, y2 = fw.stash.export(i)
+        errs[f"dact_{i}"] = O.scaled_err(host(dact), dact_ref(act, y1_ref[i]))
         errs[f"y2_{i}"] = O.scaled_err(host(y2), y2_ref[i])
     for key in ("gw1", "gb1", "gw2", "gb2", "gx"):
         errs[key] = O.scaled_err(host(getattr(g, key)), go[key])
