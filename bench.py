@@ -232,41 +232,76 @@ def run_ours(args, cfg, rank, ws, local):
         H.synthesize_routing(N, E, k, cfg["dist"], seed)
     a = r.to_device(dev)
     gy = torch.ones(N, D, dtype=dtype, device=dev)
-    run = LayerRunner(p, N, k, dev, dtype)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
+    L = _lib.lib()
+    use_graph = ws == 1 and not args.no_graph
 
-    # warm-up (also validates routing once)
-    status = torch.zeros(1, dtype=torch.int32, device=dev)
-    run.forward(x, a, status=status)
-    run.backward(x, gy)
-    torch.cuda.synchronize()
-    assert int(status.item()) == 0
+    if ws == 1:
+        run = LayerRunner(p, N, k, dev, dtype)
+        # warm-up (also validates routing once)
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+        run.forward(x, a, status=status)
+        run.backward(x, gy)
+        torch.cuda.synchronize()
+        assert int(status.item()) == 0
+        y_out = run.y
+    else:
+        # data-centric TP along H (dist_sim.cpp:352-452): rank r owns an even
+        # H-slice; every step all-gathers it into the pipeline-shared cache,
+        # runs the full layer on this rank's 16384 tokens and reduce-scatters
+        # the gradients to the shard owners
+        from paper_2411_01288_b200 import dist as HD
+        sp = HD.shard_params(p, HD.even_split(Hd, ws))
+        dc = HD.DataCentricRunner(sp.shards[rank], sp.b2 if rank == 0 else None,
+                                  sp.hidden_sizes, "gelu", N, k, None, dtype)
+        del p, sp
+        run = dc.runner
+        y_out = run.y
+    step_fn = (lambda: run.step(x, a, gy)) if ws == 1 else (lambda: dc.step(x, a, gy))
     for _ in range(max(0, args.warmup - 1)):
-        run.step(x, a, gy)
+        step_fn()
+    graph_kernels = 0
+    L.hxm_profile_reset()
+    if use_graph:
+        L.hxm_profile_enable(1)  # the region events are recorded into the graph
+        c0 = L.hxm_launch_count()
+        run.capture(x, a, gy)
+        graph_kernels = (L.hxm_launch_count() - c0) // 2  # capture() warms once
+        L.hxm_profile_enable(0)
+        L.hxm_profile_reset()
+        L.hxm_profile_enable(1)
+        run.capture(x, a, gy, warm=False)  # re-record: the profile holds one step
+        L.hxm_profile_enable(0)
+        step_fn = run.replay
+        for _ in range(2):
+            step_fn()
     barrier(ws)
 
     # ---- device-resident timed region ------------------------------------
-    L = _lib.lib()
-    L.hxm_profile_reset()
+    if not use_graph:
+        L.hxm_profile_reset()
     launches0 = L.hxm_launch_count()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     clocks = ClockSampler(local, period=0.005)
     barrier(ws)
     with clocks:
-        L.hxm_profile_enable(1)
+        if not use_graph:
+            L.hxm_profile_enable(1)
         for i in range(args.steps):
             flush.zero_()  # L2 flush outside the step's events
             evs[i][0].record(stream)
-            run.step(x, a, gy)
+            step_fn()
             evs[i][1].record(stream)
         L.hxm_profile_enable(0)
         barrier(ws)
     launches = L.hxm_launch_count() - launches0
+    if use_graph:
+        launches = graph_kernels * args.steps  # each replay runs the captured kernels
     step_ms = [s.elapsed_time(e) for s, e in evs]
     total_ms = max_over_ranks(sum(step_ms), ws)
-    prof = _lib.profile_read()
+    prof = _lib.profile_read()  # graph: the last replay's kernel regions
     L.hxm_profile_reset()
     value = N * ws * args.steps / (total_ms / 1000.0)
 
@@ -275,22 +310,23 @@ def run_ours(args, cfg, rank, ws, local):
     gyh = gy.cpu().pin_memory()
     ah = a.cpu().pin_memory()
     yh = torch.empty(N, D, dtype=torch.float32).pin_memory()
-    xd, gyd, ad = torch.empty_like(x), torch.empty_like(gy), torch.empty_like(a)
     e2e_steps = max(3, min(args.steps, 20))
+
+    def e2e_step():
+        # the graph's static inputs are x / a / gy: refill them from the host
+        x.copy_(xh, non_blocking=True)
+        a.copy_(ah, non_blocking=True)
+        gy.copy_(gyh, non_blocking=True)
+        step_fn()
+        yh.copy_(y_out, non_blocking=True)
+
     for _ in range(2):
-        xd.copy_(xh, non_blocking=True); ad.copy_(ah, non_blocking=True)
-        gyd.copy_(gyh, non_blocking=True)
-        run.step(xd, ad, gyd)
-        yh.copy_(run.y, non_blocking=True)
+        e2e_step()
     barrier(ws)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(e2e_steps):
-        xd.copy_(xh, non_blocking=True)
-        ad.copy_(ah, non_blocking=True)
-        gyd.copy_(gyh, non_blocking=True)
-        run.step(xd, ad, gyd)
-        yh.copy_(run.y, non_blocking=True)
+        e2e_step()
     e1.record(stream)
     barrier(ws)
     e2e_ms = max_over_ranks(e0.elapsed_time(e1), ws)
@@ -342,7 +378,8 @@ def run_ours(args, cfg, rank, ws, local):
         "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
         "config": {"workload": args.config, "desc": cfg["desc"], "E": E, "k": k, "d": D,
                    "ffn": Hd, "tokens_per_gpu": N, "routing": cfg["dist"],
-                   "parallelism": f"replicas{ws}" if ws > 1 else "single",
+                   "parallelism": f"data_centric_tp{ws}" if ws > 1 else "single",
+                   "cuda_graph": use_graph,
                    "l2": "flushed between steps (256 MiB write, outside the timed events)"},
         "layer_tflops": flop_step * args.steps * ws / (total_ms / 1e3) / 1e12,
         "layer_frac_of_bf16_sustained": flop_step * args.steps / (total_ms / 1e3) / 1e12
@@ -365,6 +402,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="launch the step eagerly instead of replaying its CUDA graph")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -323,6 +323,83 @@ def model_centric_step(local_x, local_assign, local_gy, shard: ParamShard, b2, a
     return DistStepResult(y, MoeGrads(g.gw1, g.gb1, g.gw2, g.gb2 if r == 0 else None, gx), log)
 
 
+class DataCentricRunner:
+    """Preallocated data-centric TP step for one process per GPU (the fast
+    path behind bench.py --gpus N; the choreography is data_centric_step's).
+
+    Each rank owns an even H-slice of the layer.  step(): (1) all-gather the
+    shards straight into the pipeline-shared cache buffers that the CUDA layer
+    reads (NCCL, side stream, joined by an event), (2) fwd+bwd of the full layer
+    on this rank's tokens (LayerRunner -> hxm_moe_forward/backward),
+    (3) reduce-scatter the fp32 parameter gradients to the shard owners (b2's
+    gradient is all-reduced, its owner is rank 0)."""
+
+    def __init__(self, shard: ParamShard, b2, hidden_sizes: Sequence[int], activation: str,
+                 n_tokens: int, k: int, group=None, dtype=torch.bfloat16):
+        from .moe_layer import MoeLayerParams
+        from .runner import LayerRunner
+        self.group = group
+        self.P, self.rank = _ws(group), _rank(group)
+        if len(set(hidden_sizes)) != 1:
+            raise ValueError("DataCentricRunner: even hidden shares only (use data_centric_step)")
+        self.h = hidden_sizes[0]
+        self.shard = shard
+        E, Di, h = shard.w1.shape
+        Do = shard.w2.shape[2]
+        dev = shard.w1.device
+        P = self.P
+        # gather buffers (rank-major) and the cache (full layer, reference layout)
+        self.w1g = torch.empty((P * E, Di, h), dtype=shard.w1.dtype, device=dev)
+        self.w2g = torch.empty((P * E, h, Do), dtype=shard.w2.dtype, device=dev)
+        self.b1g = torch.empty((P * E, h), dtype=shard.b1.dtype, device=dev)
+        self.b2 = (b2 if b2 is not None else torch.zeros((E, Do), device=dev)).float().contiguous()
+        full = MoeLayerParams(torch.empty((E, Di, P * h), dtype=shard.w1.dtype, device=dev),
+                              torch.empty((E, P * h), dtype=torch.float32, device=dev),
+                              torch.empty((E, P * h, Do), dtype=shard.w2.dtype, device=dev),
+                              self.b2, activation)
+        self.cache = PipelineSharedCache(full.param_elements())
+        self.cache.fill(0, full)
+        self.runner = LayerRunner(full, n_tokens, k, dev, dtype)
+        self.side = torch.cuda.Stream(device=dev)
+        self.gw1 = torch.empty((E, Di, h), dtype=torch.float32, device=dev)
+        self.gb1 = torch.empty((E, h), dtype=torch.float32, device=dev)
+        self.gw2 = torch.empty((E, h, Do), dtype=torch.float32, device=dev)
+
+    def gather(self) -> None:
+        """Cache fill (dist_sim.cpp:367-368) on the side stream."""
+        P, E = self.P, self.shard.w1.shape[0]
+        self.side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self.side):
+            dist.all_gather_into_tensor(self.w1g, self.shard.w1.contiguous(), group=self.group)
+            dist.all_gather_into_tensor(self.w2g, self.shard.w2.contiguous(), group=self.group)
+            dist.all_gather_into_tensor(self.b1g, self.shard.b1.contiguous(), group=self.group)
+            dist.broadcast(self.b2, src=dist.get_global_rank(self.group, 0)
+                           if self.group is not None else 0, group=self.group)
+            p = self.cache.params()
+            Di, h, Do = self.w1g.shape[1], self.h, self.w2g.shape[2]
+            p.w1.view(E, Di, P, h).copy_(self.w1g.view(P, E, Di, h).permute(1, 2, 0, 3))
+            p.w2.view(E, P, h, Do).copy_(self.w2g.view(P, E, h, Do).permute(1, 0, 2, 3))
+            self.runner.b1.view(E, P, h).copy_(self.b1g.view(P, E, h).permute(1, 0, 2))
+        torch.cuda.current_stream().wait_stream(self.side)
+
+    def step(self, x, assignments, g_y):
+        self.gather()
+        self.runner.step(x, assignments, g_y)
+        g = self.runner.grads
+        E = g.gw1.shape[0]
+        P, h = self.P, self.h
+        # reduce-scatter along H: rank-major views of the H axis
+        w1 = g.gw1.view(E, g.gw1.shape[1], P, h).permute(2, 0, 1, 3).contiguous()
+        dist.reduce_scatter_tensor(self.gw1, w1, group=self.group)
+        b1 = g.gb1.view(E, P, h).permute(1, 0, 2).contiguous()
+        dist.reduce_scatter_tensor(self.gb1, b1, group=self.group)
+        w2 = g.gw2.view(E, P, h, g.gw2.shape[2]).permute(1, 0, 2, 3).contiguous()
+        dist.reduce_scatter_tensor(self.gw2, w2, group=self.group)
+        if g.gb2 is not None:
+            dist.all_reduce(g.gb2, group=self.group)
+        return self.runner.y
+
+
 def _reduce_rows(t: torch.Tensor, counts: Sequence[int], group, how: str) -> torch.Tensor:
     if how == "all_reduce":
         dist.all_reduce(t, group=group)

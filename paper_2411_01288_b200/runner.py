@@ -59,3 +59,22 @@ class LayerRunner:
     def step(self, x, assignments, g_y, stream=None):
         self.forward(x, assignments, stream)
         return self.backward(x, g_y, stream)
+
+    # ---- CUDA graph: the whole fwd+bwd step as one launch -----------------
+    def capture(self, x, assignments, g_y, warm: bool = True) -> None:
+        """Record step(x, assignments, g_y) into a CUDA graph.  x / assignments /
+        g_y become the graph's static input buffers: refill them in place
+        (copy_) before replay()."""
+        if warm:
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                self.step(x, assignments, g_y)  # kernel attributes, tensor maps
+            torch.cuda.current_stream().wait_stream(s)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.step(x, assignments, g_y)
+
+    def replay(self) -> MoeGrads:
+        self.graph.replay()
+        return self.grads
