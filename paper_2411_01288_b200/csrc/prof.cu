@@ -42,6 +42,17 @@ cudaEvent_t get_event() {
 
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+// Inside a CUDA-graph capture a plain record only adds a dependency; an
+// External record becomes an event-record node that timestamps every replay.
+static void record(cudaEvent_t e, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+  else
+    cudaEventRecord(e, st);
+}
+
 ProfScope::ProfScope(cudaStream_t st, const char* name, double work, int kind)
     : st_(st), name_(name), work_(work), kind_(kind) {
   std::lock_guard<std::mutex> l(g_mu);
@@ -49,13 +60,13 @@ ProfScope::ProfScope(cudaStream_t st, const char* name, double work, int kind)
   active_ = true;
   a_ = get_event();
   b_ = get_event();
-  cudaEventRecord(static_cast<cudaEvent_t>(a_), st_);
+  record(static_cast<cudaEvent_t>(a_), st_);
 }
 
 ProfScope::~ProfScope() {
   if (!active_) return;
   std::lock_guard<std::mutex> l(g_mu);
-  cudaEventRecord(static_cast<cudaEvent_t>(b_), st_);
+  record(static_cast<cudaEvent_t>(b_), st_);
   g_recs.push_back(Rec{name_, static_cast<cudaEvent_t>(a_), static_cast<cudaEvent_t>(b_),
                        work_, kind_});
 }
@@ -92,8 +103,11 @@ int hxm_profile_read(int max, char* names, int name_len, double* total_ms, int64
   std::vector<std::string> order;
   for (auto& r : g_recs) {
     float ms = 0.f;
-    if (cudaEventSynchronize(r.b) != cudaSuccess) return -1;
-    cudaEventElapsedTime(&ms, r.a, r.b);
+    if (cudaEventSynchronize(r.b) != cudaSuccess ||
+        cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) {
+      cudaGetLastError();  // an unrecorded region: skip it, keep the rest
+      continue;
+    }
     if (!agg.count(r.name)) order.push_back(r.name);
     Agg& a = agg[r.name];
     a.ms += ms;
