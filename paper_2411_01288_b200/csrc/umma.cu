@@ -393,42 +393,42 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
     constexpr uint32_t kIdescEsmmMN = idesc_bf16(BN, 0, 1);
     constexpr uint32_t kIdescEsmmK = idesc_bf16(BN, 0, 0);
     constexpr uint32_t kIdescEst = idesc_bf16(BN, 1, 1);
-    const uint32_t idesc = ESTMM ? kIdescEst : (p.b_kmajor ? kIdescEsmmK : kIdescEsmmMN);
-    int s = 0, acc = 0;
-    uint32_t ph = 0, aph = 0;
-    for (int w = blockIdx.x; w < total; w += gridDim.x) {
-      const SegTile t = p.tiles[w / per_item];
-      const int nk = ESTMM ? (t.end - t.begin + BK - 1) / BK : p.K / BK;
-      mbar_wait(&tempty[acc], aph ^ 1);
-      tc_fence_after();
-      const uint32_t d = tmem + acc * BN;
-      for (int kb = 0; kb < nk; ++kb) {
-        mbar_wait(&full[s], ph);
+    // One thread issues everything; descriptors are built once and advanced
+    // by adding to the start-address field, so a k-block costs ~a dozen
+    // instructions (the tensor pipe needs a new UMMA every 64-128 cycles).
+    if (lane == 0) {
+      const uint32_t idesc = ESTMM ? kIdescEst : (p.b_kmajor ? kIdescEsmmK : kIdescEsmmMN);
+      // per UMMA_K (16) step, in 16-byte descriptor units: K-major = 32 B
+      // inside the swizzle atom; MN-major = 16 k-rows = 2 x 1024 B
+      const bool a_mn = ESTMM, b_mn = ESTMM || !p.b_kmajor;
+      const uint32_t a_step = a_mn ? 128u : 2u, b_step = b_mn ? 128u : 2u;
+      const uint32_t base = smem_u32(smem);
+      const uint64_t da0 = a_mn ? sdesc(base, 8192, 1024) : sdesc(base, 16, 1024);
+      const uint64_t db0 = b_mn ? sdesc(base + kABytes, 8192, 1024) : sdesc(base + kABytes, 16, 1024);
+      constexpr uint32_t kStageUnits = C::kStage >> 4;
+      int s = 0, acc = 0;
+      uint32_t ph = 0, aph = 0;
+      for (int w = blockIdx.x; w < total; w += gridDim.x) {
+        const SegTile t = p.tiles[w / per_item];
+        const int nk = ESTMM ? (t.end - t.begin + BK - 1) / BK : p.K / BK;
+        mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t sa = smem_u32(smem + s * C::kStage);
-          const uint32_t sb = sa + kABytes;
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint64_t da = da0 + s * kStageUnits, db = db0 + s * kStageUnits;
 #pragma unroll
-          for (int kk = 0; kk < BK / UK; ++kk) {
-            uint64_t da, db;
-            if (ESTMM) {  // both MN-major: 16 k-rows = 2 x 1024 B per UMMA_K
-              da = sdesc(sa + kk * 2048, 8192, 1024);
-              db = sdesc(sb + kk * 2048, 8192, 1024);
-            } else {      // A K-major: 32 B per UMMA_K inside the swizzle atom
-              da = sdesc(sa + kk * 32, 16, 1024);
-              db = p.b_kmajor ? sdesc(sb + kk * 32, 16, 1024) : sdesc(sb + kk * 2048, 8192, 1024);
-            }
-            umma_bf16(d, da, db, idesc, (kb | kk) != 0);
-          }
+          for (int kk = 0; kk < BK / UK; ++kk)
+            umma_bf16(d, da + kk * a_step, db + kk * b_step, idesc, (kb | kk) != 0);
           umma_commit(&empty[s]);
+          if (++s == C::kStages) { s = 0; ph ^= 1; }
         }
-        __syncwarp();
-        if (++s == C::kStages) { s = 0; ph ^= 1; }
+        umma_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; aph ^= 1; }
       }
-      if (lane == 0) umma_commit(&tfull[acc]);
-      __syncwarp();
-      if (++acc == 2) { acc = 0; aph ^= 1; }
     }
+    __syncwarp();
   } else {
     // ================================ epilogue ============================
     // 8 warps: warp w reads TMEM lane group (w % 4) -- the hardware rule --
