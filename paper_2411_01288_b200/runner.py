@@ -78,3 +78,64 @@ class LayerRunner:
     def replay(self) -> MoeGrads:
         self.graph.replay()
         return self.grads
+
+
+class HostPipeline:
+    """Layer steps fed from (pinned) HOST memory with the PCIe traffic
+    overlapped: step i's H2D copies, step i-1's compute and step i-2's D2H of
+    y run concurrently on three streams, double-buffered (two LayerRunners
+    sharing the parameters, each replaying its own CUDA graph).
+
+    push(x_h, a_h, gy_h, y_h): enqueue one step; y_h (pinned) receives y.
+    drain(): wait for everything enqueued."""
+
+    def __init__(self, p: MoeLayerParams, n_tokens: int, k: int, d_in: int, d_out: int,
+                 device="cuda", dtype=torch.bfloat16):
+        self.runners = [LayerRunner(p, n_tokens, k, device, dtype) for _ in range(2)]
+        f = dict(device=device)
+        self.x = [torch.empty(n_tokens, d_in, dtype=dtype, **f) for _ in range(2)]
+        self.a = [torch.zeros(k, n_tokens, dtype=torch.int32, **f) for _ in range(2)]
+        self.gy = [torch.empty(n_tokens, d_out, dtype=dtype, **f) for _ in range(2)]
+        self.s_in, self.s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        self.s_comp = torch.cuda.current_stream()
+        self.ev_in = [torch.cuda.Event() for _ in range(2)]
+        self.ev_comp = [torch.cuda.Event() for _ in range(2)]
+        self.ev_out = [torch.cuda.Event() for _ in range(2)]
+        self.i = 0
+        self.captured = False
+
+    def _capture(self, a_init):
+        for b in range(2):
+            self.a[b].copy_(a_init)
+            self.x[b].zero_()
+            self.gy[b].zero_()
+            self.runners[b].capture(self.x[b], self.a[b], self.gy[b])
+        torch.cuda.synchronize()
+        for b in range(2):  # events start "recorded"
+            self.ev_comp[b].record(self.s_comp)
+            self.ev_out[b].record(self.s_comp)
+        self.captured = True
+
+    def push(self, x_h, a_h, gy_h, y_h):
+        if not self.captured:
+            self._capture(a_h.to(self.a[0].device))
+        b = self.i % 2
+        self.i += 1
+        with torch.cuda.stream(self.s_in):
+            self.s_in.wait_event(self.ev_comp[b])  # step i-2 done reading buffer b
+            self.x[b].copy_(x_h, non_blocking=True)
+            self.a[b].copy_(a_h, non_blocking=True)
+            self.gy[b].copy_(gy_h, non_blocking=True)
+            self.ev_in[b].record(self.s_in)
+        self.s_comp.wait_event(self.ev_in[b])
+        self.s_comp.wait_event(self.ev_out[b])  # y_b of step i-2 copied out
+        self.runners[b].replay()
+        self.ev_comp[b].record(self.s_comp)
+        with torch.cuda.stream(self.s_out):
+            self.s_out.wait_event(self.ev_comp[b])
+            y_h.copy_(self.runners[b].y, non_blocking=True)
+            self.ev_out[b].record(self.s_out)
+
+    def drain(self):
+        self.s_comp.wait_stream(self.s_in)
+        self.s_comp.wait_stream(self.s_out)
