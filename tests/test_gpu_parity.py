@@ -296,6 +296,26 @@ def test_layer_bf16_vs_oracle(E, k, din, hid, dout, n, act, dist):
     _check_layer(p, x, r, gy, RTOL_BF16, act)
 
 
+def test_layer_skewed_split_k():
+    """c5-style skew: most slots on two experts, so their ESTMM is split over
+    several 2048-position chunks (fp32 reductions into zeroed slices), others
+    have a few tokens or none."""
+    H = hx()
+    E, k, D, Hd, N = 16, 2, 128, 256, 3000
+    p, x = H.make_random_params(E, D, Hd, D, "gelu", seed=5, n_tokens=N)
+    r = H.synthesize_routing(N, E, k, "uniform", 6)
+    a = r.assignments.copy()
+    hot = np.random.default_rng(7).random(N) < 0.9
+    a[0, hot], a[1, hot] = 0, 1
+    a[:, :] = np.where(a == 15, 14, a)  # expert 15 empty
+    bad = a[0] == a[1]
+    a[1, bad] = (a[0, bad] + 1) % 15
+    r = H.RoutingChoice(N, E, k, a)
+    gy = torch.as_tensor(np.random.default_rng(8).standard_normal((N, D))).to("cuda", torch.bfloat16)
+    errs = _check_layer(p, x, r, gy, RTOL_BF16, "gelu")
+    assert errs["gw1"] <= RTOL_BF16
+
+
 def test_layer_c2_full_size_properties():
     """c2 at full N: exact integer properties that do not need the CPU oracle.
     With g_y = ones, gb2[e] = number of (token, choice) slots routed to e
