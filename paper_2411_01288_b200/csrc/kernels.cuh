@@ -106,6 +106,7 @@ hxm_status launch_gather_rows(hxm_dtype dt, const void* src, RowMap map, int64_t
 constexpr int kEssRows = 128;
 constexpr int kSimtRows = 64;     // SIMT ESMM tile rows
 constexpr int kUmmaRows = 128;    // tcgen05 ESMM tile rows (UMMA M)
+constexpr int kUmma2Rows = 256;   // CTA-pair (cta_group::2) ESMM tile rows
 constexpr int kEstmmChunk = 2048; // ESTMM split-K chunk (positions)
 
 hxm_status launch_esmm(hxm_dtype dt, const EsmmArgs& a, cudaStream_t st);
@@ -121,6 +122,8 @@ hxm_status umma_esmm(const EsmmArgs& a, cudaStream_t st);
 hxm_status umma_estmm(const EstmmArgs& a, cudaStream_t st);
 bool umma_supports_esmm(int64_t d1, int64_t d2);
 bool umma_supports_estmm(int64_t d1, int64_t d2);
+// CTA-pair ESMM (dense A, 256-row tiles): BN must split into whole B halves
+bool umma2_supports_esmm(int64_t d1, int64_t d2, bool w_trans);
 
 // zero out[e] for experts whose ESTMM is split over several chunks
 hxm_status zero_split_experts(const SegTile* tiles, const int32_t* n_tiles,

@@ -68,7 +68,15 @@ LayerWs carve(Arena& ar, const hxm_layer_desc& d) {
                     umma_supports_esmm(d.hidden, d.d_out) &&
                     umma_supports_esmm(d.d_out, d.hidden) &&
                     umma_supports_esmm(d.hidden, d.d_in);
-  w.rows_a = umma ? kUmmaRows : kSimtRows;
+  // 256-row tiles on CTA pairs (cta_group::2) when every layer GEMM's B
+  // splits into whole halves; HXM_CTA_PAIR=0 forces single-CTA tiles
+  const char* env = std::getenv("HXM_CTA_PAIR");
+  const bool pair_ok = !(env && env[0] == '0');
+  const bool umma2 = umma && pair_ok && umma2_supports_esmm(d.d_in, d.hidden, false) &&
+                     umma2_supports_esmm(d.hidden, d.d_out, false) &&
+                     umma2_supports_esmm(d.d_out, d.hidden, true) &&
+                     umma2_supports_esmm(d.hidden, d.d_in, true);
+  w.rows_a = umma2 ? kUmma2Rows : (umma ? kUmmaRows : kSimtRows);
   w.v = ar.take<int32_t>(w.bound);
   w.idx = ar.take<int32_t>(d.n_experts + 1);
   w.rws_bytes = reindex_ws_bytes(slots, d.n_experts);

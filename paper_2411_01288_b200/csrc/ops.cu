@@ -16,7 +16,7 @@ int esmm_tile_rows(hxm_dtype dt, int64_t d1, int64_t d2) {
 
 hxm_status launch_esmm(hxm_dtype dt, const EsmmArgs& a, cudaStream_t st) {
   ProfScope ps(st, a.label ? a.label : "esmm", a.work, WORK_FLOP);
-  if (a.tile_rows == kUmmaRows) {
+  if (a.tile_rows == kUmmaRows || a.tile_rows == kUmma2Rows) {
     if (dt != HXM_BF16 || !umma_supports_esmm(a.d1, a.d2))
       return invalid_arg("esmm: 128-row tiles need the tcgen05 kernel");
     return umma_esmm(a, st);

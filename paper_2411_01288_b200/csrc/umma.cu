@@ -154,6 +154,78 @@ __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// ---- CTA-pair (cluster of 2) helpers ----------------------------------------
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// shared::cluster address of the same smem offset in CTA rank 0
+__device__ __forceinline__ uint32_t mapa0(uint32_t local) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(local));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_tx_cl(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(bar),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cl(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar)
+               : "memory");
+}
+// wait with cluster-scope acquire (barriers that receive the peer's arrivals)
+__device__ __forceinline__ void mbar_wait_cl(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done;
+  const long long t0 = clock64();
+  while (true) {
+    asm volatile(
+        "{\n.reg .pred P;\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P;\n}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (clock64() - t0 > (1ll << 34)) __trap();
+  }
+}
+// TMA loads whose completion is signalled on the leader CTA's barrier
+__device__ __forceinline__ void tma_2d_cg2(void* dst, const CUtensorMap* map, uint32_t bar, int c0,
+                                           int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d_cg2(void* dst, const CUtensorMap* map, uint32_t bar, int c0,
+                                           int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_cg2(uint32_t tmem_d, uint64_t da, uint64_t db,
+                                              uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accum));
+}
+// arrive on the barrier at this smem offset in BOTH CTAs of the pair
+__device__ __forceinline__ void umma_commit_cg2(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+
 // same load without the completion wait (pair with tmem_wait)
 __device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
@@ -185,10 +257,10 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
          (static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
 }
 // Instruction descriptor kind::f16: D=f32, A=B=bf16, majors, N>>3, M>>4.
-__host__ __device__ constexpr uint32_t idesc_bf16(int n, int a_mn, int b_mn) {
+__host__ __device__ constexpr uint32_t idesc_bf16(int n, int a_mn, int b_mn, int m = BM) {
   return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(a_mn) << 15) |
          (static_cast<uint32_t>(b_mn) << 16) | (static_cast<uint32_t>(n >> 3) << 17) |
-         (static_cast<uint32_t>(BM >> 4) << 24);
+         (static_cast<uint32_t>(m >> 4) << 24);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -239,9 +311,11 @@ struct UParams {
   float* est_out;
 };
 
-template <int BN>
+// CG = CTAs per UMMA (cta_group): with CG = 2 a CTA pair runs M = 256 tiles,
+// each CTA holding 128 rows of A / D and half (BN/2) of the B columns.
+template <int BN, int CG = 1>
 struct Cfg {
-  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kBBytes = (BN / CG) * BK * 2;
   static constexpr int kStage = kABytes + kBBytes;
   // 227 KB opt-in smem = stages + per-epilogue-warp staging (4 KB each) +
   // 1 KB alignment slack + barriers
@@ -255,10 +329,18 @@ struct Cfg {
 // bias + activation into the bf16 stash (y1, y2); 2 = ESMM times F'(y1) into
 // the bf16 g_y1 stash; 3 = ESTMM.  One instantiation per mode keeps each
 // epilogue's register footprint to what it uses.
-template <int BN, int MODE>
+//
+// CG = 2 (dense operands only): clusters of 2 CTAs; the leader (rank 0)
+// issues tcgen05.mma.cta_group::2 with M = 256; both CTAs' TMA loads signal
+// the leader's full barrier; commits multicast to both CTAs' empty / tfull
+// barriers; both CTAs' epilogues arrive on the leader's tempty barrier.
+template <int BN, int MODE, int CG = 1>
 __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant__ UParams p) {
   constexpr bool ESTMM = MODE == 3;
-  using C = Cfg<BN>;
+  using C = Cfg<BN, CG>;
+  uint32_t rank = 0;
+  if constexpr (CG == 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int cluster = blockIdx.x / CG, n_clusters = gridDim.x / CG;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -272,25 +354,35 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], CG);  // CG = 2: both CTAs' producers arrive on the leader's
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], kEpiWarps);
+      mbar_init(&tempty[a], kEpiWarps * CG);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // the leader CTA's copies of the shared barriers (CG = 2)
+  const uint32_t full_lead = CG == 2 ? mapa0(smem_u32(full)) : smem_u32(full);
+  const uint32_t tempty_lead = CG == 2 ? mapa0(smem_u32(tempty)) : smem_u32(tempty);
 
   const int n_items = *p.n_tiles;
   const int per_item = ESTMM ? p.n_mt * p.n_nt : p.n_nt;
@@ -304,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
     }
     int s = 0;
     uint32_t ph = 0;
-    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+    for (int w = cluster; w < total; w += n_clusters) {
       const SegTile t = p.tiles[w / per_item];
       const int rem = w % per_item;
       if (!ESTMM) {
@@ -320,21 +412,39 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* sa = smem + s * C::kStage;
           uint8_t* sb = sa + kABytes;
-          if (lane == 0) mbar_arrive_tx(&full[s], C::kStage);
-          __syncwarp();
-          if (p.a_gather) {
-            tma_gather4(sa + lane * 512, &p.tmA, &full[s], kb * BK, rows[0], rows[1], rows[2],
-                        rows[3]);
-          } else if (lane == 0) {
-            tma_2d(sa, &p.tmA, &full[s], kb * BK, t.begin);
-          }
-          if (lane == 0) {
-            if (p.b_kmajor) {
-              tma_3d(sb, &p.tmB, &full[s], kb * BK, n0, t.expert);
-            } else {
+          if constexpr (CG == 2) {
+            // dense only: this CTA's 128 rows of A and BN/2 columns of B,
+            // completion counted on the leader's full barrier
+            if (lane == 0) {
+              const uint32_t fb = full_lead + 8u * s;
+              mbar_arrive_tx_cl(fb, C::kStage);
+              tma_2d_cg2(sa, &p.tmA, fb, kb * BK, t.begin + static_cast<int>(rank) * BM);
+              const int nb = n0 + static_cast<int>(rank) * (BN / 2);
+              if (p.b_kmajor) {
+                tma_3d_cg2(sb, &p.tmB, fb, kb * BK, nb, t.expert);
+              } else {
 #pragma unroll
-              for (int j = 0; j < BN / 64; ++j)
-                tma_3d(sb + j * 8192, &p.tmB, &full[s], n0 + 64 * j, kb * BK, t.expert);
+                for (int j = 0; j < BN / 128; ++j)
+                  tma_3d_cg2(sb + j * 8192, &p.tmB, fb, nb + 64 * j, kb * BK, t.expert);
+              }
+            }
+          } else {
+            if (lane == 0) mbar_arrive_tx(&full[s], C::kStage);
+            __syncwarp();
+            if (p.a_gather) {
+              tma_gather4(sa + lane * 512, &p.tmA, &full[s], kb * BK, rows[0], rows[1], rows[2],
+                          rows[3]);
+            } else if (lane == 0) {
+              tma_2d(sa, &p.tmA, &full[s], kb * BK, t.begin);
+            }
+            if (lane == 0) {
+              if (p.b_kmajor) {
+                tma_3d(sb, &p.tmB, &full[s], kb * BK, n0, t.expert);
+              } else {
+#pragma unroll
+                for (int j = 0; j < BN / 64; ++j)
+                  tma_3d(sb + j * 8192, &p.tmB, &full[s], n0 + 64 * j, kb * BK, t.expert);
+              }
             }
           }
           __syncwarp();
@@ -342,13 +452,27 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
         }
       } else {
         const int mt = rem / p.n_nt, nt = rem % p.n_nt;
-        const int m0 = mt * BM, n0 = nt * BN;
+        const int m0 = mt * BM * CG + static_cast<int>(rank) * BM;
+        const int n0 = nt * BN + static_cast<int>(rank) * (BN / CG);
         const int nk = (t.end - t.begin + BK - 1) / BK;
         for (int kb = 0; kb < nk; ++kb) {
           const int p0 = t.begin + kb * BK;
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* sa = smem + s * C::kStage;
           uint8_t* sb = sa + kABytes;
+          if constexpr (CG == 2) {  // dense only (host guarantees)
+            if (lane == 0) {
+              const uint32_t fb = full_lead + 8u * s;
+              mbar_arrive_tx_cl(fb, C::kStage);
+              tma_2d_cg2(sa, &p.tmA, fb, m0, p0);
+              tma_2d_cg2(sa + 8192, &p.tmA, fb, m0 + 64, p0);
+#pragma unroll
+              for (int j = 0; j < BN / 128; ++j) tma_2d_cg2(sb + j * 8192, &p.tmB, fb, n0 + 64 * j, p0);
+            }
+            __syncwarp();
+            if (++s == C::kStages) { s = 0; ph ^= 1; }
+            continue;
+          }
           if (lane == 0) mbar_arrive_tx(&full[s], C::kStage);
           __syncwarp();
           // A = X1^T: two 64-column chunks of the 64 k-rows
@@ -390,13 +514,15 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
     }
   } else if (warp == 1) {
     // ================================ MMA issuer ==========================
-    constexpr uint32_t kIdescEsmmMN = idesc_bf16(BN, 0, 1);
-    constexpr uint32_t kIdescEsmmK = idesc_bf16(BN, 0, 0);
-    constexpr uint32_t kIdescEst = idesc_bf16(BN, 1, 1);
+    constexpr uint32_t kIdescEsmmMN = idesc_bf16(BN, 0, 1, BM * CG);
+    constexpr uint32_t kIdescEsmmK = idesc_bf16(BN, 0, 0, BM * CG);
+    constexpr uint32_t kIdescEst = idesc_bf16(BN, 1, 1, BM * CG);
     // One thread issues everything; descriptors are built once and advanced
     // by adding to the start-address field, so a k-block costs ~a dozen
     // instructions (the tensor pipe needs a new UMMA every 64-128 cycles).
-    if (lane == 0) {
+    // CG = 2: only the leader CTA issues; its descriptors address the same
+    // smem offsets in both CTAs.
+    if (lane == 0 && rank == 0) {
       const uint32_t idesc = ESTMM ? kIdescEst : (p.b_kmajor ? kIdescEsmmK : kIdescEsmmMN);
       // per UMMA_K (16) step, in 16-byte descriptor units: K-major = 32 B
       // inside the swizzle atom; MN-major = 16 k-rows = 2 x 1024 B
@@ -408,23 +534,31 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
       constexpr uint32_t kStageUnits = C::kStage >> 4;
       int s = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
-      for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      for (int w = cluster; w < total; w += n_clusters) {
         const SegTile t = p.tiles[w / per_item];
         const int nk = ESTMM ? (t.end - t.begin + BK - 1) / BK : p.K / BK;
-        mbar_wait(&tempty[acc], aph ^ 1);
+        if constexpr (CG == 2) mbar_wait_cl(&tempty[acc], aph ^ 1);
+        else mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
         for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(&full[s], ph);
+          if constexpr (CG == 2) mbar_wait_cl(&full[s], ph);
+          else mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint64_t da = da0 + s * kStageUnits, db = db0 + s * kStageUnits;
 #pragma unroll
-          for (int kk = 0; kk < BK / UK; ++kk)
-            umma_bf16(d, da + kk * a_step, db + kk * b_step, idesc, (kb | kk) != 0);
-          umma_commit(&empty[s]);
+          for (int kk = 0; kk < BK / UK; ++kk) {
+            if constexpr (CG == 2)
+              umma_bf16_cg2(d, da + kk * a_step, db + kk * b_step, idesc, (kb | kk) != 0);
+            else
+              umma_bf16(d, da + kk * a_step, db + kk * b_step, idesc, (kb | kk) != 0);
+          }
+          if constexpr (CG == 2) umma_commit_cg2(&empty[s]);
+          else umma_commit(&empty[s]);
           if (++s == C::kStages) { s = 0; ph ^= 1; }
         }
-        umma_commit(&tfull[acc]);
+        if constexpr (CG == 2) umma_commit_cg2(&tfull[acc]);
+        else umma_commit(&tfull[acc]);
         if (++acc == 2) { acc = 0; aph ^= 1; }
       }
     }
@@ -441,14 +575,20 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
     const int lg = warp & 3;
     const int half = (warp - 2) / 4;
     uint8_t* stg = staging + (warp - 2) * 4096;
+    // accumulator drained by this warp: arrive on the (leader's) tempty
+    auto release_acc = [&](int a) {
+      if constexpr (CG == 2) mbar_arrive_cl(tempty_lead + 8u * a);
+      else mbar_arrive(&tempty[a]);
+    };
     int acc = 0;
     uint32_t aph = 0;
-    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+    for (int w = cluster; w < total; w += n_clusters) {
       const SegTile t = p.tiles[w / per_item];
       const int rem = w % per_item;
       if (!ESTMM) {
         const int n0 = rem * BN + half * HB;
-        const int q0 = t.begin + lg * 32;  // first position of this warp's rows
+        // first position of this warp's rows (CG = 2: this CTA's half of 256)
+        const int q0 = t.begin + static_cast<int>(rank) * BM + lg * 32;
         const int q = q0 + lane;
         const bool valid = q < t.end;
         const int orow = valid ? p.omap(q) : -1;
@@ -473,7 +613,8 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
         if (has_bias && lane * 4 < HB)
           bl = __ldg(reinterpret_cast<const float4*>(p.bias + static_cast<int64_t>(t.expert) * N +
                                                      n0) + lane);
-        mbar_wait(&tfull[acc], aph);
+        if constexpr (CG == 2) mbar_wait_cl(&tfull[acc], aph);
+        else mbar_wait(&tfull[acc], aph);
         tc_fence_after();
         const uint32_t taddr =
             tmem + (static_cast<uint32_t>(lg * 32) << 16) + acc * BN + half * HB;
@@ -483,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
         if (HB == 32) {
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (lane == 0) release_acc(acc);
         }
 #pragma unroll
         for (int c0 = 0; c0 < HB; c0 += 32) {
@@ -605,18 +746,20 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
             if (c0 + 64 >= HB) {  // last TMEM load landed: free the accumulator
               tc_fence_before();
               __syncwarp();
-              if (lane == 0) mbar_arrive(&tempty[acc]);
+              if (lane == 0) release_acc(acc);
             }
           }
         }
       } else {
         const int mt = rem / p.n_nt, nt = rem % p.n_nt;
-        const int m0 = mt * BM + lg * 32;  // first output row of this warp
+        // first output row of this warp (CG = 2: this CTA's half of 256)
+        const int m0 = mt * BM * CG + static_cast<int>(rank) * BM + lg * 32;
         const int n0 = nt * BN + half * HB;
         const bool split = t.flags & 1;
         const bool empty_seg = t.end <= t.begin;
         float* obase = p.est_out + static_cast<int64_t>(t.expert) * p.M * p.N;
-        mbar_wait(&tfull[acc], aph);
+        if constexpr (CG == 2) mbar_wait_cl(&tfull[acc], aph);
+        else mbar_wait(&tfull[acc], aph);
         tc_fence_after();
         const uint32_t taddr =
             tmem + (static_cast<uint32_t>(lg * 32) << 16) + acc * BN + half * HB;
@@ -632,7 +775,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
           if (c0 + 32 == HB) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) release_acc(acc);
           }
           __syncwarp();
 #pragma unroll
@@ -656,11 +799,15 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
     if (lane == 0) bulk_wait0();  // this warp's TMA stores are complete
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();  // pair done with TMEM
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(kTmemCols));
+    if constexpr (CG == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(kTmemCols));
   }
 }
 
@@ -709,11 +856,20 @@ int pick_bn(int64_t n) {
     if (n % bn == 0) return bn;
   return 0;
 }
+// CTA-pair tiles: an MN-major B half must be whole 64-column swizzle chunks
+int pick_bn2(int64_t n, bool b_mn) {
+  if (b_mn) {
+    for (int bn : {256, 128})
+      if (n % bn == 0) return bn;
+    return 0;
+  }
+  return pick_bn(n);
+}
 
-template <int BN, int MODE>
+template <int BN, int MODE, int CG>
 hxm_status launch_bn(const UParams& prm, int max_work, cudaStream_t st) {
-  using C = Cfg<BN>;
-  auto kern = umma_kernel<BN, MODE>;
+  using C = Cfg<BN, CG>;
+  auto kern = umma_kernel<BN, MODE, CG>;
   static bool attr_set = false;
   if (!attr_set) {
     HXM_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
@@ -721,19 +877,36 @@ hxm_status launch_bn(const UParams& prm, int max_work, cudaStream_t st) {
   }
   const int sms = sm_count();
   if (sms <= 0) return invalid_arg("tcgen05 path: no CUDA device");
-  const int grid = std::max(1, std::min(sms, max_work));
-  kern<<<grid, kThreads, C::kSmem, st>>>(prm);
+  // persistent: one CTA (CG = 1) or CTA pair (CG = 2) per SM (pair)
+  const int grid = std::max(1, std::min(sms / CG, max_work)) * CG;
+  if constexpr (CG == 1) {
+    kern<<<grid, kThreads, C::kSmem, st>>>(prm);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    HXM_TRY_CUDA(cudaLaunchKernelEx(&cfg, kern, prm));
+  }
   HXM_CHECK_LAUNCH();
   return HXM_OK;
 }
 
-template <int MODE>
+template <int MODE, int CG>
 hxm_status launch_bn_any(int bn, const UParams& prm, int max_work, cudaStream_t st) {
   switch (bn) {
-    case 256: return launch_bn<256, MODE>(prm, max_work, st);
-    case 192: return launch_bn<192, MODE>(prm, max_work, st);
-    case 128: return launch_bn<128, MODE>(prm, max_work, st);
-    default: return launch_bn<64, MODE>(prm, max_work, st);
+    case 256: return launch_bn<256, MODE, CG>(prm, max_work, st);
+    case 192: return launch_bn<192, MODE, CG>(prm, max_work, st);
+    case 128: return launch_bn<128, MODE, CG>(prm, max_work, st);
+    default: return launch_bn<64, MODE, CG>(prm, max_work, st);
   }
 }
 
@@ -745,13 +918,20 @@ bool umma_supports_esmm(int64_t d1, int64_t d2) {
   return d1 > 0 && d2 > 0 && d1 % 64 == 0 && d2 % 64 == 0 && d1 < (1 << 30) && d2 < (1 << 30);
 }
 bool umma_supports_estmm(int64_t d1, int64_t d2) { return umma_supports_esmm(d1, d2); }
+bool umma2_supports_esmm(int64_t d1, int64_t d2, bool w_trans) {
+  return umma_supports_esmm(d1, d2) && pick_bn2(d2, !w_trans) > 0;
+}
 
 hxm_status umma_esmm(const EsmmArgs& a, cudaStream_t st) {
   if (a.max_tiles <= 0) return HXM_OK;
-  if (a.tile_rows != kUmmaRows) return invalid_arg("umma_esmm: tiles must have 128 rows");
-  const int bn = pick_bn(a.d2);
-  UParams prm{};
+  const int CG = a.tile_rows == kUmma2Rows ? 2 : 1;
+  if (a.tile_rows != kUmmaRows && CG == 1)
+    return invalid_arg("umma_esmm: tiles must have 128 (or 256) rows");
   const bool gather = a.amap.kind != MAP_DENSE;
+  if (CG == 2 && (gather || !umma2_supports_esmm(a.d1, a.d2, a.w_trans)))
+    return invalid_arg("umma_esmm: 256-row (CTA-pair) tiles need dense A and BN | N");
+  const int bn = CG == 2 ? pick_bn2(a.d2, !a.w_trans) : pick_bn(a.d2);
+  UParams prm{};
   // A: gathered token rows (n_rows = a_rows) or the dense sorted stash
   {
     const uint64_t dims[2] = {static_cast<uint64_t>(a.d1), static_cast<uint64_t>(a.a_rows)};
@@ -776,7 +956,7 @@ hxm_status umma_esmm(const EsmmArgs& a, cudaStream_t st) {
                                 static_cast<uint64_t>(E)};
       const uint64_t strides[2] = {static_cast<uint64_t>(a.d1) * 2,
                                    static_cast<uint64_t>(a.d1 * a.d2) * 2};
-      const uint32_t box[3] = {64, static_cast<uint32_t>(bn), 1};
+      const uint32_t box[3] = {64, static_cast<uint32_t>(bn / CG), 1};  // this CTA's B rows
       if (!make_map(&prm.tmB, a.w, 3, dims, strides, box))
         return invalid_arg("umma_esmm: cannot encode the W^T tensor map");
     }
@@ -811,16 +991,24 @@ hxm_status umma_esmm(const EsmmArgs& a, cudaStream_t st) {
       return invalid_arg("umma_esmm: cannot encode the output tensor map");
   }
   const int work = a.max_tiles * prm.n_nt;
-  if (a.epi == EPI_FWD_ACT) return launch_bn_any<1>(bn, prm, work, st);
-  if (a.epi == EPI_BWD_ACT) return launch_bn_any<2>(bn, prm, work, st);
-  return launch_bn_any<0>(bn, prm, work, st);
+  if (CG == 2) {
+    if (a.epi == EPI_FWD_ACT) return launch_bn_any<1, 2>(bn, prm, work, st);
+    if (a.epi == EPI_BWD_ACT) return launch_bn_any<2, 2>(bn, prm, work, st);
+    return launch_bn_any<0, 2>(bn, prm, work, st);
+  }
+  if (a.epi == EPI_FWD_ACT) return launch_bn_any<1, 1>(bn, prm, work, st);
+  if (a.epi == EPI_BWD_ACT) return launch_bn_any<2, 1>(bn, prm, work, st);
+  return launch_bn_any<0, 1>(bn, prm, work, st);
 }
 
 hxm_status umma_estmm(const EstmmArgs& a, cudaStream_t st) {
   if (a.max_tiles <= 0) return HXM_OK;
-  const int bn = pick_bn(a.d2);
-  UParams prm{};
   const bool ga = a.m1.kind != MAP_DENSE, gb = a.m2.kind != MAP_DENSE;
+  // CTA pairs (M = 256 output rows per pair) when both operands are dense
+  // and the output rows tile evenly
+  const int CG = (!ga && !gb && a.d1 % 256 == 0 && pick_bn2(a.d2, true) > 0) ? 2 : 1;
+  const int bn = CG == 2 ? pick_bn2(a.d2, true) : pick_bn(a.d2);
+  UParams prm{};
   {
     const uint64_t dims[2] = {static_cast<uint64_t>(a.d1), static_cast<uint64_t>(a.x1_rows)};
     const uint64_t strides[1] = {static_cast<uint64_t>(a.d1) * 2};
@@ -841,12 +1029,14 @@ hxm_status umma_estmm(const EstmmArgs& a, cudaStream_t st) {
   prm.b_gather = gb;
   prm.M = static_cast<int>(a.d1);
   prm.N = static_cast<int>(a.d2);
-  prm.n_mt = static_cast<int>(ceil_div(a.d1, BM));
+  prm.n_mt = static_cast<int>(ceil_div(a.d1, BM * CG));
   prm.n_nt = static_cast<int>(a.d2 / bn);
   prm.tiles = a.tiles;
   prm.n_tiles = a.n_tiles;
   prm.est_out = a.out;
-  return launch_bn_any<3>(bn, prm, a.max_tiles * prm.n_mt * prm.n_nt, st);
+  const int work = a.max_tiles * prm.n_mt * prm.n_nt;
+  if (CG == 2) return launch_bn_any<3, 2>(bn, prm, work, st);
+  return launch_bn_any<3, 1>(bn, prm, work, st);
 }
 
 }  // namespace hxm
