@@ -165,30 +165,20 @@ __device__ __forceinline__ uint32_t mapa0(uint32_t local) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(local));
   return r;
 }
+// Arrivals on the leader's barriers.  Default (cta-scope) semantics, as in
+// CUTLASS's ClusterBarrier: what they order is TMA / TMEM traffic, which the
+// tcgen05 fences cover; a .cluster-scope release/acquire would make ptxas
+// emit MEMBAR / CCTL.IVALL (L1 invalidation) on every spin.
 __device__ __forceinline__ void mbar_arrive_tx_cl(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(bar),
-               "r"(bytes)
+  asm volatile("mbarrier.arrive.expect_tx.shared::cluster.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_cl(uint32_t bar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar)
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
 }
-// wait with cluster-scope acquire (barriers that receive the peer's arrivals)
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity);
 __device__ __forceinline__ void mbar_wait_cl(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = smem_u32(bar);
-  uint32_t done;
-  const long long t0 = clock64();
-  while (true) {
-    asm volatile(
-        "{\n.reg .pred P;\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n"
-        "selp.u32 %0, 1, 0, P;\n}\n"
-        : "=r"(done)
-        : "r"(a), "r"(parity)
-        : "memory");
-    if (done) return;
-    if (clock64() - t0 > (1ll << 34)) __trap();
-  }
+  mbar_wait(bar, parity);
 }
 // TMA loads whose completion is signalled on the leader CTA's barrier
 __device__ __forceinline__ void tma_2d_cg2(void* dst, const CUtensorMap* map, uint32_t bar, int c0,
