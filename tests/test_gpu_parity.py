@@ -335,6 +335,31 @@ def test_layer_c2_full_size_properties():
     assert torch.isfinite(g.gw1).all() and torch.isfinite(g.gx).all()
 
 
+@pytest.mark.parametrize("E,k,D,Hd,N,dtype", [
+    (1, 1, 64, 128, 1, torch.bfloat16),     # one token, one expert
+    (3, 3, 64, 128, 5, torch.bfloat16),     # k == E
+    (2, 1, 8, 16, 0, torch.float32),        # no tokens
+    (2, 1, 64, 64, 0, torch.bfloat16),
+    (5, 2, 64, 256, 130, torch.bfloat16),   # segments straddling 64/128/256 rows
+])
+def test_layer_edge_cases(E, k, D, Hd, N, dtype):
+    H = hx()
+    p, x = H.make_random_params(E, D, Hd, D, "gelu", seed=E + N, n_tokens=max(N, 1), dtype=dtype)
+    x = x[:N]
+    r = H.synthesize_routing(N, E, k, "uniform", 3) if N else \
+        H.RoutingChoice(0, E, k, np.zeros((k, 0), np.int32))
+    gy = torch.as_tensor(np.random.default_rng(1).standard_normal((N, D))).to("cuda", dtype)
+    fw = H.moe_forward(x, p, r)
+    g = H.moe_backward(fw.stash, p, gy)
+    torch.cuda.synchronize()
+    if N == 0:
+        assert fw.y.shape == (0, D)
+        for key in ("gw1", "gb1", "gw2", "gb2"):
+            assert torch.count_nonzero(getattr(g, key)) == 0, key  # es_ops.cpp:202 zeros
+        return
+    _check_layer(p, x, r, gy, RTOL_BF16 if dtype == torch.bfloat16 else RTOL_F32, "gelu")
+
+
 def test_layer_routing_validation():
     H = hx()
     p, x = H.make_random_params(2, 8, 16, 8, "gelu", seed=28, n_tokens=4)
