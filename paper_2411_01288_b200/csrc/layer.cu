@@ -175,7 +175,8 @@ hxm_status hxm_moe_forward(const hxm_layer_desc* d, const void* x, const void* w
                            const int32_t* assignments, float* y, void* ws, size_t ws_bytes,
                            int32_t* status, hxm_stream_t stream) {
   HXM_RETURN_IF(check_desc(d));
-  if (!x || !w1 || !b1 || !w2 || (d->add_b2 && !b2) || !assignments || !y)
+  const bool tok = d->n_tokens > 0;  // token tensors may be empty (null) when N == 0
+  if ((tok && (!x || !assignments || !y)) || !w1 || !b1 || !w2 || (d->add_b2 && !b2))
     return invalid_arg("moe_forward: null tensor");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   Arena ar(ws, ws_bytes);
@@ -183,7 +184,7 @@ hxm_status hxm_moe_forward(const hxm_layer_desc* d, const void* x, const void* w
   if (ar.overflow) return invalid_arg("moe_forward: workspace too small");
   const hxm_dtype dt = static_cast<hxm_dtype>(d->dtype);
   const int64_t N = d->n_tokens, E = d->n_experts, slots = d->k * N;
-  HXM_TRY_CUDA(cudaMemsetAsync(y, 0, sizeof(float) * N * d->d_out, st));
+  if (N > 0) HXM_TRY_CUDA(cudaMemsetAsync(y, 0, sizeof(float) * N * d->d_out, st));
   if (status && N > 0 && d->k > 1) {
     check_distinct<<<std::max<int64_t>(1, std::min<int64_t>(1024, ceil_div(N, 256))), 256, 0,
                      st>>>(assignments, N, static_cast<int>(d->k), static_cast<int>(E), status);
@@ -253,7 +254,9 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
                             float* gw1, float* gb1, float* gw2, float* gb2, float* gx,
                             hxm_stream_t stream) {
   HXM_RETURN_IF(check_desc(d));
-  if (!x || !w1 || !w2 || !g_y || !gw1 || !gb1 || !gw2 || (d->add_b2 && !gb2) || !gx)
+  const bool tok = d->n_tokens > 0;  // token tensors may be empty (null) when N == 0
+  if ((tok && (!x || !g_y || !gx)) || !w1 || !w2 || !gw1 || !gb1 || !gw2 ||
+      (d->add_b2 && !gb2))
     return invalid_arg("moe_backward: null tensor");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   Arena ar(ws, ws_bytes);
@@ -262,7 +265,7 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
   const hxm_dtype dt = static_cast<hxm_dtype>(d->dtype);
   const int64_t N = d->n_tokens, E = d->n_experts;
   const int64_t Di = d->d_in, H = d->hidden, Do = d->d_out;
-  HXM_TRY_CUDA(cudaMemsetAsync(gx, 0, sizeof(float) * N * Di, st));
+  if (N > 0) HXM_TRY_CUDA(cudaMemsetAsync(gx, 0, sizeof(float) * N * Di, st));
   // tile tables were built by hxm_moe_forward (they live in the stash)
   const RowMap slot = map_slot(w.v, N > 0 ? N : 1);
   // (4) gb2 = sum_i ESS(g_y, R_i)             (moe_layer.cpp:103)

@@ -153,6 +153,10 @@ __device__ __forceinline__ void bulk_wait0() {
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// named barrier among a subset of warps (id 0 is __syncthreads)
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
 
 // ---- CTA-pair (cluster of 2) helpers ----------------------------------------
 __device__ __forceinline__ void cluster_sync() {
@@ -281,8 +285,11 @@ __device__ __forceinline__ void act_both(int act, float x, float& f, float& df) 
 struct UParams {
   CUtensorMap tmA;  // ESMM A / ESTMM X1
   CUtensorMap tmB;  // ESMM W / ESTMM X2
-  CUtensorMap tmO1;  // MODE 1/2: dense bf16 stash output(s), 32 x 32 boxes
+  CUtensorMap tmO1;  // MODE 1/2: dense bf16 stash output(s), 32-col x 128-row boxes
   CUtensorMap tmO2;
+  CUtensorMap tmO1s;  // the same outputs, 32 x 32 boxes (segment-end slices)
+  CUtensorMap tmO2s;
+  CUtensorMap tmY;  // MODE 2: F'(y1) stash, 32 x 128 boxes
   RowMap amap;      // gather map of A (ESMM rows / ESTMM X1 rows)
   RowMap bmap;      // ESTMM X2 rows
   int a_gather, b_gather, b_kmajor;
@@ -303,13 +310,14 @@ struct UParams {
 
 // CG = CTAs per UMMA (cta_group): with CG = 2 a CTA pair runs M = 256 tiles,
 // each CTA holding 128 rows of A / D and half (BN/2) of the B columns.
-template <int BN, int CG = 1>
+template <int BN, int CG = 1, int MODE = 0>
 struct Cfg {
   static constexpr int kBBytes = (BN / CG) * BK * 2;
   static constexpr int kStage = kABytes + kBBytes;
-  // 227 KB opt-in smem = stages + per-epilogue-warp staging (4 KB each) +
-  // 1 KB alignment slack + barriers
-  static constexpr int kStaging = kEpiWarps * 4096;
+  // 227 KB opt-in smem = stages + epilogue staging + 1 KB alignment slack +
+  // barriers.  Staging: 4 KB per epilogue warp (MODE 0 / 3; MODE 1 uses it as
+  // two 16 KB half-group boxes), MODE 2 adds two 8 KB F'(y1) boxes per half.
+  static constexpr int kStaging = MODE == 2 ? 49152 : kEpiWarps * 4096;
   static constexpr int kBudget = 232448 - 1024 - 256 - kStaging;
   static constexpr int kStages = kBudget / kStage > 8 ? 8 : kBudget / kStage;
   static constexpr int kSmem = kStages * kStage + kStaging + 1024 /*align*/ + 256 /*barriers*/;
@@ -327,7 +335,7 @@ struct Cfg {
 template <int BN, int MODE, int CG = 1>
 __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant__ UParams p) {
   constexpr bool ESTMM = MODE == 3;
-  using C = Cfg<BN, CG>;
+  using C = Cfg<BN, CG, MODE>;
   uint32_t rank = 0;
   if constexpr (CG == 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   const int cluster = blockIdx.x / CG, n_clusters = gridDim.x / CG;
@@ -339,7 +347,8 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* dbar = tempty + 2;  // MODE 2: F'(y1) box loads, [half][buffer]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dbar + 4);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
@@ -351,6 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], kEpiWarps * CG);
     }
+    for (int b = 0; b < 4; ++b) mbar_init(&dbar[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -572,6 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
     };
     int acc = 0;
     uint32_t aph = 0;
+    int dchunk = 0;  // MODE 2: running chunk count (F'(y1) buffer / phase)
     for (int w = cluster; w < total; w += n_clusters) {
       const SegTile t = p.tiles[w / per_item];
       const int rem = w % per_item;
@@ -585,16 +596,19 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
         const int N = p.N;
         constexpr bool bwd = MODE == 2;
         constexpr bool dense_out = MODE == 1 || MODE == 2;
-        // F'(y1) operand (MODE 2, from the stash): issued before the
-        // accumulator wait so the loads overlap this tile's MMA (two 32-column
-        // chunks ahead; later chunks are fetched two ahead inside the loop to
-        // bound register pressure)
-        uint4 yv[HB / 8];
-        const uint4* y4 = reinterpret_cast<const uint4*>(
-            static_cast<const __nv_bfloat16*>(p.y1s) + static_cast<int64_t>(q) * N + n0);
-        if (bwd && valid) {
-#pragma unroll
-          for (int i = 0; i < (HB / 8 < 8 ? HB / 8 : 8); ++i) yv[i] = __ldg(y4 + i);
+        // dense bf16 outputs (MODE 1/2): the 4 warps of a column half stage a
+        // 128-row x 32-column box per chunk and one elected thread TMA-stores
+        // it (and, MODE 2, TMA-loads the matching F'(y1) box, double-buffered).
+        // The layer's segments end on 64-row boundaries, so every 32-row warp
+        // slice is entirely valid or entirely past the segment end.
+        const int qbase = t.begin + static_cast<int>(rank) * BM;  // row 0 of the box
+        const int rows_here = t.end - qbase;
+        const bool elect = ((warp - 2) & 3) == 0 && lane == 0;
+        uint8_t* hstage = staging + half * (C::kStaging / 2);  // this half-group's staging
+        if (bwd && elect) {  // F'(y1) box of chunk 0, overlapping the MMA
+          const int b = dchunk & 1;
+          mbar_arrive_tx(&dbar[half * 2 + b], 8192);
+          tma_2d(hstage + 8192 + b * 8192, &p.tmY, &dbar[half * 2 + b], n0, qbase);
         }
         // bias of this warp's HB columns: lane l holds columns 4l..4l+3,
         // broadcast by shuffles (loaded before the wait)
@@ -621,10 +635,6 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
           uint32_t (&r)[32] = rbuf[(c0 / 32) & 1];
           // next chunk's TMEM load overlaps this chunk's math
           if (c0 + 32 < HB) tmem_ld32_async(taddr + c0 + 32, rbuf[((c0 / 32) + 1) & 1]);
-          if (bwd && valid && c0 + 64 < HB) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) yv[(c0 + 64) / 8 + i] = __ldg(y4 + (c0 + 64) / 8 + i);
-          }
           const int n = n0 + c0;
           float v[32];
 #pragma unroll
@@ -640,13 +650,27 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
             }
           }
           if (dense_out) {
-            // bf16 rows of the sorted stash: stage 2 KB per output
             const bool pad = orow < 0;  // padding slot -> zero row
-            // all 32 rows of this warp inside the segment (always, for the
-            // layer's 64-aligned segments): TMA-store the staged 32 x 32 box
-            const bool full_warp = q0 + 31 < t.end;
-            if (lane == 0) bulk_wait_read0();  // staging free again
-            __syncwarp();
+            const int hrow = lg * 32 + lane;  // this thread's row in the 128-row box
+            const int swz = (hrow >> 1) & 3;  // TMA 64B swizzle: chunk ^= (row >> 1) & 3
+            // (1) the previous chunk's box has been read by its TMA store,
+            //     and every thread is past the previous chunk's F'(y1) reads
+            if (elect) bulk_wait_read0();
+            named_bar_sync(1 + half, 128);
+            if (bwd && elect && c0 + 32 < HB) {  // prefetch the next F'(y1) box
+              const int b = (dchunk + 1) & 1;
+              mbar_arrive_tx(&dbar[half * 2 + b], 8192);
+              tma_2d(hstage + 8192 + b * 8192, &p.tmY, &dbar[half * 2 + b], n + 32, qbase);
+            }
+            uint4 dv[4];
+            if (bwd) {  // this row's F'(y1) chunk from the staged box
+              const int b = dchunk & 1;
+              mbar_wait(&dbar[half * 2 + b], (dchunk >> 1) & 1);
+              const uint8_t* src = hstage + 8192 + b * 8192 + hrow * 64;
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                dv[j] = *reinterpret_cast<const uint4*>(src + ((j ^ swz) * 16));
+            }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               uint32_t a1[4], a2[4];
@@ -661,9 +685,8 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
                   a2[i] = pad ? 0u : pack_bf16(f0, f1);
                 }
               } else {
-                // g_y1 = g_y2 * F'(y1), F'(y1) read from the stash
-                const uint4 yy = yv[c0 / 8 + j];
-                const __nv_bfloat16* yb = reinterpret_cast<const __nv_bfloat16*>(&yy);
+                // g_y1 = g_y2 * F'(y1)
+                const __nv_bfloat16* yb = reinterpret_cast<const __nv_bfloat16*>(&dv[j]);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                   const float g0 = v[8 * j + 2 * i] * __bfloat162float(yb[2 * i]);
@@ -671,39 +694,29 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
                   a1[i] = pad ? 0u : pack_bf16(g0, g1);
                 }
               }
-              // 64B swizzle (TMA pattern: chunk ^= (row >> 1) & 3) for the
-              // TMA store; plain XOR for the LDS read-back path
-              const int sw = (full_warp ? (j ^ ((lane >> 1) & 3)) : (j ^ (lane & 3))) * 16;
-              *reinterpret_cast<uint4*>(stg + lane * 64 + sw) = make_uint4(a1[0], a1[1], a1[2], a1[3]);
+              *reinterpret_cast<uint4*>(hstage + hrow * 64 + ((j ^ swz) * 16)) =
+                  make_uint4(a1[0], a1[1], a1[2], a1[3]);
               if (!bwd)
-                *reinterpret_cast<uint4*>(stg + 2048 + lane * 64 + sw) =
+                *reinterpret_cast<uint4*>(hstage + 8192 + hrow * 64 + ((j ^ swz) * 16)) =
                     make_uint4(a2[0], a2[1], a2[2], a2[3]);
             }
-            if (full_warp) {
-              fence_async_smem();
-              __syncwarp();
-              if (lane == 0) {
-                tma_store_2d(&p.tmO1, stg, n, q0);
-                if (!bwd) tma_store_2d(&p.tmO2, stg + 2048, n, q0);
-                bulk_commit();
+            // (2) box complete -> one TMA store per output (or per valid
+            //     32-row slice at a segment end)
+            fence_async_smem();
+            named_bar_sync(1 + half, 128);
+            if (elect && rows_here > 0) {
+              if (rows_here >= BM) {
+                tma_store_2d(&p.tmO1, hstage, n, qbase);
+                if (!bwd) tma_store_2d(&p.tmO2, hstage + 8192, n, qbase);
+              } else {
+                for (int sl = 0; sl * 32 < rows_here; ++sl) {
+                  tma_store_2d(&p.tmO1s, hstage + sl * 2048, n, qbase + sl * 32);
+                  if (!bwd) tma_store_2d(&p.tmO2s, hstage + 8192 + sl * 2048, n, qbase + sl * 32);
+                }
               }
-              goto chunk_done;
+              bulk_commit();
             }
-            __syncwarp();
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int rr = i * 8 + lane / 4, cc = lane % 4;
-              const bool ok = q0 + rr < t.end;
-              const int so = rr * 64 + ((cc ^ (rr & 3)) * 16);
-              const int64_t off = static_cast<int64_t>(q0 + rr) * N + n + cc * 8;
-              if (ok) {
-                *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out1) + off) =
-                    *reinterpret_cast<const uint4*>(stg + so);
-                if (!bwd)
-                  *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out2) + off) =
-                      *reinterpret_cast<const uint4*>(stg + 2048 + so);
-              }
-            }
+            ++dchunk;
           } else {
             // fp32 rows scattered to token order: stage 4 KB (32 x 128 B)
             __syncwarp();
@@ -730,7 +743,6 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
               }
             }
           }
-        chunk_done:
           if (c0 + 32 < HB) {
             tmem_wait();
             if (c0 + 64 >= HB) {  // last TMEM load landed: free the accumulator
@@ -858,7 +870,7 @@ int pick_bn2(int64_t n, bool b_mn) {
 
 template <int BN, int MODE, int CG>
 hxm_status launch_bn(const UParams& prm, int max_work, cudaStream_t st) {
-  using C = Cfg<BN, CG>;
+  using C = Cfg<BN, CG, MODE>;
   auto kern = umma_kernel<BN, MODE, CG>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -973,12 +985,16 @@ hxm_status umma_esmm(const EsmmArgs& a, cudaStream_t st) {
     // 32 x 32 boxes stored by TMA from the epilogue's 64B-swizzled staging
     const uint64_t dims[2] = {static_cast<uint64_t>(a.d2), static_cast<uint64_t>(a.a_rows)};
     const uint64_t strides[1] = {static_cast<uint64_t>(a.d2) * 2};
-    const uint32_t box[2] = {32, 32};
-    if (!make_map(&prm.tmO1, a.out1, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B))
-      return invalid_arg("umma_esmm: cannot encode the output tensor map");
-    if (a.epi == EPI_FWD_ACT &&
-        !make_map(&prm.tmO2, a.out2, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B))
-      return invalid_arg("umma_esmm: cannot encode the output tensor map");
+    const uint32_t box[2] = {32, 128}, box_s[2] = {32, 32};
+    const auto sw = CU_TENSOR_MAP_SWIZZLE_64B;
+    bool ok = make_map(&prm.tmO1, a.out1, 2, dims, strides, box, sw) &&
+              make_map(&prm.tmO1s, a.out1, 2, dims, strides, box_s, sw);
+    if (a.epi == EPI_FWD_ACT)
+      ok = ok && make_map(&prm.tmO2, a.out2, 2, dims, strides, box, sw) &&
+           make_map(&prm.tmO2s, a.out2, 2, dims, strides, box_s, sw);
+    else
+      ok = ok && make_map(&prm.tmY, a.y1s, 2, dims, strides, box, sw);
+    if (!ok) return invalid_arg("umma_esmm: cannot encode the stash tensor maps");
   }
   const int work = a.max_tiles * prm.n_nt;
   if (CG == 2) {
