@@ -125,8 +125,12 @@ def dist_init(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if ws > 1:
+    if ws > 1 or args.mode in ("data_centric", "model_centric"):
         import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(ws))
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
@@ -235,9 +239,28 @@ def run_ours(args, cfg, rank, ws, local):
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
     L = _lib.lib()
-    use_graph = ws == 1 and not args.no_graph
+    mode = args.mode if args.mode != "auto" else ("single" if ws == 1 else "data_centric")
+    use_graph = mode == "single" and not args.no_graph
 
-    if ws == 1:
+    if mode == "model_centric":
+        # model-centric TP along H (dist_sim.cpp:454-601): tokens / routing /
+        # g_y all-gathered, each rank runs the global batch on its H-slice,
+        # partial y and g_x reduce-scattered back to the token owners
+        from paper_2411_01288_b200 import dist as HD
+        sp = HD.shard_params(p, HD.even_split(Hd, ws))
+        shard, b2 = sp.shards[rank], sp.b2
+        del p, sp
+        comp = HD.cuda_compute()
+        mc_out = {}
+
+        def mc_step():
+            res = HD.model_centric_step(x, a, gy, shard, b2, "gelu", comp, reduce="reduce_scatter")
+            mc_out["y"] = res.y
+            return res
+        mc_step()
+        torch.cuda.synchronize()
+        y_out = mc_out["y"]
+    elif mode == "single":
         run = LayerRunner(p, N, k, dev, dtype)
         # warm-up (also validates routing once)
         status = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -258,7 +281,12 @@ def run_ours(args, cfg, rank, ws, local):
         del p, sp
         run = dc.runner
         y_out = run.y
-    step_fn = (lambda: run.step(x, a, gy)) if ws == 1 else (lambda: dc.step(x, a, gy))
+    if mode == "single":
+        step_fn = lambda: run.step(x, a, gy)  # noqa: E731
+    elif mode == "data_centric":
+        step_fn = lambda: dc.step(x, a, gy)  # noqa: E731
+    else:
+        step_fn = mc_step
     for _ in range(max(0, args.warmup - 1)):
         step_fn()
     graph_kernels = 0
@@ -327,7 +355,7 @@ def run_ours(args, cfg, rank, ws, local):
             a.copy_(ah, non_blocking=True)
             gy.copy_(gyh, non_blocking=True)
             step_fn()
-            yh.copy_(y_out, non_blocking=True)
+            yh.copy_(mc_out["y"] if mode == "model_centric" else y_out, non_blocking=True)
 
     for _ in range(2):
         e2e_step()
@@ -391,7 +419,7 @@ def run_ours(args, cfg, rank, ws, local):
         "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
         "config": {"workload": args.config, "desc": cfg["desc"], "E": E, "k": k, "d": D,
                    "ffn": Hd, "tokens_per_gpu": N, "routing": cfg["dist"],
-                   "parallelism": f"data_centric_tp{ws}" if ws > 1 else "single",
+                   "parallelism": f"{mode}_tp{ws}" if mode != "single" else "single",
                    "cuda_graph": use_graph,
                    "l2": "flushed between steps (256 MiB write, outside the timed events)"},
         "layer_tflops": flop_step * args.steps * ws / (total_ms / 1e3) / 1e12,
@@ -415,6 +443,9 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="auto",
+                    choices=["auto", "single", "data_centric", "model_centric"],
+                    help="auto: single GPU at N=1, data-centric TP along H at N>1")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the step eagerly instead of replaying its CUDA graph")
     args = ap.parse_args()
@@ -429,8 +460,8 @@ def main():
     try:
         run_ours(args, cfg, rank, ws, local)
     finally:
-        if ws > 1:
-            import torch.distributed as dist
+        import torch.distributed as dist
+        if dist.is_initialized():
             dist.destroy_process_group()
 
 
