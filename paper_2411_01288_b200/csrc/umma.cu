@@ -332,7 +332,7 @@ struct Cfg {
 // issues tcgen05.mma.cta_group::2 with M = 256; both CTAs' TMA loads signal
 // the leader's full barrier; commits multicast to both CTAs' empty / tfull
 // barriers; both CTAs' epilogues arrive on the leader's tempty barrier.
-template <int BN, int MODE, int CG = 1>
+template <int BN, int MODE, int CG = 1, int ACT = -1>
 __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant__ UParams p) {
   constexpr bool ESTMM = MODE == 3;
   using C = Cfg<BN, CG, MODE>;
@@ -679,8 +679,9 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                   float f0, d0, f1, d1;
-                  act_both(p.act, v[8 * j + 2 * i], f0, d0);
-                  act_both(p.act, v[8 * j + 2 * i + 1], f1, d1);
+                  // activation fixed at compile time (MODE 1 instantiations)
+                  act_both(ACT >= 0 ? ACT : p.act, v[8 * j + 2 * i], f0, d0);
+                  act_both(ACT >= 0 ? ACT : p.act, v[8 * j + 2 * i + 1], f1, d1);
                   a1[i] = pad ? 0u : pack_bf16(d0, d1);
                   a2[i] = pad ? 0u : pack_bf16(f0, f1);
                 }
@@ -868,10 +869,10 @@ int pick_bn2(int64_t n, bool b_mn) {
   return pick_bn(n);
 }
 
-template <int BN, int MODE, int CG>
+template <int BN, int MODE, int CG, int ACT = -1>
 hxm_status launch_bn(const UParams& prm, int max_work, cudaStream_t st) {
   using C = Cfg<BN, CG, MODE>;
-  auto kern = umma_kernel<BN, MODE, CG>;
+  auto kern = umma_kernel<BN, MODE, CG, ACT>;
   static bool attr_set = false;
   if (!attr_set) {
     HXM_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
@@ -902,14 +903,21 @@ hxm_status launch_bn(const UParams& prm, int max_work, cudaStream_t st) {
   return HXM_OK;
 }
 
-template <int MODE, int CG>
+template <int MODE, int CG, int ACT = -1>
 hxm_status launch_bn_any(int bn, const UParams& prm, int max_work, cudaStream_t st) {
   switch (bn) {
-    case 256: return launch_bn<256, MODE, CG>(prm, max_work, st);
-    case 192: return launch_bn<192, MODE, CG>(prm, max_work, st);
-    case 128: return launch_bn<128, MODE, CG>(prm, max_work, st);
-    default: return launch_bn<64, MODE, CG>(prm, max_work, st);
+    case 256: return launch_bn<256, MODE, CG, ACT>(prm, max_work, st);
+    case 192: return launch_bn<192, MODE, CG, ACT>(prm, max_work, st);
+    case 128: return launch_bn<128, MODE, CG, ACT>(prm, max_work, st);
+    default: return launch_bn<64, MODE, CG, ACT>(prm, max_work, st);
   }
+}
+// the forward activation epilogue is specialised per activation
+template <int CG>
+hxm_status launch_fwd_act(int act, int bn, const UParams& prm, int max_work, cudaStream_t st) {
+  if (act == HXM_ACT_GELU) return launch_bn_any<1, CG, HXM_ACT_GELU>(bn, prm, max_work, st);
+  if (act == HXM_ACT_RELU) return launch_bn_any<1, CG, HXM_ACT_RELU>(bn, prm, max_work, st);
+  return launch_bn_any<1, CG, HXM_ACT_IDENTITY>(bn, prm, max_work, st);
 }
 
 // rows of the tensor behind a row map: gathered sources are bounded by the
@@ -998,11 +1006,11 @@ hxm_status umma_esmm(const EsmmArgs& a, cudaStream_t st) {
   }
   const int work = a.max_tiles * prm.n_nt;
   if (CG == 2) {
-    if (a.epi == EPI_FWD_ACT) return launch_bn_any<1, 2>(bn, prm, work, st);
+    if (a.epi == EPI_FWD_ACT) return launch_fwd_act<2>(a.act, bn, prm, work, st);
     if (a.epi == EPI_BWD_ACT) return launch_bn_any<2, 2>(bn, prm, work, st);
     return launch_bn_any<0, 2>(bn, prm, work, st);
   }
-  if (a.epi == EPI_FWD_ACT) return launch_bn_any<1, 1>(bn, prm, work, st);
+  if (a.epi == EPI_FWD_ACT) return launch_fwd_act<1>(a.act, bn, prm, work, st);
   if (a.epi == EPI_BWD_ACT) return launch_bn_any<2, 1>(bn, prm, work, st);
   return launch_bn_any<0, 1>(bn, prm, work, st);
 }
