@@ -292,44 +292,52 @@ def run_ours(args, cfg, rank, ws, local):
     graph_kernels = 0
     L.hxm_profile_reset()
     if use_graph:
-        L.hxm_profile_enable(1)  # the region events are recorded into the graph
+        # two graphs of the same step: the timed one carries no event nodes;
+        # the profiled one (per-kernel event pairs recorded as graph nodes)
+        # gives the kernel durations in a second pass of K steps
         c0 = L.hxm_launch_count()
         run.capture(x, a, gy)
         graph_kernels = (L.hxm_launch_count() - c0) // 2  # capture() warms once
-        L.hxm_profile_enable(0)
-        L.hxm_profile_reset()
+        g_plain = run.graph
         L.hxm_profile_enable(1)
-        run.capture(x, a, gy, warm=False)  # re-record: the profile holds one step
+        run.capture(x, a, gy, warm=False)
         L.hxm_profile_enable(0)
-        step_fn = run.replay
+        g_prof = run.graph
+        step_fn = g_plain.replay
         for _ in range(2):
-            step_fn()
+            g_plain.replay()
+            g_prof.replay()
     barrier(ws)
 
-    # ---- device-resident timed region ------------------------------------
-    if not use_graph:
-        L.hxm_profile_reset()
-    launches0 = L.hxm_launch_count()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    clocks = ClockSampler(local, period=0.005)
-    barrier(ws)
-    with clocks:
-        if not use_graph:
+    def timed(fn, profile_eager):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        barrier(ws)
+        if profile_eager:
+            L.hxm_profile_reset()
             L.hxm_profile_enable(1)
         for i in range(args.steps):
             flush.zero_()  # L2 flush outside the step's events
             evs[i][0].record(stream)
-            step_fn()
+            fn()
             evs[i][1].record(stream)
         L.hxm_profile_enable(0)
         barrier(ws)
-    launches = L.hxm_launch_count() - launches0
-    if use_graph:
-        launches = graph_kernels * args.steps  # each replay runs the captured kernels
-    step_ms = [s.elapsed_time(e) for s, e in evs]
-    total_ms = max_over_ranks(sum(step_ms), ws)
-    prof = _lib.profile_read()  # graph: the last replay's kernel regions
+        return sum(s.elapsed_time(e) for s, e in evs)
+
+    # ---- device-resident timed region ------------------------------------
+    launches0 = L.hxm_launch_count()
+    clocks = ClockSampler(local, period=0.005)
+    with clocks:
+        total_ms = max_over_ranks(timed(step_fn, not use_graph), ws)
+        launches = L.hxm_launch_count() - launches0
+        prof_ms = None
+        if use_graph:
+            launches = graph_kernels * args.steps  # each replay runs the captured kernels
+            # second pass: the profiled graph (its event nodes hold the last
+            # replay's per-kernel durations)
+            prof_ms = max_over_ranks(timed(g_prof.replay, False), ws)
+    prof = _lib.profile_read()
     L.hxm_profile_reset()
     value = N * ws * args.steps / (total_ms / 1000.0)
 
@@ -421,7 +429,10 @@ def run_ours(args, cfg, rank, ws, local):
                    "ffn": Hd, "tokens_per_gpu": N, "routing": cfg["dist"],
                    "parallelism": f"{mode}_tp{ws}" if mode != "single" else "single",
                    "cuda_graph": use_graph,
+                   "kernel_times": "second K-step pass of the same step captured with per-kernel "
+                                   "event nodes" if use_graph else "events around each launch",
                    "l2": "flushed between steps (256 MiB write, outside the timed events)"},
+        "ms_per_step_profiled": (prof_ms / args.steps) if prof_ms else None,
         "layer_tflops": flop_step * args.steps * ws / (total_ms / 1e3) / 1e12,
         "layer_frac_of_bf16_sustained": flop_step * args.steps / (total_ms / 1e3) / 1e12
         / pk["tensor_sustained"],
@@ -448,10 +459,15 @@ def main():
                     help="auto: single GPU at N=1, data-centric TP along H at N>1")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the step eagerly instead of replaying its CUDA graph")
+    ap.add_argument("--shape", default=None,
+                    help="experiment override E,k,D,H,N of the chosen config (not a bench line)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.shape:
+        E, k, D, H, N = (int(v) for v in args.shape.split(","))
+        cfg.update(E=E, k=k, D=D, H=H, N=N, desc=f"experiment shape {args.shape}")
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))
         run_reference(args, cfg, rank, int(os.environ.get("WORLD_SIZE", "1")))

@@ -7,6 +7,8 @@
 // Two deterministic phases, no float atomics:
 //   ess_partial : one CTA per <=128-position segment tile -> partial[tile][D]
 //   ess_combine : out[e][d] = sum of e's tile partials in tile order.
+#include <cooperative_groups.h>
+
 #include "kernels.cuh"
 
 namespace hxm {
@@ -41,22 +43,22 @@ __device__ __forceinline__ void store_vec(T* p, const float (&v)[VEC]) {
   }
 }
 
+// One (segment tile, column slab) item: the tile's rows summed into
+// partial[tile] (and optionally copied to expert-sorted order).  The 8 warps
+// split the tile's rows, each keeping U = 4 row loads in flight, and are
+// combined in a fixed order through smem (deterministic).
 template <class T, int VEC>
-__global__ void __launch_bounds__(NT) ess_partial(EssArgs a) {
-  // grid: x = segment tile (<= 128 positions), y = column slab of 32 vector
-  // groups (one per lane); the 8 warps split the tile's rows, each keeping
-  // U = 4 row loads in flight, and are combined in fixed order through smem.
-  const int ti = blockIdx.x;
-  if (ti >= *a.n_tiles) return;
+__device__ __forceinline__ void ess_item(const EssArgs& a, int ti, int slab) {
   const SegTile tile = a.tiles[ti];
   const T* X = static_cast<const T*>(a.x);
   const int64_t D = a.d;
   const int col_groups = static_cast<int>((D + VEC - 1) / VEC);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   constexpr int W = NT / 32;
-  const int cg = blockIdx.y * 32 + lane;
+  const int cg = slab * 32 + lane;
   __shared__ int rows[kEssRows];
   __shared__ float red[W][32 * VEC];
+  __syncthreads();  // previous item's smem reads are done
   for (int i = threadIdx.x; i < kEssRows; i += NT) {
     const int64_t p = tile.begin + i;
     rows[i] = p < tile.end ? a.map(p) : -1;
@@ -102,7 +104,7 @@ __global__ void __launch_bounds__(NT) ess_partial(EssArgs a) {
   __syncthreads();
   // column sums in a fixed warp order (deterministic)
   for (int c = threadIdx.x; c < 32 * VEC; c += NT) {
-    const int64_t col = static_cast<int64_t>(blockIdx.y) * 32 * VEC + c;
+    const int64_t col = static_cast<int64_t>(slab) * 32 * VEC + c;
     if (col >= D) continue;
     float s = 0.f;
 #pragma unroll
@@ -111,14 +113,48 @@ __global__ void __launch_bounds__(NT) ess_partial(EssArgs a) {
   }
 }
 
+template <class T, int VEC>
+__global__ void __launch_bounds__(NT) ess_partial(EssArgs a) {
+  // grid: x = segment tile (<= 128 positions), y = column slab of 32 vector
+  // groups (one per lane)
+  if (static_cast<int>(blockIdx.x) >= *a.n_tiles) return;
+  ess_item<T, VEC>(a, blockIdx.x, blockIdx.y);
+}
+
+// out[e][c] = sum of partial rows r0..r1 (in order) -- 8 independent loads in
+// flight per thread instead of one dependent chain
+__device__ __forceinline__ float sum_rows(const float* __restrict__ partial, int64_t r0,
+                                          int64_t r1, int64_t d, int64_t c) {
+  float s = 0.f;
+  int64_t r = r0;
+  for (; r + 8 <= r1; r += 8) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = partial[(r + u) * d + c];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += v[u];
+  }
+  for (; r < r1; ++r) s += partial[r * d + c];
+  return s;
+}
+
 __global__ void ess_combine(EssArgs a) {
   const int e = blockIdx.y;
   const int64_t d = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (d >= a.d) return;
-  const int t0 = a.tile_off[e], t1 = a.tile_off[e + 1];
-  float s = 0.f;
-  for (int t = t0; t < t1; ++t) s += a.partial[static_cast<int64_t>(t) * a.d + d];
-  a.out[static_cast<int64_t>(e) * a.d + d] = s;
+  a.out[static_cast<int64_t>(e) * a.d + d] =
+      sum_rows(a.partial, a.tile_off[e], a.tile_off[e + 1], a.d, d);
+}
+
+__global__ void colsum_combine(const float* __restrict__ partial,
+                               const int32_t* __restrict__ tile_off, int parts, int64_t d,
+                               float* __restrict__ out) {
+  const int e = blockIdx.y;
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= d) return;
+  out[static_cast<int64_t>(e) * d + c] = sum_rows(
+      partial, static_cast<int64_t>(tile_off[e]) * parts,
+      static_cast<int64_t>(tile_off[e + 1]) * parts, d, c);
 }
 
 template <class T>
@@ -186,6 +222,72 @@ hxm_status gather_typed(const void* src, RowMap map, int64_t d, const int32_t* i
   return HXM_OK;
 }
 
+
+// ------------------------------------------------ fused backward prologue --
+// One cooperative launch before the backward GEMMs: g_x = 0, zeroed gW
+// slices of the experts whose ESTMM is split over chunks (they accumulate
+// with red.add), gb2 partials of g_y fused with its expert-sorted copy
+// (ESS, es_ops.cpp:86-102) | grid barrier | per-expert gb2 combine.
+template <class T, int VEC>
+__global__ void __launch_bounds__(NT) bwd_prologue(BwdPrologue b) {
+  namespace cgp = cooperative_groups;
+  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x;
+  const int64_t gthreads = static_cast<int64_t>(gridDim.x) * NT;
+  {
+    float4* g4 = reinterpret_cast<float4*>(b.gx);
+    const int64_t n4 = b.gx_elems / 4;
+    for (int64_t i = gtid; i < n4; i += gthreads) g4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t i = n4 * 4 + gtid; i < b.gx_elems; i += gthreads) b.gx[i] = 0.f;
+  }
+  // split experts: 16 block-sized parts of each first chunk's slices
+  constexpr int kParts = 16;
+  const int nk = *b.n_ktiles;
+  for (int it = blockIdx.x; it < nk * kParts; it += gridDim.x) {
+    const int ti = it / kParts, part = it % kParts;
+    const SegTile t = b.ktiles[ti];
+    if (!(t.flags & 1) || (ti > 0 && b.ktiles[ti - 1].expert == t.expert)) continue;
+    for (int o = 0; o < 2; ++o) {
+      float* out = o == 0 ? b.gw2 : b.gw1;
+      const int64_t slice = o == 0 ? b.gw2_slice : b.gw1_slice;
+      if (!out) continue;
+      out += static_cast<int64_t>(t.expert) * slice;
+      const int64_t per = ceil_div(slice, kParts);
+      const int64_t lo = part * per, hi = min(slice, lo + per);
+      for (int64_t i = lo + threadIdx.x; i < hi; i += NT) out[i] = 0.f;
+    }
+  }
+  const EssArgs& a = b.es;
+  const int col_groups = static_cast<int>((a.d + VEC - 1) / VEC);
+  const int slabs = static_cast<int>(ceil_div(col_groups, 32));
+  const int items = *a.n_tiles * slabs;
+  for (int it = blockIdx.x; it < items; it += gridDim.x) ess_item<T, VEC>(a, it / slabs, it % slabs);
+  if (!a.out) return;
+  cgp::this_grid().sync();
+  for (int64_t i = gtid; i < static_cast<int64_t>(a.n_experts) * a.d; i += gthreads) {
+    const int e = static_cast<int>(i / a.d);
+    const int64_t c = i % a.d;
+    a.out[i] = sum_rows(a.partial, a.tile_off[e], a.tile_off[e + 1], a.d, c);
+  }
+}
+
+template <class T>
+hxm_status bwd_prologue_typed(BwdPrologue& b, cudaStream_t st) {
+  constexpr int V = 16 / sizeof(T);
+  const EssArgs& a = b.es;
+  const bool vec_ok = (a.d % V == 0) && (reinterpret_cast<uintptr_t>(a.x) % 16 == 0) &&
+                      (reinterpret_cast<uintptr_t>(a.copy_out) % 16 == 0);
+  const void* kern = vec_ok ? reinterpret_cast<const void*>(bwd_prologue<T, V>)
+                            : reinterpret_cast<const void*>(bwd_prologue<T, 1>);
+  int occ = 0;
+  HXM_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, 0));
+  if (occ < 1) return invalid_arg("backward prologue: cannot be resident");
+  const int grid = sm_count() * std::min(occ, 4);
+  void* args[] = {&b};
+  HXM_TRY_CUDA(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(NT), args, 0, st));
+  HXM_CHECK_LAUNCH();
+  return HXM_OK;
+}
+
 }  // namespace
 
 hxm_status launch_gather_rows(hxm_dtype dt, const void* src, RowMap map, int64_t d,
@@ -194,6 +296,23 @@ hxm_status launch_gather_rows(hxm_dtype dt, const void* src, RowMap map, int64_t
   ProfScope ps(st, "gather_rows", work_bytes, WORK_BYTES);
   return dt == HXM_BF16 ? gather_typed<__nv_bfloat16>(src, map, d, idx, n_experts, bound, dst, st)
                         : gather_typed<float>(src, map, d, idx, n_experts, bound, dst, st);
+}
+
+hxm_status launch_colsum_combine(const float* partial, const int32_t* tile_off, int n_experts,
+                                 int parts, int64_t d, float* out, cudaStream_t st,
+                                 const char* label, double work_bytes) {
+  ProfScope ps(st, label ? label : "colsum_combine", work_bytes, WORK_BYTES);
+  if (d <= 0 || n_experts <= 0) return HXM_OK;
+  dim3 grid(static_cast<unsigned>(ceil_div(d, 128)), static_cast<unsigned>(n_experts));
+  colsum_combine<<<grid, 128, 0, st>>>(partial, tile_off, parts, d, out);
+  HXM_CHECK_LAUNCH();
+  return HXM_OK;
+}
+
+hxm_status launch_bwd_prologue(hxm_dtype dt, BwdPrologue b, cudaStream_t st) {
+  ProfScope ps(st, b.label ? b.label : "bwd_prologue", b.work, WORK_BYTES);
+  return dt == HXM_BF16 ? bwd_prologue_typed<__nv_bfloat16>(b, st)
+                        : bwd_prologue_typed<float>(b, st);
 }
 
 hxm_status launch_ess(hxm_dtype dt, const EssArgs& a, cudaStream_t st) {

@@ -62,6 +62,8 @@ struct EsmmArgs {
   void* out1;      // FWD_ACT / BWD_ACT dense outputs (dtype), row stride d2
   void* out2;
   const void* y1s;  // BWD_ACT: pre-activation stash (dtype), row stride d2
+  float* colsum;    // BWD_ACT (tcgen05): per-(tile, CTA) column sums of out1,
+                    // [(tile * CG + cta) x d2] -> colsum_combine (fused ESS)
 };
 
 struct EstmmArgs {
@@ -78,6 +80,7 @@ struct EstmmArgs {
   int max_tiles;
   int n_experts;
   float* out;  // E x d1 x d2
+  int skip_zero_split;  // split experts' slices already zeroed by the caller
 };
 
 struct EssArgs {
@@ -102,6 +105,31 @@ struct EssArgs {
 hxm_status launch_gather_rows(hxm_dtype dt, const void* src, RowMap map, int64_t d,
                               const int32_t* idx, int n_experts, int64_t bound, void* dst,
                               cudaStream_t st, double work_bytes = 0.0);
+
+// out[e] = sum over e's tiles t (tile_off[e]..tile_off[e+1]) and the
+// `parts` partial rows of each tile of partial[(t * parts + r) x d]: the
+// deterministic second phase of an ESS fused into a GEMM epilogue.
+hxm_status launch_colsum_combine(const float* partial, const int32_t* tile_off, int n_experts,
+                                 int parts, int64_t d, float* out, cudaStream_t st,
+                                 const char* label, double work_bytes);
+
+// The layer backward's prologue in one cooperative launch: gx = 0, zeroed
+// gW1 / gW2 slices of split ESTMM experts (per the ESTMM chunk table), and the
+// gb2 ESS of g_y fused with its expert-sorted copy (es.copy_out) + combine.
+struct BwdPrologue {
+  const char* label;
+  double work;
+  EssArgs es;
+  float* gx;
+  int64_t gx_elems;
+  const SegTile* ktiles;
+  const int32_t* n_ktiles;
+  float* gw2;
+  int64_t gw2_slice;
+  float* gw1;
+  int64_t gw1_slice;
+};
+hxm_status launch_bwd_prologue(hxm_dtype dt, BwdPrologue b, cudaStream_t st);
 
 constexpr int kEssRows = 128;
 constexpr int kSimtRows = 64;     // SIMT ESMM tile rows

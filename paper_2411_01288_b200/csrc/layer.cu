@@ -50,6 +50,7 @@ struct LayerWs {
   void* y1s;
   void* y2s;
   void* g1s;
+  float* colsum;  // tcgen05 path: per-(tile, CTA) column sums of g_y1 (fused gb1)
   int64_t bound;
   int max_tiles_a, max_ktiles, max_etiles;
   int rows_a;
@@ -100,6 +101,10 @@ LayerWs carve(Arena& ar, const hxm_layer_desc& d) {
   w.y1s = ar.take<char>(stash);
   w.y2s = ar.take<char>(stash);
   w.g1s = ar.take<char>(stash);
+  const char* fuse = std::getenv("HXM_FUSE_GB1");  // 0: separate ESS pass for gb1
+  if (w.rows_a >= kUmmaRows && !(fuse && fuse[0] == '0'))
+    w.colsum = ar.take<float>(static_cast<size_t>(max_tiles(w.bound, d.n_experts, w.rows_a)) *
+                              (w.rows_a / kUmmaRows) * d.hidden);
   return w;
 }
 
@@ -114,24 +119,6 @@ hxm_status check_desc(const hxm_layer_desc* d) {
   if (d->k * d->n_tokens + d->n_experts * kSortedBlk > 0x7fffffffLL)
     return invalid_arg("moe layer: k*N exceeds int32 slot range");
   return HXM_OK;
-}
-
-// Reference moe_layer.cpp:33-43 validates before any work; per-token
-// distinctness of the k choices (routing.cpp:30-39) is data-dependent and
-// checked on the device.
-__global__ void check_distinct(const int32_t* a, int64_t n, int k, int E, int32_t* status) {
-  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    for (int i = 0; i < k; ++i) {
-      const int ei = a[i * n + t];
-      if (ei < 0 || ei >= E) {
-        atomicExch(status, HXM_ERR_INVALID_ARG);
-        continue;
-      }
-      for (int j = i + 1; j < k; ++j)
-        if (a[j * n + t] == ei) atomicExch(status, HXM_ERR_INVALID_ARG);
-    }
-  }
 }
 
 // stash export: sorted row p (slot s = choice*N + t) -> token-order fp32
@@ -184,29 +171,42 @@ hxm_status hxm_moe_forward(const hxm_layer_desc* d, const void* x, const void* w
   if (ar.overflow) return invalid_arg("moe_forward: workspace too small");
   const hxm_dtype dt = static_cast<hxm_dtype>(d->dtype);
   const int64_t N = d->n_tokens, E = d->n_experts, slots = d->k * N;
-  if (N > 0) HXM_TRY_CUDA(cudaMemsetAsync(y, 0, sizeof(float) * N * d->d_out, st));
-  if (status && N > 0 && d->k > 1) {
-    check_distinct<<<std::max<int64_t>(1, std::min<int64_t>(1024, ceil_div(N, 256))), 256, 0,
-                     st>>>(assignments, N, static_cast<int>(d->k), static_cast<int>(E), status);
-    HXM_CHECK_LAUNCH();
+  // (0) one cooperative launch: routing validation, the k-choice slot index
+  // (v, idx), its three tilings (ESMM tiles, ESTMM chunks, ESS tiles -- the
+  // backward reuses them from the stash), y = 0 and the expert-sorted copy of
+  // x, so every later GEMM reads dense tiles
+  {
+    FwdPrologue pro{};
+    pro.a = assignments;
+    pro.n_slots = slots;
+    pro.n_tok = N;
+    pro.k = static_cast<int>(d->k);
+    pro.E = static_cast<int>(E);
+    pro.blk = kSortedBlk;
+    pro.v = w.v;
+    pro.idx = w.idx;
+    pro.s0 = {w.rows_a, 0, w.tiles_a, w.tiles_a_off, w.n_tiles_a};
+    pro.s1 = {kEstmmChunk, 1, w.ktiles, w.ktiles_off, w.n_ktiles};
+    pro.s2 = {kEssRows, 0, w.etiles, w.etiles_off, w.n_etiles};
+    pro.x = N > 0 ? x : nullptr;
+    pro.xs = w.xs;
+    pro.row_bytes = d->d_in * static_cast<int64_t>(esize(d->dtype));
+    pro.unit = (pro.row_bytes % 16 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0) ? 16
+               : (pro.row_bytes % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 4 == 0) ? 4 : 2;
+    pro.y = y;
+    pro.y_elems = N * d->d_out;
+    pro.status = status;
+    pro.ws = w.rws;
+    pro.ws_bytes = w.rws_bytes;
+    // algorithmic bytes: assignments read twice, v written, every routed
+    // slot's x row read and written once, y zeroed
+    const double bytes = 8.0 * slots + 4.0 * w.bound +
+                         2.0 * static_cast<double>(slots) * pro.row_bytes + 4.0 * N * d->d_out;
+    ProfScope ps(st, "fwd_prologue", bytes, WORK_BYTES);
+    HXM_RETURN_IF(launch_fwd_prologue(pro, st));
   }
-  HXM_RETURN_IF(build_reindex_slots(assignments, slots, E, kSortedBlk, w.v, w.idx, w.rws,
-                                    w.rws_bytes, status, st));
-  // the three tilings of the index (ESMM tiles, ESTMM chunks, ESS tiles) in
-  // one launch; the backward reuses them from the stash
-  const TileSpec specs[3] = {
-      {w.rows_a, 0, w.tiles_a, w.tiles_a_off, w.n_tiles_a},
-      {kEstmmChunk, 1, w.ktiles, w.ktiles_off, w.n_ktiles},
-      {kEssRows, 0, w.etiles, w.etiles_off, w.n_etiles}};
-  HXM_RETURN_IF(launch_tiles3<int32_t>(w.idx, E, specs, 3, st));
   if (N == 0) return HXM_OK;
   const RowMap slot = map_slot(w.v, N);
-  // (0) expert-sorted copy of x: every later GEMM reads dense tiles
-  // algorithmic bytes: every routed slot's row read once and written once
-  HXM_RETURN_IF(launch_gather_rows(dt, x, slot, d->d_in, w.idx, static_cast<int>(E), w.bound,
-                                   w.xs, st,
-                                   2.0 * static_cast<double>(slots) * d->d_in *
-                                       static_cast<double>(esize(d->dtype))));
   // (1) y1 = x W1 + b1 ; y2 = F(y1)          (moe_layer.cpp:56-57)
   EsmmArgs a1{};
   a1.a = w.xs;
@@ -265,7 +265,6 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
   const hxm_dtype dt = static_cast<hxm_dtype>(d->dtype);
   const int64_t N = d->n_tokens, E = d->n_experts;
   const int64_t Di = d->d_in, H = d->hidden, Do = d->d_out;
-  if (N > 0) HXM_TRY_CUDA(cudaMemsetAsync(gx, 0, sizeof(float) * N * Di, st));
   // tile tables were built by hxm_moe_forward (they live in the stash)
   const RowMap slot = map_slot(w.v, N > 0 ? N : 1);
   // (4) gb2 = sum_i ESS(g_y, R_i)             (moe_layer.cpp:103)
@@ -285,7 +284,25 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
   const double esz = static_cast<double>(esize(d->dtype));
   es.label = "ess_gb2";
   es.work = kn * Do * esz + static_cast<double>(E) * Do * 4.0;
-  HXM_RETURN_IF(launch_ess(dt, es, st));
+  {
+    // one cooperative launch: gx = 0, split experts' gW slices = 0, and the
+    // gb2 ESS fused with the expert-sorted copy of g_y
+    BwdPrologue bp{};
+    bp.label = "bwd_prologue";
+    bp.es = es;
+    bp.gx = gx;
+    bp.gx_elems = N * Di;
+    bp.ktiles = w.ktiles;
+    bp.n_ktiles = w.n_ktiles;
+    bp.gw2 = gw2;
+    bp.gw2_slice = H * Do;
+    bp.gw1 = gw1;
+    bp.gw1_slice = Di * H;
+    // algorithmic bytes: g_y read once per routed slot, its sorted copy
+    // written, gb2 written, gx zeroed (split-expert zeroing is data-dependent)
+    bp.work = 2.0 * kn * Do * esz + static_cast<double>(E) * Do * 4.0 + 4.0 * N * Di;
+    HXM_RETURN_IF(launch_bwd_prologue(dt, bp, st));
+  }
   es.copy_out = nullptr;
   // (5) gW2 = sum_i ESTMM(y2_i, g_y, R_i)     (moe_layer.cpp:104)
   EstmmArgs t2{};
@@ -302,6 +319,7 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
   t2.max_tiles = w.max_ktiles;
   t2.n_experts = static_cast<int>(E);
   t2.out = gw2;
+  t2.skip_zero_split = 1;  // done by the backward prologue
   t2.label = "estmm_gw2";
   t2.work = 2.0 * kn * H * Do;
   HXM_RETURN_IF(launch_estmm(dt, t2, st));
@@ -326,15 +344,25 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
   b6.omap = slot;
   b6.out1 = w.g1s;
   b6.y1s = w.y1s;
-  HXM_RETURN_IF(launch_esmm(dt, b6, st));
   // (8) gb1 = sum_i ESS(g_y1_i, R_i)          (moe_layer.cpp:116)
-  es.x = w.g1s;
-  es.map = map_dense();
-  es.d = H;
-  es.out = gb1;
-  es.label = "ess_gb1";
-  es.work = kn * H * esz + static_cast<double>(E) * H * 4.0;
-  HXM_RETURN_IF(launch_ess(dt, es, st));
+  // tcgen05 path: fused into the g_y1 epilogue (column sums of the stored
+  // bf16 tile per (tile, CTA)), then a deterministic per-expert combine
+  b6.colsum = w.colsum;
+  HXM_RETURN_IF(launch_esmm(dt, b6, st));
+  if (w.colsum) {
+    const int parts = w.rows_a / kUmmaRows;
+    HXM_RETURN_IF(launch_colsum_combine(
+        w.colsum, w.tiles_a_off, static_cast<int>(E), parts, H, gb1, st, "gb1_combine",
+        (static_cast<double>(max_tiles(w.bound, E, w.rows_a)) * parts + E) * H * 4.0));
+  } else {
+    es.x = w.g1s;
+    es.map = map_dense();
+    es.d = H;
+    es.out = gb1;
+    es.label = "ess_gb1";
+    es.work = kn * H * esz + static_cast<double>(E) * H * 4.0;
+    HXM_RETURN_IF(launch_ess(dt, es, st));
+  }
   // (9) gW1 = sum_i ESTMM(x, g_y1_i, R_i)     (moe_layer.cpp:117)
   EstmmArgs t1 = t2;
   t1.x1 = w.xs;

@@ -14,6 +14,7 @@
 //                       token order exactly as the reference's cursor loop.
 // Traffic is read 4 B/token + write 8 B/slot: it is launch/latency bound at
 // every BASELINE.json size.
+#include <cooperative_groups.h>
 #include <cub/block/block_scan.cuh>
 
 #include "common.cuh"
@@ -193,17 +194,17 @@ hxm_status build_impl(const int32_t* a, int64_t n, int64_t E, int64_t blk,
 // tiles of at most `rows` positions per expert segment; min_one: experts
 // with an empty segment still get one (empty) tile -- used by ESTMM so that
 // their zero gradient is written (es_ops.cpp:202 zero-initialised output).
-template <class IdxT>
+template <class IdxT, int NT = 1024>
 __device__ void tile_pass(const IdxT* __restrict__ idx, int E, int rows, int min_one,
                           SegTile* __restrict__ tiles, int32_t* __restrict__ tile_off,
                           int32_t* __restrict__ n_tiles) {
-  using Scan = cub::BlockScan<int32_t, 1024>;
+  using Scan = cub::BlockScan<int32_t, NT>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int32_t carry;
   __syncthreads();
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
-  for (int e0 = 0; e0 < E; e0 += 1024) {
+  for (int e0 = 0; e0 < E; e0 += NT) {
     const int e = e0 + threadIdx.x;
     int32_t nt = 0;
     int64_t b = 0, len = 0;
@@ -247,6 +248,198 @@ __global__ void build_tiles(const IdxT* __restrict__ idx, int E, TileSpec a, Til
   tile_pass<IdxT>(idx, E, a.rows, a.min_one, a.tiles, a.tile_off, a.n_tiles);
   if (count > 1) tile_pass<IdxT>(idx, E, b.rows, b.min_one, b.tiles, b.tile_off, b.n_tiles);
   if (count > 2) tile_pass<IdxT>(idx, E, c.rows, c.min_one, c.tiles, c.tile_off, c.n_tiles);
+}
+
+// ------------------------------------------------- fused layer prologue --
+// The forward's whole index build in ONE cooperative launch (three grid
+// barriers instead of seven dependent launches): validation + per-chunk
+// counts (+ zeroing y) | per-expert chunk scans | segment offsets, -1 pads,
+// in-order placement and the three tile tables | expert-sorted copy of x.
+// Same placement rule as count_chunks / scan_experts / scatter above, so v
+// and idx are bit-identical to the reference's build_reindex order.
+__device__ __forceinline__ void copy_row(const char* src, char* dst, int64_t bytes, int lane,
+                                         int unit) {
+  if (unit == 16) {
+    for (int64_t o = lane * 16; o < bytes; o += 512)
+      *reinterpret_cast<uint4*>(dst + o) = __ldg(reinterpret_cast<const uint4*>(src + o));
+  } else if (unit == 4) {
+    for (int64_t o = lane * 4; o < bytes; o += 128)
+      *reinterpret_cast<uint32_t*>(dst + o) = __ldg(reinterpret_cast<const uint32_t*>(src + o));
+  } else {
+    for (int64_t o = lane * 2; o < bytes; o += 64)
+      *reinterpret_cast<uint16_t*>(dst + o) = __ldg(reinterpret_cast<const uint16_t*>(src + o));
+  }
+}
+__device__ __forceinline__ void zero_row(char* dst, int64_t bytes, int lane, int unit) {
+  if (unit == 16) {
+    for (int64_t o = lane * 16; o < bytes; o += 512)
+      *reinterpret_cast<uint4*>(dst + o) = make_uint4(0u, 0u, 0u, 0u);
+  } else if (unit == 4) {
+    for (int64_t o = lane * 4; o < bytes; o += 128) *reinterpret_cast<uint32_t*>(dst + o) = 0u;
+  } else {
+    for (int64_t o = lane * 2; o < bytes; o += 64) *reinterpret_cast<uint16_t*>(dst + o) = 0;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) fwd_prologue(FwdPrologue a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ unsigned char smem_raw[];
+  const int E = a.E;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int gwarp = blockIdx.x * kWarps + warp, nwarps = gridDim.x * kWarps;
+  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+  const int64_t gthreads = static_cast<int64_t>(gridDim.x) * kThreads;
+  // ---- 1: validation, per-chunk histograms, y = 0 ------------------------
+  {
+    int32_t* h = reinterpret_cast<int32_t*>(smem_raw) + warp * E;
+    for (int c = gwarp; c < a.nchunks; c += nwarps) {
+      for (int e = lane; e < E; e += 32) h[e] = 0;
+      __syncwarp();
+      const int64_t t0 = static_cast<int64_t>(c) * a.chunk;
+      const int64_t t1 = min(a.n_slots, t0 + a.chunk);
+      for (int64_t t = t0 + lane; t < t1; t += 32) {
+        const int e = a.a[t];
+        if (e < 0 || e >= E) {
+          if (a.status) atomicExch(a.status, HXM_ERR_INVALID_ARG);
+          continue;
+        }
+        atomicAdd(&h[e], 1);
+      }
+      __syncwarp();
+      for (int e = lane; e < E; e += 32) a.cnt[static_cast<int64_t>(c) * E + e] = h[e];
+      __syncwarp();
+    }
+    // per-token distinctness of the k choices (routing.cpp:30-39)
+    if (a.status && a.k > 1) {
+      for (int64_t t = gtid; t < a.n_tok; t += gthreads)
+        for (int i = 0; i < a.k; ++i) {
+          const int ei = a.a[i * a.n_tok + t];
+          for (int j = i + 1; j < a.k; ++j)
+            if (a.a[j * a.n_tok + t] == ei) atomicExch(a.status, HXM_ERR_INVALID_ARG);
+        }
+    }
+    float4* y4 = reinterpret_cast<float4*>(a.y);
+    const int64_t n4 = a.y_elems / 4;
+    for (int64_t i = gtid; i < n4; i += gthreads) y4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t i = n4 * 4 + gtid; i < a.y_elems; i += gthreads) a.y[i] = 0.f;
+  }
+  grid.sync();
+  // ---- 2: per expert, exclusive scan of its chunk counts -----------------
+  {
+    using Scan = cub::BlockScan<int32_t, kThreads>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ int32_t carry;
+    for (int e = blockIdx.x; e < E; e += gridDim.x) {
+      __syncthreads();
+      if (threadIdx.x == 0) carry = 0;
+      __syncthreads();
+      for (int c0 = 0; c0 < a.nchunks; c0 += kThreads) {
+        const int c = c0 + threadIdx.x;
+        const int32_t val = c < a.nchunks ? a.cnt[static_cast<int64_t>(c) * E + e] : 0;
+        int32_t excl, agg;
+        Scan(tmp).ExclusiveSum(val, excl, agg);
+        if (c < a.nchunks) a.base[static_cast<int64_t>(c) * E + e] = carry + excl;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += agg;
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) a.total[e] = carry;
+    }
+  }
+  grid.sync();
+  // ---- 3: offsets, -1 pads, stable placement, tile tables ----------------
+  int32_t* sidx = reinterpret_cast<int32_t*>(smem_raw);  // E+1
+  {
+    int32_t* cursor = sidx + align_up(E + 1, 4);  // [kWarps][E]
+    block_idx<int32_t>(a.total, E, a.blk, sidx);
+    if (blockIdx.x == 0)
+      for (int e = threadIdx.x; e <= E; e += kThreads) a.idx[e] = sidx[e];
+    for (int e = gwarp; e < E; e += nwarps) {
+      const int64_t s0 = static_cast<int64_t>(sidx[e]) + a.total[e];
+      for (int64_t p = s0 + lane; p < sidx[e + 1]; p += 32) a.v[p] = -1;
+    }
+    int32_t* cur = cursor + warp * E;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int c = gwarp; c < a.nchunks; c += nwarps) {
+      for (int e = lane; e < E; e += 32) cur[e] = sidx[e] + a.base[static_cast<int64_t>(c) * E + e];
+      __syncwarp();
+      const int64_t t0 = static_cast<int64_t>(c) * a.chunk;
+      const int64_t t1 = min(a.n_slots, t0 + a.chunk);
+      for (int64_t tb = t0; tb < t1; tb += 32) {
+        const int64_t t = tb + lane;
+        int e = t < t1 ? a.a[t] : -1;
+        if (e >= E) e = -1;  // out of range: reported in phase 1, skipped
+        const unsigned peers = __match_any_sync(0xffffffffu, e);
+        if (e >= 0) a.v[cur[e] + __popc(peers & lt)] = static_cast<int32_t>(t);
+        __syncwarp();
+        if (e >= 0 && (__ffs(peers) - 1) == lane) cur[e] += __popc(peers);
+        __syncwarp();
+      }
+    }
+    if (blockIdx.x == gridDim.x - 1) {
+      tile_pass<int32_t, kThreads>(sidx, E, a.s0.rows, a.s0.min_one, a.s0.tiles, a.s0.tile_off,
+                                   a.s0.n_tiles);
+      tile_pass<int32_t, kThreads>(sidx, E, a.s1.rows, a.s1.min_one, a.s1.tiles, a.s1.tile_off,
+                                   a.s1.n_tiles);
+      tile_pass<int32_t, kThreads>(sidx, E, a.s2.rows, a.s2.min_one, a.s2.tiles, a.s2.tile_off,
+                                   a.s2.n_tiles);
+    }
+  }
+  if (!a.x) return;
+  grid.sync();
+  // ---- 4: expert-sorted copy of x (pads -> zero rows) --------------------
+  // a warp moves 4 rows at a time: the 4 index loads, then every 16-byte
+  // unit of the 4 rows loaded into registers (8 per lane in flight) before
+  // any store, so a warp keeps up to 4 KB of reads outstanding
+  {
+    const int64_t np = sidx[E];
+    const char* X = static_cast<const char*>(a.x);
+    char* XS = static_cast<char*>(a.xs);
+    const int64_t rb = a.row_bytes;
+    if (a.unit == 16) {
+      const int upr = static_cast<int>(rb / 16);  // 16-byte units per row
+      for (int64_t p0 = static_cast<int64_t>(gwarp) * 4; p0 < np;
+           p0 += static_cast<int64_t>(nwarps) * 4) {
+        const int nr = np - p0 < 4 ? static_cast<int>(np - p0) : 4;
+        int src[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int sv = u < nr ? a.v[p0 + u] : -1;
+          src[u] = sv < 0 ? -1 : static_cast<int>(sv % a.n_tok);
+        }
+        const int total_u = nr * upr;
+        for (int j0 = 0; j0 < total_u; j0 += 32 * 8) {
+          uint4 buf[8];
+#pragma unroll
+          for (int m = 0; m < 8; ++m) {
+            const int j = j0 + m * 32 + lane;
+            buf[m] = make_uint4(0u, 0u, 0u, 0u);
+            if (j < total_u) {
+              const int u = j / upr, o = j - u * upr;
+              const int r = u == 0 ? src[0] : u == 1 ? src[1] : u == 2 ? src[2] : src[3];
+              if (r >= 0) buf[m] = __ldg(reinterpret_cast<const uint4*>(X + r * rb) + o);
+            }
+          }
+#pragma unroll
+          for (int m = 0; m < 8; ++m) {
+            const int j = j0 + m * 32 + lane;
+            if (j < total_u) {
+              const int u = j / upr, o = j - u * upr;
+              reinterpret_cast<uint4*>(XS + (p0 + u) * rb)[o] = buf[m];
+            }
+          }
+        }
+      }
+    } else {
+      for (int64_t p = gwarp; p < np; p += nwarps) {
+        const int sv = a.v[p];
+        char* dst = XS + p * rb;
+        if (sv < 0) zero_row(dst, rb, lane, a.unit);
+        else copy_row(X + (sv % a.n_tok) * rb, dst, rb, lane, a.unit);
+      }
+    }
+  }
 }
 
 }  // namespace
@@ -293,6 +486,36 @@ template hxm_status launch_tiles<int32_t>(const int32_t*, int64_t, int, bool, Se
                                           int32_t*, int32_t*, cudaStream_t);
 template hxm_status launch_tiles<int64_t>(const int64_t*, int64_t, int, bool, SegTile*,
                                           int32_t*, int32_t*, cudaStream_t);
+
+hxm_status launch_fwd_prologue(FwdPrologue a, cudaStream_t st) {
+  a.chunk = pick_chunk(a.n_slots);
+  a.nchunks = static_cast<int>(ceil_div(a.n_slots, a.chunk));
+  Arena ar(a.ws, a.ws_bytes);
+  a.cnt = ar.take<int32_t>(static_cast<size_t>(a.nchunks) * a.E + 1);
+  a.base = ar.take<int32_t>(static_cast<size_t>(a.nchunks) * a.E + 1);
+  a.total = ar.take<int32_t>(a.E + 1);
+  if (ar.overflow) return invalid_arg("layer prologue: workspace too small");
+  const size_t smem = std::max(static_cast<size_t>(kWarps) * a.E * sizeof(int32_t),
+                               (align_up(a.E + 1, 4) + static_cast<size_t>(kWarps) * a.E) *
+                                   sizeof(int32_t));
+  static int occ_cache = 0;
+  static size_t occ_smem = 0;
+  if (smem > 48 * 1024 || occ_smem != smem) {
+    if (smem > 48 * 1024)
+      HXM_TRY_CUDA(cudaFuncSetAttribute(fwd_prologue, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+    HXM_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cache, fwd_prologue, kThreads,
+                                                               smem));
+    occ_smem = smem;
+  }
+  if (occ_cache < 1) return invalid_arg("layer prologue: cannot be resident");
+  const int grid = sm_count() * std::min(occ_cache, 2);
+  void* args[] = {&a};
+  HXM_TRY_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fwd_prologue), dim3(grid),
+                                           dim3(kThreads), args, smem, st));
+  HXM_CHECK_LAUNCH();
+  return HXM_OK;
+}
 
 int64_t max_tiles(int64_t n_padded_bound, int64_t E, int rows) {
   return ceil_div(n_padded_bound, rows) + E + 1;

@@ -34,4 +34,32 @@ hxm_status launch_tiles3(const IdxT* idx, int64_t E, const TileSpec* specs, int 
 
 int64_t max_tiles(int64_t n_padded_bound, int64_t E, int rows);
 
+// The layer forward's prologue in one cooperative launch: k-choice slot index
+// (v, idx; bit-exact with build_reindex_slots), routing validation into
+// `status`, the three tile tables, y = 0 and the expert-sorted copy of x.
+struct FwdPrologue {
+  const int32_t* a;  // k x N assignments = n_slots slots
+  int64_t n_slots, n_tok;
+  int k, E;
+  int64_t blk;
+  int32_t* v;
+  int32_t* idx;
+  TileSpec s0, s1, s2;
+  const void* x;  // token-order rows (row_bytes each), or null: no copy
+  void* xs;
+  int64_t row_bytes;
+  int unit;  // copy granule: 16, 4 or 2 bytes
+  float* y;
+  int64_t y_elems;
+  int32_t* status;
+  void* ws;  // reindex scratch (reindex_ws_bytes)
+  size_t ws_bytes;
+  // filled by the launcher
+  int chunk, nchunks;
+  int32_t* cnt;
+  int32_t* base;
+  int32_t* total;
+};
+hxm_status launch_fwd_prologue(FwdPrologue a, cudaStream_t st);
+
 }  // namespace hxm

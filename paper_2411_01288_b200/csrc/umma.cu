@@ -144,9 +144,6 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
-__device__ __forceinline__ void bulk_wait_read0() {
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-}
 __device__ __forceinline__ void bulk_wait0() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
@@ -315,9 +312,10 @@ struct Cfg {
   static constexpr int kBBytes = (BN / CG) * BK * 2;
   static constexpr int kStage = kABytes + kBBytes;
   // 227 KB opt-in smem = stages + epilogue staging + 1 KB alignment slack +
-  // barriers.  Staging: 4 KB per epilogue warp (MODE 0 / 3; MODE 1 uses it as
-  // two 16 KB half-group boxes), MODE 2 adds two 8 KB F'(y1) boxes per half.
-  static constexpr int kStaging = MODE == 2 ? 49152 : kEpiWarps * 4096;
+  // barriers.  Staging: 4 KB per epilogue warp (MODE 0 / 3); per column half,
+  // MODE 1 double-buffers its two 8 KB output boxes (32 KB), MODE 2
+  // double-buffers its output box and keeps a 3-deep F'(y1) ring (40 KB).
+  static constexpr int kStaging = MODE == 2 ? 81920 : MODE == 1 ? 65536 : kEpiWarps * 4096;
   static constexpr int kBudget = 232448 - 1024 - 256 - kStaging;
   static constexpr int kStages = kBudget / kStage > 8 ? 8 : kBudget / kStage;
   static constexpr int kSmem = kStages * kStage + kStaging + 1024 /*align*/ + 256 /*barriers*/;
@@ -347,8 +345,8 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + 2;
-  uint64_t* dbar = tempty + 2;  // MODE 2: F'(y1) box loads, [half][buffer]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dbar + 4);
+  uint64_t* dbar = tempty + 2;  // MODE 2: F'(y1) box loads, [half][ring slot]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dbar + 6);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
@@ -360,7 +358,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], kEpiWarps * CG);
     }
-    for (int b = 0; b < 4; ++b) mbar_init(&dbar[b], 1);
+    for (int b = 0; b < 6; ++b) mbar_init(&dbar[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -582,33 +580,49 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
     };
     int acc = 0;
     uint32_t aph = 0;
-    int dchunk = 0;  // MODE 2: running chunk count (F'(y1) buffer / phase)
+    int dchunk = 0;  // MODE 1/2: running chunk count of this half-group (buffers / phases)
+    constexpr int kYRing = 3;  // MODE 2: F'(y1) boxes in flight per half-group
+    constexpr bool bwd = MODE == 2;
+    constexpr bool dense_out = MODE == 1 || MODE == 2;
+    constexpr int kNch = HB / 32;  // 32-column chunks per warp per tile
+    const bool elect = ((warp - 2) & 3) == 0 && lane == 0;
+    // this half-group's staging: MODE 1 = 2 x (out1, out2) boxes, MODE 2 =
+    // 2 x out1 box + kYRing F'(y1) boxes (8 KB each: 128 rows x 32 bf16)
+    uint8_t* hstage = staging + half * (C::kStaging / 2);
+    // ESMM: the next work item's tile and this lane's output row are loaded
+    // one item ahead, so an epilogue that finds its accumulator already full
+    // does not wait on the tile table / index latency.
+    auto tile_at = [&](int wi) { return wi < total ? p.tiles[wi / per_item] : SegTile{0, 0, 0, 0}; };
+    auto orow_of = [&](const SegTile& tt) {
+      const int qq = tt.begin + static_cast<int>(rank) * BM + lg * 32 + lane;
+      return qq < tt.end ? p.omap(qq) : -1;
+    };
+    SegTile t_cur = ESTMM ? SegTile{0, 0, 0, 0} : tile_at(cluster);
+    int orow_cur = ESTMM ? -1 : orow_of(t_cur);
     for (int w = cluster; w < total; w += n_clusters) {
-      const SegTile t = p.tiles[w / per_item];
+      const SegTile t = ESTMM ? p.tiles[w / per_item] : t_cur;
       const int rem = w % per_item;
       if (!ESTMM) {
+        const SegTile t_nx = tile_at(w + n_clusters);  // prefetch (consumed next item)
+        int orow_nx = -1;
         const int n0 = rem * BN + half * HB;
-        // first position of this warp's rows (CG = 2: this CTA's half of 256)
-        const int q0 = t.begin + static_cast<int>(rank) * BM + lg * 32;
-        const int q = q0 + lane;
-        const bool valid = q < t.end;
-        const int orow = valid ? p.omap(q) : -1;
+        const int orow = orow_cur;
         const int N = p.N;
-        constexpr bool bwd = MODE == 2;
-        constexpr bool dense_out = MODE == 1 || MODE == 2;
         // dense bf16 outputs (MODE 1/2): the 4 warps of a column half stage a
-        // 128-row x 32-column box per chunk and one elected thread TMA-stores
-        // it (and, MODE 2, TMA-loads the matching F'(y1) box, double-buffered).
-        // The layer's segments end on 64-row boundaries, so every 32-row warp
-        // slice is entirely valid or entirely past the segment end.
+        // 128-row x 32-column box per chunk (double-buffered) and one elected
+        // thread TMA-stores it; MODE 2 TMA-loads the matching F'(y1) boxes two
+        // chunks ahead.  The layer's segments end on 64-row boundaries, so
+        // every 32-row warp slice is entirely valid or entirely past the end.
         const int qbase = t.begin + static_cast<int>(rank) * BM;  // row 0 of the box
         const int rows_here = t.end - qbase;
-        const bool elect = ((warp - 2) & 3) == 0 && lane == 0;
-        uint8_t* hstage = staging + half * (C::kStaging / 2);  // this half-group's staging
-        if (bwd && elect) {  // F'(y1) box of chunk 0, overlapping the MMA
-          const int b = dchunk & 1;
-          mbar_arrive_tx(&dbar[half * 2 + b], 8192);
-          tma_2d(hstage + 8192 + b * 8192, &p.tmY, &dbar[half * 2 + b], n0, qbase);
+        auto ybox = [&](int gchunk) { return hstage + 16384 + (gchunk % kYRing) * 8192; };
+        auto ybar = [&](int gchunk) { return &dbar[half * kYRing + gchunk % kYRing]; };
+        if (bwd && elect) {  // F'(y1) boxes of chunks 0 and 1, overlapping the MMA
+#pragma unroll
+          for (int j = 0; j < (kNch < 2 ? kNch : 2); ++j) {
+            mbar_arrive_tx(ybar(dchunk + j), 8192);
+            tma_2d(ybox(dchunk + j), &p.tmY, ybar(dchunk + j), n0 + 32 * j, qbase);
+          }
         }
         // bias of this warp's HB columns: lane l holds columns 4l..4l+3,
         // broadcast by shuffles (loaded before the wait)
@@ -635,6 +649,8 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
           uint32_t (&r)[32] = rbuf[(c0 / 32) & 1];
           // next chunk's TMEM load overlaps this chunk's math
           if (c0 + 32 < HB) tmem_ld32_async(taddr + c0 + 32, rbuf[((c0 / 32) + 1) & 1]);
+          // the next item's output row (its tile was loaded at this item's start)
+          if (c0 == 0 && w + n_clusters < total) orow_nx = orow_of(t_nx);
           const int n = n0 + c0;
           float v[32];
 #pragma unroll
@@ -653,20 +669,19 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
             const bool pad = orow < 0;  // padding slot -> zero row
             const int hrow = lg * 32 + lane;  // this thread's row in the 128-row box
             const int swz = (hrow >> 1) & 3;  // TMA 64B swizzle: chunk ^= (row >> 1) & 3
-            // (1) the previous chunk's box has been read by its TMA store,
-            //     and every thread is past the previous chunk's F'(y1) reads
-            if (elect) bulk_wait_read0();
+            uint8_t* obox = hstage + (dchunk & 1) * (bwd ? 8192 : 16384);
+            // (1) the store of two chunks ago (same box) has read its smem, and
+            //     every thread is past the previous chunk's F'(y1) reads
+            if (elect) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
             named_bar_sync(1 + half, 128);
-            if (bwd && elect && c0 + 32 < HB) {  // prefetch the next F'(y1) box
-              const int b = (dchunk + 1) & 1;
-              mbar_arrive_tx(&dbar[half * 2 + b], 8192);
-              tma_2d(hstage + 8192 + b * 8192, &p.tmY, &dbar[half * 2 + b], n + 32, qbase);
+            if (bwd && elect && c0 + 64 < HB) {  // F'(y1) box two chunks ahead
+              mbar_arrive_tx(ybar(dchunk + 2), 8192);
+              tma_2d(ybox(dchunk + 2), &p.tmY, ybar(dchunk + 2), n + 64, qbase);
             }
             uint4 dv[4];
             if (bwd) {  // this row's F'(y1) chunk from the staged box
-              const int b = dchunk & 1;
-              mbar_wait(&dbar[half * 2 + b], (dchunk >> 1) & 1);
-              const uint8_t* src = hstage + 8192 + b * 8192 + hrow * 64;
+              mbar_wait(ybar(dchunk), (dchunk / kYRing) & 1);
+              const uint8_t* src = ybox(dchunk) + hrow * 64;
 #pragma unroll
               for (int j = 0; j < 4; ++j)
                 dv[j] = *reinterpret_cast<const uint4*>(src + ((j ^ swz) * 16));
@@ -695,27 +710,47 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
                   a1[i] = pad ? 0u : pack_bf16(g0, g1);
                 }
               }
-              *reinterpret_cast<uint4*>(hstage + hrow * 64 + ((j ^ swz) * 16)) =
+              *reinterpret_cast<uint4*>(obox + hrow * 64 + ((j ^ swz) * 16)) =
                   make_uint4(a1[0], a1[1], a1[2], a1[3]);
               if (!bwd)
-                *reinterpret_cast<uint4*>(hstage + 8192 + hrow * 64 + ((j ^ swz) * 16)) =
+                *reinterpret_cast<uint4*>(obox + 8192 + hrow * 64 + ((j ^ swz) * 16)) =
                     make_uint4(a2[0], a2[1], a2[2], a2[3]);
             }
             // (2) box complete -> one TMA store per output (or per valid
-            //     32-row slice at a segment end)
+            //     32-row slice at a segment end), one bulk group per chunk
             fence_async_smem();
             named_bar_sync(1 + half, 128);
-            if (elect && rows_here > 0) {
+            if (elect) {
               if (rows_here >= BM) {
-                tma_store_2d(&p.tmO1, hstage, n, qbase);
-                if (!bwd) tma_store_2d(&p.tmO2, hstage + 8192, n, qbase);
+                tma_store_2d(&p.tmO1, obox, n, qbase);
+                if (!bwd) tma_store_2d(&p.tmO2, obox + 8192, n, qbase);
               } else {
                 for (int sl = 0; sl * 32 < rows_here; ++sl) {
-                  tma_store_2d(&p.tmO1s, hstage + sl * 2048, n, qbase + sl * 32);
-                  if (!bwd) tma_store_2d(&p.tmO2s, hstage + 8192 + sl * 2048, n, qbase + sl * 32);
+                  tma_store_2d(&p.tmO1s, obox + sl * 2048, n, qbase + sl * 32);
+                  if (!bwd) tma_store_2d(&p.tmO2s, obox + 8192 + sl * 2048, n, qbase + sl * 32);
                 }
               }
               bulk_commit();
+            }
+            if (bwd && p.colsum) {
+              // fused gb1 (ESS of g_y1, es_ops.cpp:86-102): column sums of the
+              // staged 128 x 32 box (the stored bf16 values; pads are zero
+              // rows).  Warp wq of the half sums columns 8wq..8wq+7, lane group
+              // g rows 32g..32g+31 (row order rotated by 2g: conflict-free),
+              // then one deterministic partial per (tile, CTA) is written.
+              const int wq = (warp - 2) & 3, g = lane >> 3, c = wq * 8 + (lane & 7);
+              float s = 0.f;
+#pragma unroll 8
+              for (int i = 0; i < 32; ++i) {
+                const int r = g * 32 + ((i + 2 * g) & 31);
+                const __nv_bfloat16 b = *reinterpret_cast<const __nv_bfloat16*>(
+                    obox + r * 64 + ((wq ^ ((r >> 1) & 3)) * 16) + (lane & 7) * 2);
+                s += __bfloat162float(b);
+              }
+              s += __shfl_xor_sync(0xffffffffu, s, 8);
+              s += __shfl_xor_sync(0xffffffffu, s, 16);
+              if (lane < 8)
+                p.colsum[(static_cast<int64_t>(w / per_item) * CG + rank) * N + n + c] = s;
             }
             ++dchunk;
           } else {
@@ -753,6 +788,8 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
             }
           }
         }
+        t_cur = t_nx;
+        orow_cur = orow_nx;
       } else {
         const int mt = rem / p.n_nt, nt = rem % p.n_nt;
         // first output row of this warp (CG = 2: this CTA's half of 256)
@@ -988,6 +1025,7 @@ hxm_status umma_esmm(const EsmmArgs& a, cudaStream_t st) {
   prm.out1 = a.out1;
   prm.out2 = a.out2;
   prm.y1s = a.y1s;
+  prm.colsum = a.epi == EPI_BWD_ACT ? a.colsum : nullptr;
   if (a.epi == EPI_FWD_ACT || a.epi == EPI_BWD_ACT) {
     // dense bf16 stash outputs (same row space as the dense A operand):
     // 32 x 32 boxes stored by TMA from the epilogue's 64B-swizzled staging
