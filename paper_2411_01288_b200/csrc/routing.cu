@@ -15,6 +15,7 @@
 // Traffic is read 4 B/token + write 8 B/slot: it is launch/latency bound at
 // every BASELINE.json size.
 #include <cooperative_groups.h>
+#include <cstdlib>
 #include <cub/block/block_scan.cuh>
 
 #include "common.cuh"
@@ -281,8 +282,17 @@ __device__ __forceinline__ void zero_row(char* dst, int64_t bytes, int lane, int
   }
 }
 
+__device__ unsigned long long g_pro_ts[8];
+__device__ __forceinline__ void pro_ts(int i) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_pro_ts[i] = t;
+  }
+}
 __global__ void __launch_bounds__(kThreads) fwd_prologue(FwdPrologue a) {
   namespace cg = cooperative_groups;
+  pro_ts(0);
   cg::grid_group grid = cg::this_grid();
   extern __shared__ unsigned char smem_raw[];
   const int E = a.E;
@@ -290,7 +300,7 @@ __global__ void __launch_bounds__(kThreads) fwd_prologue(FwdPrologue a) {
   const int gwarp = blockIdx.x * kWarps + warp, nwarps = gridDim.x * kWarps;
   const int64_t gtid = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
   const int64_t gthreads = static_cast<int64_t>(gridDim.x) * kThreads;
-  // ---- 1: validation, per-chunk histograms, y = 0 ------------------------
+  // ---- 1: validation, per-chunk histograms --------------------------------
   {
     int32_t* h = reinterpret_cast<int32_t*>(smem_raw) + warp * E;
     for (int c = gwarp; c < a.nchunks; c += nwarps) {
@@ -319,13 +329,11 @@ __global__ void __launch_bounds__(kThreads) fwd_prologue(FwdPrologue a) {
             if (a.a[j * a.n_tok + t] == ei) atomicExch(a.status, HXM_ERR_INVALID_ARG);
         }
     }
-    float4* y4 = reinterpret_cast<float4*>(a.y);
-    const int64_t n4 = a.y_elems / 4;
-    for (int64_t i = gtid; i < n4; i += gthreads) y4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int64_t i = n4 * 4 + gtid; i < a.y_elems; i += gthreads) a.y[i] = 0.f;
   }
+  pro_ts(1);
   grid.sync();
-  // ---- 2: per expert, exclusive scan of its chunk counts -----------------
+  pro_ts(2);
+  // ---- 2: per expert, exclusive scan of its chunk counts; y = 0 ----------
   {
     using Scan = cub::BlockScan<int32_t, kThreads>;
     __shared__ typename Scan::TempStorage tmp;
@@ -346,8 +354,20 @@ __global__ void __launch_bounds__(kThreads) fwd_prologue(FwdPrologue a) {
       }
       if (threadIdx.x == 0) a.total[e] = carry;
     }
+    // y = 0 by the blocks without a scan (all of them when E >= grid)
+    const int zb0 = gridDim.x > static_cast<unsigned>(E) ? E : 0;
+    const int64_t zt = static_cast<int64_t>(blockIdx.x - zb0) * kThreads + threadIdx.x;
+    const int64_t zn = static_cast<int64_t>(gridDim.x - zb0) * kThreads;
+    if (static_cast<int>(blockIdx.x) >= zb0) {
+      float4* y4 = reinterpret_cast<float4*>(a.y);
+      const int64_t n4 = a.y_elems / 4;
+      for (int64_t i = zt; i < n4; i += zn) y4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int64_t i = n4 * 4 + zt; i < a.y_elems; i += zn) a.y[i] = 0.f;
+    }
   }
+  pro_ts(3);
   grid.sync();
+  pro_ts(4);
   // ---- 3: offsets, -1 pads, stable placement, tile tables ----------------
   int32_t* sidx = reinterpret_cast<int32_t*>(smem_raw);  // E+1
   {
@@ -386,8 +406,10 @@ __global__ void __launch_bounds__(kThreads) fwd_prologue(FwdPrologue a) {
                                    a.s2.n_tiles);
     }
   }
+  pro_ts(5);
   if (!a.x) return;
   grid.sync();
+  pro_ts(6);
   // ---- 4: expert-sorted copy of x (pads -> zero rows) --------------------
   // a warp moves 4 rows at a time: the 4 index loads, then every 16-byte
   // unit of the 4 rows loaded into registers (8 per lane in flight) before
@@ -398,35 +420,44 @@ __global__ void __launch_bounds__(kThreads) fwd_prologue(FwdPrologue a) {
     char* XS = static_cast<char*>(a.xs);
     const int64_t rb = a.row_bytes;
     if (a.unit == 16) {
+      // each warp owns a contiguous run of positions: one coalesced load of
+      // its indices, then batches of 8 rows with every load in flight
+      // before the stores (8 rows x 1 KB per pass)
       const int upr = static_cast<int>(rb / 16);  // 16-byte units per row
-      for (int64_t p0 = static_cast<int64_t>(gwarp) * 4; p0 < np;
-           p0 += static_cast<int64_t>(nwarps) * 4) {
-        const int nr = np - p0 < 4 ? static_cast<int>(np - p0) : 4;
-        int src[4];
+      const int ntok = static_cast<int>(a.n_tok);
+      const int64_t per = (ceil_div(np, nwarps) + 7) / 8 * 8;
+      const int64_t pb = static_cast<int64_t>(gwarp) * per;
+      const int64_t pe = min(np, pb + per);
+      for (int64_t q0 = pb; q0 < pe; q0 += 32) {
+        const int sv_l = q0 + lane < pe ? a.v[q0 + lane] : -1;
+        const int tok_l = sv_l < 0 ? -1 : sv_l % ntok;
+        for (int r0 = 0; r0 < 32 && q0 + r0 < pe; r0 += 8) {
+          const char* src[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int sv = u < nr ? a.v[p0 + u] : -1;
-          src[u] = sv < 0 ? -1 : static_cast<int>(sv % a.n_tok);
-        }
-        const int total_u = nr * upr;
-        for (int j0 = 0; j0 < total_u; j0 += 32 * 8) {
-          uint4 buf[8];
-#pragma unroll
-          for (int m = 0; m < 8; ++m) {
-            const int j = j0 + m * 32 + lane;
-            buf[m] = make_uint4(0u, 0u, 0u, 0u);
-            if (j < total_u) {
-              const int u = j / upr, o = j - u * upr;
-              const int r = u == 0 ? src[0] : u == 1 ? src[1] : u == 2 ? src[2] : src[3];
-              if (r >= 0) buf[m] = __ldg(reinterpret_cast<const uint4*>(X + r * rb) + o);
-            }
+          for (int u = 0; u < 8; ++u) {
+            const int tk = __shfl_sync(0xffffffffu, tok_l, r0 + u);
+            src[u] = tk < 0 ? nullptr : X + static_cast<int64_t>(tk) * rb;
           }
+          for (int c0 = 0; c0 < upr; c0 += 64) {
+            uint4 buf[8][2];
 #pragma unroll
-          for (int m = 0; m < 8; ++m) {
-            const int j = j0 + m * 32 + lane;
-            if (j < total_u) {
-              const int u = j / upr, o = j - u * upr;
-              reinterpret_cast<uint4*>(XS + (p0 + u) * rb)[o] = buf[m];
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+              for (int m = 0; m < 2; ++m) {
+                const int o = c0 + m * 32 + lane;
+                buf[u][m] = (src[u] && o < upr)
+                                ? __ldg(reinterpret_cast<const uint4*>(src[u]) + o)
+                                : make_uint4(0u, 0u, 0u, 0u);
+              }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              if (q0 + r0 + u >= pe) break;
+              uint4* dst = reinterpret_cast<uint4*>(XS + (q0 + r0 + u) * rb);
+#pragma unroll
+              for (int m = 0; m < 2; ++m) {
+                const int o = c0 + m * 32 + lane;
+                if (o < upr) dst[o] = buf[u][m];
+              }
             }
           }
         }
@@ -440,6 +471,8 @@ __global__ void __launch_bounds__(kThreads) fwd_prologue(FwdPrologue a) {
       }
     }
   }
+  __syncthreads();
+  pro_ts(7);
 }
 
 }  // namespace
@@ -509,7 +542,9 @@ hxm_status launch_fwd_prologue(FwdPrologue a, cudaStream_t st) {
     occ_smem = smem;
   }
   if (occ_cache < 1) return invalid_arg("layer prologue: cannot be resident");
-  const int grid = sm_count() * std::min(occ_cache, 2);
+  const char* ge = std::getenv("HXM_PRO_BLOCKS");
+  const int per_sm = ge ? std::max(1, std::atoi(ge)) : 2;
+  const int grid = sm_count() * std::min(occ_cache, per_sm);
   void* args[] = {&a};
   HXM_TRY_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fwd_prologue), dim3(grid),
                                            dim3(kThreads), args, smem, st));
@@ -517,6 +552,11 @@ hxm_status launch_fwd_prologue(FwdPrologue a, cudaStream_t st) {
   return HXM_OK;
 }
 
+}  // namespace hxm
+extern "C" void hxm_debug_prologue_ts(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, hxm::g_pro_ts, sizeof(unsigned long long) * 8);
+}
+namespace hxm {
 int64_t max_tiles(int64_t n_padded_bound, int64_t E, int rows) {
   return ceil_div(n_padded_bound, rows) + E + 1;
 }

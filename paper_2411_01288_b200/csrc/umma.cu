@@ -242,10 +242,12 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
 
 // UMMA shared-memory descriptor (sm100): start>>4 [0,14), LBO>>4 [16,30),
 // SBO>>4 [32,46), version=1 [46,48), layout SWIZZLE_128B=2 [61,64).
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// layout 2 = SWIZZLE_128B, 4 = SWIZZLE_64B.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
+                                          uint64_t layout = 2) {
   return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) |
          (static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16) |
-         (static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
+         (static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (layout << 61);
 }
 // Instruction descriptor kind::f16: D=f32, A=B=bf16, majors, N>>3, M>>4.
 __host__ __device__ constexpr uint32_t idesc_bf16(int n, int a_mn, int b_mn, int m = BM) {
@@ -290,6 +292,7 @@ struct UParams {
   RowMap amap;      // gather map of A (ESMM rows / ESTMM X1 rows)
   RowMap bmap;      // ESTMM X2 rows
   int a_gather, b_gather, b_kmajor;
+  int b_sw64;  // CG = 2, MN-major B halves of 32-column multiples: 64B-swizzled boxes
   int K, N, M;  // ESMM: K=d1, N=d2 ; ESTMM: M=d1, N=d2
   int n_nt, n_mt;
   const SegTile* tiles;
@@ -420,6 +423,10 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
               const int nb = n0 + static_cast<int>(rank) * (BN / 2);
               if (p.b_kmajor) {
                 tma_3d_cg2(sb, &p.tmB, fb, kb * BK, nb, t.expert);
+              } else if (p.b_sw64) {
+#pragma unroll
+                for (int j = 0; j < BN / 64; ++j)
+                  tma_3d_cg2(sb + j * 4096, &p.tmB, fb, nb + 32 * j, kb * BK, t.expert);
               } else {
 #pragma unroll
                 for (int j = 0; j < BN / 128; ++j)
@@ -464,8 +471,13 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
               mbar_arrive_tx_cl(fb, C::kStage);
               tma_2d_cg2(sa, &p.tmA, fb, m0, p0);
               tma_2d_cg2(sa + 8192, &p.tmA, fb, m0 + 64, p0);
+              if (p.b_sw64) {
 #pragma unroll
-              for (int j = 0; j < BN / 128; ++j) tma_2d_cg2(sb + j * 8192, &p.tmB, fb, n0 + 64 * j, p0);
+                for (int j = 0; j < BN / 64; ++j) tma_2d_cg2(sb + j * 4096, &p.tmB, fb, n0 + 32 * j, p0);
+              } else {
+#pragma unroll
+                for (int j = 0; j < BN / 128; ++j) tma_2d_cg2(sb + j * 8192, &p.tmB, fb, n0 + 64 * j, p0);
+              }
             }
             __syncwarp();
             if (++s == C::kStages) { s = 0; ph ^= 1; }
@@ -525,10 +537,14 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
       // per UMMA_K (16) step, in 16-byte descriptor units: K-major = 32 B
       // inside the swizzle atom; MN-major = 16 k-rows = 2 x 1024 B
       const bool a_mn = ESTMM, b_mn = ESTMM || !p.b_kmajor;
-      const uint32_t a_step = a_mn ? 128u : 2u, b_step = b_mn ? 128u : 2u;
+      // SW64 MN-major B: 32-column atoms, 4 KB per 64 k-rows, 512 B per 8 rows
+      const bool sw64 = b_mn && p.b_sw64;
+      const uint32_t a_step = a_mn ? 128u : 2u, b_step = b_mn ? (sw64 ? 64u : 128u) : 2u;
       const uint32_t base = smem_u32(smem);
       const uint64_t da0 = a_mn ? sdesc(base, 8192, 1024) : sdesc(base, 16, 1024);
-      const uint64_t db0 = b_mn ? sdesc(base + kABytes, 8192, 1024) : sdesc(base + kABytes, 16, 1024);
+      const uint64_t db0 = !b_mn ? sdesc(base + kABytes, 16, 1024)
+                           : sw64 ? sdesc(base + kABytes, 4096, 512, 4)
+                                  : sdesc(base + kABytes, 8192, 1024);
       constexpr uint32_t kStageUnits = C::kStage >> 4;
       int s = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
@@ -896,15 +912,17 @@ int pick_bn(int64_t n) {
     if (n % bn == 0) return bn;
   return 0;
 }
-// CTA-pair tiles: an MN-major B half must be whole 64-column swizzle chunks
+// CTA-pair tiles: an MN-major B half must be whole swizzle atoms -- 64
+// columns (128B swizzle), or 32 columns with 64B-swizzled boxes (BN = 192)
 int pick_bn2(int64_t n, bool b_mn) {
   if (b_mn) {
-    for (int bn : {256, 128})
+    for (int bn : {256, 192, 128})
       if (n % bn == 0) return bn;
     return 0;
   }
   return pick_bn(n);
 }
+bool bn2_sw64(int bn, bool b_mn) { return b_mn && (bn / 2) % 64 != 0; }
 
 template <int BN, int MODE, int CG, int ACT = -1>
 hxm_status launch_bn(const UParams& prm, int max_work, cudaStream_t st) {
@@ -995,9 +1013,12 @@ hxm_status umma_esmm(const EsmmArgs& a, cudaStream_t st) {
                                 static_cast<uint64_t>(E)};
       const uint64_t strides[2] = {static_cast<uint64_t>(a.d2) * 2,
                                    static_cast<uint64_t>(a.d1 * a.d2) * 2};
-      const uint32_t box[3] = {64, 64, 1};
-      if (!make_map(&prm.tmB, a.w, 3, dims, strides, box))
+      const bool sw64 = CG == 2 && bn2_sw64(bn, true);
+      const uint32_t box[3] = {sw64 ? 32u : 64u, 64, 1};
+      if (!make_map(&prm.tmB, a.w, 3, dims, strides, box,
+                    sw64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
         return invalid_arg("umma_esmm: cannot encode the W tensor map");
+      prm.b_sw64 = sw64;
     } else {
       const uint64_t dims[3] = {static_cast<uint64_t>(a.d1), static_cast<uint64_t>(a.d2),
                                 static_cast<uint64_t>(E)};
@@ -1071,9 +1092,12 @@ hxm_status umma_estmm(const EstmmArgs& a, cudaStream_t st) {
   {
     const uint64_t dims[2] = {static_cast<uint64_t>(a.d2), static_cast<uint64_t>(a.x2_rows)};
     const uint64_t strides[1] = {static_cast<uint64_t>(a.d2) * 2};
-    const uint32_t box[2] = {64, gb ? 1u : 64u};
-    if (!make_map(&prm.tmB, a.x2, 2, dims, strides, box))
+    const bool sw64 = CG == 2 && bn2_sw64(bn, true);
+    const uint32_t box[2] = {sw64 ? 32u : 64u, gb ? 1u : 64u};
+    if (!make_map(&prm.tmB, a.x2, 2, dims, strides, box,
+                  sw64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
       return invalid_arg("umma_estmm: cannot encode the X2 tensor map");
+    prm.b_sw64 = sw64;
   }
   prm.amap = a.m1;
   prm.bmap = a.m2;
