@@ -88,6 +88,14 @@ __device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, uint64
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+__device__ __forceinline__ void tma_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                       int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
 // 4 rows (r0..r3, -1 = out of bounds -> zero fill) x 64 columns from col.
 __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, uint64_t* bar,
                                             int col, int r0, int r1, int r2, int r3) {
@@ -196,6 +204,14 @@ __device__ __forceinline__ void tma_3d_cg2(void* dst, const CUtensorMap* map, ui
       "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
       "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_4d_cg2(void* dst, const CUtensorMap* map, uint32_t bar, int c0,
+                                           int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
 __device__ __forceinline__ void umma_bf16_cg2(uint32_t tmem_d, uint64_t da, uint64_t db,
@@ -423,14 +439,9 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
               const int nb = n0 + static_cast<int>(rank) * (BN / 2);
               if (p.b_kmajor) {
                 tma_3d_cg2(sb, &p.tmB, fb, kb * BK, nb, t.expert);
-              } else if (p.b_sw64) {
-#pragma unroll
-                for (int j = 0; j < BN / 64; ++j)
-                  tma_3d_cg2(sb + j * 4096, &p.tmB, fb, nb + 32 * j, kb * BK, t.expert);
               } else {
-#pragma unroll
-                for (int j = 0; j < BN / 128; ++j)
-                  tma_3d_cg2(sb + j * 8192, &p.tmB, fb, nb + 64 * j, kb * BK, t.expert);
+                // all of this CTA's swizzle-atom column chunks in one 4D box
+                tma_4d_cg2(sb, &p.tmB, fb, 0, kb * BK, nb / (p.b_sw64 ? 32 : 64), t.expert);
               }
             }
           } else {
@@ -446,9 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
               if (p.b_kmajor) {
                 tma_3d(sb, &p.tmB, &full[s], kb * BK, n0, t.expert);
               } else {
-#pragma unroll
-                for (int j = 0; j < BN / 64; ++j)
-                  tma_3d(sb + j * 8192, &p.tmB, &full[s], n0 + 64 * j, kb * BK, t.expert);
+                tma_4d(sb, &p.tmB, &full[s], 0, kb * BK, n0 / 64, t.expert);
               }
             }
           }
@@ -469,15 +478,9 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
             if (lane == 0) {
               const uint32_t fb = full_lead + 8u * s;
               mbar_arrive_tx_cl(fb, C::kStage);
-              tma_2d_cg2(sa, &p.tmA, fb, m0, p0);
-              tma_2d_cg2(sa + 8192, &p.tmA, fb, m0 + 64, p0);
-              if (p.b_sw64) {
-#pragma unroll
-                for (int j = 0; j < BN / 64; ++j) tma_2d_cg2(sb + j * 4096, &p.tmB, fb, n0 + 32 * j, p0);
-              } else {
-#pragma unroll
-                for (int j = 0; j < BN / 128; ++j) tma_2d_cg2(sb + j * 8192, &p.tmB, fb, n0 + 64 * j, p0);
-              }
+              // both 64-column chunks of A, all chunks of B: one 3D box each
+              tma_3d_cg2(sa, &p.tmA, fb, 0, p0, m0 / 64);
+              tma_3d_cg2(sb, &p.tmB, fb, 0, p0, n0 / (p.b_sw64 ? 32 : 64));
             }
             __syncwarp();
             if (++s == C::kStages) { s = 0; ph ^= 1; }
@@ -497,8 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
             tma_gather4(sa + ch * 8192 + rg * 512, &p.tmA, &full[s], m0 + 64 * ch, r[0], r[1],
                         r[2], r[3]);
           } else if (lane == 0) {
-            tma_2d(sa, &p.tmA, &full[s], m0, p0);
-            tma_2d(sa + 8192, &p.tmA, &full[s], m0 + 64, p0);
+            tma_3d(sa, &p.tmA, &full[s], 0, p0, m0 / 64);
           }
           // B = X2: BN/64 chunks of the 64 k-rows
           if (p.b_gather) {
@@ -514,8 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
                           r[2], r[3]);
             }
           } else if (lane == 0) {
-#pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_2d(sb + j * 8192, &p.tmB, &full[s], n0 + 64 * j, p0);
+            tma_3d(sb, &p.tmB, &full[s], 0, p0, n0 / 64);
           }
           __syncwarp();
           if (++s == C::kStages) { s = 0; ph ^= 1; }
@@ -894,8 +895,8 @@ bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
               CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeFn enc = encoder();
   if (!enc) return false;
-  cuuint64_t gd[3], gs[2];
-  cuuint32_t bx[3], es[3] = {1, 1, 1};
+  cuuint64_t gd[5], gs[4];
+  cuuint32_t bx[5], es[5] = {1, 1, 1, 1, 1};
   for (int i = 0; i < rank; ++i) {
     gd[i] = dims[i];
     bx[i] = box[i];
@@ -1009,13 +1010,17 @@ hxm_status umma_esmm(const EsmmArgs& a, cudaStream_t st) {
   {
     const int64_t E = a.n_experts;
     if (!a.w_trans) {
-      const uint64_t dims[3] = {static_cast<uint64_t>(a.d2), static_cast<uint64_t>(a.d1),
-                                static_cast<uint64_t>(E)};
-      const uint64_t strides[2] = {static_cast<uint64_t>(a.d2) * 2,
-                                   static_cast<uint64_t>(a.d1 * a.d2) * 2};
+      // 4D view (atom column, k row, atom chunk, expert): one box carries
+      // every swizzle-atom column chunk of this CTA's B for a k-block
       const bool sw64 = CG == 2 && bn2_sw64(bn, true);
-      const uint32_t box[3] = {sw64 ? 32u : 64u, 64, 1};
-      if (!make_map(&prm.tmB, a.w, 3, dims, strides, box,
+      const uint64_t bw = sw64 ? 32 : 64;
+      const uint64_t dims[4] = {bw, static_cast<uint64_t>(a.d1), static_cast<uint64_t>(a.d2) / bw,
+                                static_cast<uint64_t>(E)};
+      const uint64_t strides[3] = {static_cast<uint64_t>(a.d2) * 2, bw * 2,
+                                   static_cast<uint64_t>(a.d1 * a.d2) * 2};
+      const uint32_t box[4] = {static_cast<uint32_t>(bw), 64,
+                               static_cast<uint32_t>((bn / CG) / static_cast<int>(bw)), 1};
+      if (!make_map(&prm.tmB, a.w, 4, dims, strides, box,
                     sw64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
         return invalid_arg("umma_esmm: cannot encode the W tensor map");
       prm.b_sw64 = sw64;
@@ -1082,21 +1087,43 @@ hxm_status umma_estmm(const EstmmArgs& a, cudaStream_t st) {
   const int CG = (!ga && !gb && a.d1 % 256 == 0 && pick_bn2(a.d2, true) > 0) ? 2 : 1;
   const int bn = CG == 2 ? pick_bn2(a.d2, true) : pick_bn(a.d2);
   UParams prm{};
+  // dense operands: 3D views (atom column, row, atom chunk) so one box
+  // carries every column chunk of a k-block; gathered ones: 2D row maps
   {
-    const uint64_t dims[2] = {static_cast<uint64_t>(a.d1), static_cast<uint64_t>(a.x1_rows)};
-    const uint64_t strides[1] = {static_cast<uint64_t>(a.d1) * 2};
-    const uint32_t box[2] = {64, ga ? 1u : 64u};
-    if (!make_map(&prm.tmA, a.x1, 2, dims, strides, box))
-      return invalid_arg("umma_estmm: cannot encode the X1 tensor map");
+    bool ok;
+    if (ga) {
+      const uint64_t dims[2] = {static_cast<uint64_t>(a.d1), static_cast<uint64_t>(a.x1_rows)};
+      const uint64_t strides[1] = {static_cast<uint64_t>(a.d1) * 2};
+      const uint32_t box[2] = {64, 1};
+      ok = make_map(&prm.tmA, a.x1, 2, dims, strides, box);
+    } else {
+      const uint64_t dims[3] = {64, static_cast<uint64_t>(a.x1_rows),
+                                static_cast<uint64_t>(a.d1) / 64};
+      const uint64_t strides[2] = {static_cast<uint64_t>(a.d1) * 2, 128};
+      const uint32_t box[3] = {64, 64, BM / 64};
+      ok = make_map(&prm.tmA, a.x1, 3, dims, strides, box);
+    }
+    if (!ok) return invalid_arg("umma_estmm: cannot encode the X1 tensor map");
   }
   {
-    const uint64_t dims[2] = {static_cast<uint64_t>(a.d2), static_cast<uint64_t>(a.x2_rows)};
-    const uint64_t strides[1] = {static_cast<uint64_t>(a.d2) * 2};
     const bool sw64 = CG == 2 && bn2_sw64(bn, true);
-    const uint32_t box[2] = {sw64 ? 32u : 64u, gb ? 1u : 64u};
-    if (!make_map(&prm.tmB, a.x2, 2, dims, strides, box,
-                  sw64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
-      return invalid_arg("umma_estmm: cannot encode the X2 tensor map");
+    bool ok;
+    if (gb) {
+      const uint64_t dims[2] = {static_cast<uint64_t>(a.d2), static_cast<uint64_t>(a.x2_rows)};
+      const uint64_t strides[1] = {static_cast<uint64_t>(a.d2) * 2};
+      const uint32_t box[2] = {64, 1};
+      ok = make_map(&prm.tmB, a.x2, 2, dims, strides, box);
+    } else {
+      const uint64_t bw = sw64 ? 32 : 64;
+      const uint64_t dims[3] = {bw, static_cast<uint64_t>(a.x2_rows),
+                                static_cast<uint64_t>(a.d2) / bw};
+      const uint64_t strides[2] = {static_cast<uint64_t>(a.d2) * 2, bw * 2};
+      const uint32_t box[3] = {static_cast<uint32_t>(bw), 64,
+                               static_cast<uint32_t>((bn / CG) / static_cast<int>(bw))};
+      ok = make_map(&prm.tmB, a.x2, 3, dims, strides, box,
+                    sw64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
+    }
+    if (!ok) return invalid_arg("umma_estmm: cannot encode the X2 tensor map");
     prm.b_sw64 = sw64;
   }
   prm.amap = a.m1;
