@@ -7,6 +7,8 @@
 #include <string>
 #include <vector>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace hxm {
@@ -27,6 +29,14 @@ int sm_count() {
   if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
   if (dev < 64) cached[dev] = n;
   return n;
+}
+
+bool pdl_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("HXM_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 // moekit::Rng (reference core/include/moekit/random.hpp:13-40): the same

@@ -401,6 +401,9 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
   const uint32_t full_lead = CG == 2 ? mapa0(smem_u32(full)) : smem_u32(full);
   const uint32_t tempty_lead = CG == 2 ? mapa0(smem_u32(tempty)) : smem_u32(tempty);
 
+  // PDL: everything above overlapped the previous kernel; from here on the
+  // kernel reads what earlier kernels wrote (tile tables, operands)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int n_items = *p.n_tiles;
   const int per_item = ESTMM ? p.n_mt * p.n_nt : p.n_nt;
   const int total = n_items * per_item;
@@ -938,23 +941,31 @@ hxm_status launch_bn(const UParams& prm, int max_work, cudaStream_t st) {
   if (sms <= 0) return invalid_arg("tcgen05 path: no CUDA device");
   // persistent: one CTA (CG = 1) or CTA pair (CG = 2) per SM (pair)
   const int grid = std::max(1, std::min(sms / CG, max_work)) * CG;
-  if constexpr (CG == 1) {
-    kern<<<grid, kThreads, C::kSmem, st>>>(prm);
-  } else {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = C::kSmem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    HXM_TRY_CUDA(cudaLaunchKernelEx(&cfg, kern, prm));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  // programmatic dependent launch: this grid's CTAs may start (barrier
+  // init, TMEM alloc, tensor-map prefetch) while the previous kernel in the
+  // stream drains; griddepcontrol.wait in the kernel orders the data
+  if (pdl_on()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
   }
+  if constexpr (CG == 2) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  HXM_TRY_CUDA(cudaLaunchKernelEx(&cfg, kern, prm));
   HXM_CHECK_LAUNCH();
   return HXM_OK;
 }
