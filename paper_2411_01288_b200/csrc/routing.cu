@@ -195,10 +195,13 @@ hxm_status build_impl(const int32_t* a, int64_t n, int64_t E, int64_t blk,
 // tiles of at most `rows` positions per expert segment; min_one: experts
 // with an empty segment still get one (empty) tile -- used by ESTMM so that
 // their zero gradient is written (es_ops.cpp:202 zero-initialised output).
+// flags: bit 0 = the expert spans several tiles (split), bit 1 = empty
+// segment; with `counts` (real slots per expert) bit 2 is set and bits 8..
+// hold how many of the tile's rows are real (the rest are -1 pads).
 template <class IdxT, int NT = 1024>
 __device__ void tile_pass(const IdxT* __restrict__ idx, int E, int rows, int min_one,
                           SegTile* __restrict__ tiles, int32_t* __restrict__ tile_off,
-                          int32_t* __restrict__ n_tiles) {
+                          int32_t* __restrict__ n_tiles, const int32_t* counts = nullptr) {
   using Scan = cub::BlockScan<int32_t, NT>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int32_t carry;
@@ -230,6 +233,11 @@ __device__ void tile_pass(const IdxT* __restrict__ idx, int E, int rows, int min
         t.end = static_cast<int>(hi < b + len ? hi : b + len);
         if (len == 0) t.end = t.begin;
         t.flags = split | empty;
+        if (counts) {
+          const int64_t real = b + counts[e] - t.begin;
+          const int vr = static_cast<int>(real < 0 ? 0 : (real > t.end - t.begin ? t.end - t.begin : real));
+          t.flags |= 4 | (vr << 8);
+        }
         tiles[off + j] = t;
       }
     }
@@ -399,11 +407,11 @@ __global__ void __launch_bounds__(kThreads) fwd_prologue(FwdPrologue a) {
     }
     if (blockIdx.x == gridDim.x - 1) {
       tile_pass<int32_t, kThreads>(sidx, E, a.s0.rows, a.s0.min_one, a.s0.tiles, a.s0.tile_off,
-                                   a.s0.n_tiles);
+                                   a.s0.n_tiles, a.total);
       tile_pass<int32_t, kThreads>(sidx, E, a.s1.rows, a.s1.min_one, a.s1.tiles, a.s1.tile_off,
-                                   a.s1.n_tiles);
+                                   a.s1.n_tiles, a.total);
       tile_pass<int32_t, kThreads>(sidx, E, a.s2.rows, a.s2.min_one, a.s2.tiles, a.s2.tile_off,
-                                   a.s2.n_tiles);
+                                   a.s2.n_tiles, a.total);
     }
   }
   pro_ts(5);

@@ -613,9 +613,20 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
     // one item ahead, so an epilogue that finds its accumulator already full
     // does not wait on the tile table / index latency.
     auto tile_at = [&](int wi) { return wi < total ? p.tiles[wi / per_item] : SegTile{0, 0, 0, 0}; };
+    // MODE 0: this lane's token-order output row.  MODE 1/2 only need to
+    // know pads, which the layer's tile flags carry (no index load).
     auto orow_of = [&](const SegTile& tt) {
       const int qq = tt.begin + static_cast<int>(rank) * BM + lg * 32 + lane;
-      return qq < tt.end ? p.omap(qq) : -1;
+      if (dense_out && (tt.flags & 4)) return qq - tt.begin < (tt.flags >> 8) ? 0 : -1;
+      if (qq >= tt.end) return -1;
+      if (p.omap.kind == MAP_SLOT) {  // issued where written (asm volatile: not sunk)
+        int sv;
+        asm volatile("ld.global.nc.b32 %0, [%1];"
+                     : "=r"(sv)
+                     : "l"(static_cast<const int32_t*>(p.omap.v) + qq));
+        return sv < 0 ? -1 : sv % p.omap.n;
+      }
+      return p.omap(qq);
     };
     SegTile t_cur = ESTMM ? SegTile{0, 0, 0, 0} : tile_at(cluster);
     int orow_cur = ESTMM ? -1 : orow_of(t_cur);
