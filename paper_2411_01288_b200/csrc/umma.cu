@@ -297,6 +297,51 @@ __device__ __forceinline__ void act_both(int act, float x, float& f, float& df) 
   }
 }
 
+// ---- packed fp32x2 math (FFMA2 / FMUL2 on sm_100): two lanes per issue ----
+__device__ __forceinline__ float2 f2_fma(float2 a, float2 b, float2 c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)),
+        "l"(*reinterpret_cast<uint64_t*>(&c)));
+  return *reinterpret_cast<float2*>(&d);
+}
+__device__ __forceinline__ float2 f2_mul(float2 a, float2 b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)));
+  return *reinterpret_cast<float2*>(&d);
+}
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float tanh_approx(float u) {
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
+  return t;
+}
+// F and F' of two values at once (tensor.cpp:39-53, 62-72); GELU-tanh with
+// one tanh.approx per value shared by F and F', the rest in f32x2 ops.
+template <int ACT>
+__device__ __forceinline__ void act_pair(float2 x, float2& f, float2& df) {
+  if constexpr (ACT == HXM_ACT_GELU) {
+    constexpr float k0 = 0.7978845608028654f, k1 = 0.7978845608028654f * 0.044715f;
+    const float2 x2 = f2_mul(x, x);
+    const float2 u = f2_mul(x, f2_fma(f2(k1), x2, f2(k0)));
+    const float2 t = make_float2(tanh_approx(u.x), tanh_approx(u.y));
+    const float2 hx = f2_mul(x, f2(0.5f));
+    f = f2_fma(hx, t, hx);
+    const float2 du = f2_fma(f2(3.f * k1), x2, f2(k0));
+    const float2 omt = f2_fma(make_float2(-t.x, -t.y), t, f2(1.f));
+    df = f2_fma(f2_mul(hx, omt), du, f2_fma(t, f2(0.5f), f2(0.5f)));
+  } else if constexpr (ACT == HXM_ACT_RELU) {
+    f = make_float2(x.x > 0.f ? x.x : 0.f, x.y > 0.f ? x.y : 0.f);
+    df = make_float2(x.x > 0.f ? 1.f : 0.f, x.y > 0.f ? 1.f : 0.f);
+  } else {
+    f = x;
+    df = f2(1.f);
+  }
+}
+
 struct UParams {
   CUtensorMap tmA;  // ESMM A / ESTMM X1
   CUtensorMap tmB;  // ESMM W / ESTMM X2
@@ -724,21 +769,20 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
                 // stash = (F'(y1), F(y1)): everything the backward needs
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                  float f0, d0, f1, d1;
+                  float2 f, df;
                   // activation fixed at compile time (MODE 1 instantiations)
-                  act_both(ACT >= 0 ? ACT : p.act, v[8 * j + 2 * i], f0, d0);
-                  act_both(ACT >= 0 ? ACT : p.act, v[8 * j + 2 * i + 1], f1, d1);
-                  a1[i] = pad ? 0u : pack_bf16(d0, d1);
-                  a2[i] = pad ? 0u : pack_bf16(f0, f1);
+                  act_pair<ACT>(make_float2(v[8 * j + 2 * i], v[8 * j + 2 * i + 1]), f, df);
+                  a1[i] = pad ? 0u : pack_bf16(df.x, df.y);
+                  a2[i] = pad ? 0u : pack_bf16(f.x, f.y);
                 }
               } else {
                 // g_y1 = g_y2 * F'(y1)
                 const __nv_bfloat16* yb = reinterpret_cast<const __nv_bfloat16*>(&dv[j]);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                  const float g0 = v[8 * j + 2 * i] * __bfloat162float(yb[2 * i]);
-                  const float g1 = v[8 * j + 2 * i + 1] * __bfloat162float(yb[2 * i + 1]);
-                  a1[i] = pad ? 0u : pack_bf16(g0, g1);
+                  const float2 g = f2_mul(make_float2(v[8 * j + 2 * i], v[8 * j + 2 * i + 1]),
+                                          __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(yb)[i]));
+                  a1[i] = pad ? 0u : pack_bf16(g.x, g.y);
                 }
               }
               *reinterpret_cast<uint4*>(obox + hrow * 64 + ((j ^ swz) * 16)) =
