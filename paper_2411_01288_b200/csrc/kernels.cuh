@@ -62,8 +62,8 @@ struct EsmmArgs {
   void* out1;      // FWD_ACT / BWD_ACT dense outputs (dtype), row stride d2
   void* out2;
   const void* y1s;  // BWD_ACT: pre-activation stash (dtype), row stride d2
-  float* colsum;    // BWD_ACT (tcgen05): per-(tile, CTA) column sums of out1,
-                    // [(tile * CG + cta) x d2] -> colsum_combine (fused ESS)
+  float* colsum;    // BWD_ACT (tcgen05): per-(tile, CTA, lane group) column sums of out1,
+                    // [((tile * CG + cta) * 4 + group) x d2] -> colsum_combine
 };
 
 struct EstmmArgs {

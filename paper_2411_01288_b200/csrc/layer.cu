@@ -104,7 +104,7 @@ LayerWs carve(Arena& ar, const hxm_layer_desc& d) {
   const char* fuse = std::getenv("HXM_FUSE_GB1");  // 0: separate ESS pass for gb1
   if (w.rows_a >= kUmmaRows && !(fuse && fuse[0] == '0'))
     w.colsum = ar.take<float>(static_cast<size_t>(max_tiles(w.bound, d.n_experts, w.rows_a)) *
-                              (w.rows_a / kUmmaRows) * d.hidden);
+                              (w.rows_a / kUmmaRows) * 4 * d.hidden);
   return w;
 }
 
@@ -350,7 +350,7 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
   b6.colsum = w.colsum;
   HXM_RETURN_IF(launch_esmm(dt, b6, st));
   if (w.colsum) {
-    const int parts = w.rows_a / kUmmaRows;
+    const int parts = (w.rows_a / kUmmaRows) * 4;  // per tile: CTAs x TMEM lane groups
     HXM_RETURN_IF(launch_colsum_combine(
         w.colsum, w.tiles_a_off, static_cast<int>(E), parts, H, gb1, st, "gb1_combine",
         (static_cast<double>(max_tiles(w.bound, E, w.rows_a)) * parts + E) * H * 4.0));

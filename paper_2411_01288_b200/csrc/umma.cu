@@ -809,23 +809,40 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
             }
             if (bwd && p.colsum) {
               // fused gb1 (ESS of g_y1, es_ops.cpp:86-102): column sums of the
-              // staged 128 x 32 box (the stored bf16 values; pads are zero
-              // rows).  Warp wq of the half sums columns 8wq..8wq+7, lane group
-              // g rows 32g..32g+31 (row order rotated by 2g: conflict-free),
-              // then one deterministic partial per (tile, CTA) is written.
-              const int wq = (warp - 2) & 3, g = lane >> 3, c = wq * 8 + (lane & 7);
-              float s = 0.f;
-#pragma unroll 8
-              for (int i = 0; i < 32; ++i) {
-                const int r = g * 32 + ((i + 2 * g) & 31);
-                const __nv_bfloat16 b = *reinterpret_cast<const __nv_bfloat16*>(
-                    obox + r * 64 + ((wq ^ ((r >> 1) & 3)) * 16) + (lane & 7) * 2);
-                s += __bfloat162float(b);
+              // bf16 values this warp just staged (its own 32 rows, so only
+              // __syncwarp ordering).  Lane (rsub, cq) reads 16-byte column
+              // chunk cq of rows rsub + 8i (4 x LDS.128, conflict-free),
+              // sums them in f32x2, reduces the 8 row groups by shuffles;
+              // lanes 0..3 write this warp's 32 column sums: one
+              // deterministic partial row per (tile, CTA, lane group).
+              __syncwarp();
+              const int cq = lane & 3, rsub = lane >> 2;
+              float2 cs[4] = {f2(0.f), f2(0.f), f2(0.f), f2(0.f)};
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int r = lg * 32 + rsub + 8 * i;
+                const uint4 q4 = *reinterpret_cast<const uint4*>(obox + r * 64 +
+                                                                 ((cq ^ ((r >> 1) & 3)) * 16));
+                const uint32_t w4[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  cs[k] = f2_fma(make_float2(__uint_as_float(w4[k] << 16),
+                                             __uint_as_float(w4[k] & 0xffff0000u)),
+                                 f2(1.f), cs[k]);
               }
-              s += __shfl_xor_sync(0xffffffffu, s, 8);
-              s += __shfl_xor_sync(0xffffffffu, s, 16);
-              if (lane < 8)
-                p.colsum[(static_cast<int64_t>(w / per_item) * CG + rank) * N + n + c] = s;
+#pragma unroll
+              for (int o = 4; o < 32; o <<= 1)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  cs[k].x += __shfl_xor_sync(0xffffffffu, cs[k].x, o);
+                  cs[k].y += __shfl_xor_sync(0xffffffffu, cs[k].y, o);
+                }
+              if (lane < 4) {
+                float* dst = p.colsum + ((static_cast<int64_t>(w / per_item) * CG + rank) * 4 + lg) * N +
+                             n + cq * 8;
+                reinterpret_cast<float4*>(dst)[0] = make_float4(cs[0].x, cs[0].y, cs[1].x, cs[1].y);
+                reinterpret_cast<float4*>(dst)[1] = make_float4(cs[2].x, cs[2].y, cs[3].x, cs[3].y);
+              }
             }
             ++dchunk;
           } else {
