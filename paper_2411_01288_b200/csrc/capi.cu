@@ -31,6 +31,22 @@ int sm_count() {
   return n;
 }
 
+// A non-blocking side stream per device plus two fork/join events, for
+// independent work that runs beside the main stream (recorded into CUDA
+// graphs as parallel branches under stream capture).
+SideStream side_stream() {
+  static SideStream cached[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  SideStream& s = cached[dev < 64 ? dev : 0];
+  if (!s.st) {
+    cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming);
+  }
+  return s;
+}
+
 bool pdl_on() {
   static const bool on = [] {
     const char* e = std::getenv("HXM_PDL");

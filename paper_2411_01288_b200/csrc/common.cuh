@@ -59,6 +59,11 @@ inline hxm_status invalid_arg(const std::string& m) {
 
 int sm_count();  // cached per device
 bool pdl_on();   // programmatic dependent launch (HXM_PDL=0 disables)
+struct SideStream {
+  cudaStream_t st = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream side_stream();  // per device, created on first use
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) {
   return (a + b - 1) / b;

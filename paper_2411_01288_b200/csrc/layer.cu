@@ -349,11 +349,18 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
   // bf16 tile per (tile, CTA)), then a deterministic per-expert combine
   b6.colsum = w.colsum;
   HXM_RETURN_IF(launch_esmm(dt, b6, st));
+  SideStream side{};
   if (w.colsum) {
+    // the gb1 combine is independent of gW1 / gx: it runs on the side
+    // stream beside them (a parallel branch of the captured graph)
+    side = side_stream();
+    HXM_TRY_CUDA(cudaEventRecord(side.fork, st));
+    HXM_TRY_CUDA(cudaStreamWaitEvent(side.st, side.fork, 0));
     const int parts = (w.rows_a / kUmmaRows) * 4;  // per tile: CTAs x TMEM lane groups
     HXM_RETURN_IF(launch_colsum_combine(
-        w.colsum, w.tiles_a_off, static_cast<int>(E), parts, H, gb1, st, "gb1_combine",
+        w.colsum, w.tiles_a_off, static_cast<int>(E), parts, H, gb1, side.st, "gb1_combine",
         (static_cast<double>(max_tiles(w.bound, E, w.rows_a)) * parts + E) * H * 4.0));
+    HXM_TRY_CUDA(cudaEventRecord(side.join, side.st));
   } else {
     es.x = w.g1s;
     es.map = map_dense();
@@ -392,7 +399,9 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
   b10.out_f32 = gx;
   b10.out1 = nullptr;
   b10.y1s = nullptr;
-  return launch_esmm(dt, b10, st);
+  HXM_RETURN_IF(launch_esmm(dt, b10, st));
+  if (side.st) HXM_TRY_CUDA(cudaStreamWaitEvent(st, side.join, 0));
+  return HXM_OK;
 }
 
 hxm_status hxm_moe_stash_export(const hxm_layer_desc* d, const void* ws, int64_t choice,
