@@ -215,6 +215,11 @@ void hxm_profile_reset(void);
  * Returns the number of names written, -1 on a CUDA error. */
 int hxm_profile_read(int max, char* names, int name_len, double* total_ms,
                      int64_t* launches, double* work, int32_t* kind);
+/* Same aggregation plus the algorithmic HBM bytes of each region (0 when the
+ * region only states FLOP): GEMM regions carry both, so a caller can place
+ * each kernel under the tensor or the HBM roofline. */
+int hxm_profile_read2(int max, char* names, int name_len, double* total_ms,
+                      int64_t* launches, double* work, int32_t* kind, double* bytes);
 /* Kernels launched by this library since load. */
 uint64_t hxm_launch_count(void);
 

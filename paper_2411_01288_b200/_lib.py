@@ -72,27 +72,30 @@ SIGNATURES = {
     "hxm_profile_enable": (None, [C.c_int]),
     "hxm_profile_reset": (None, []),
     "hxm_profile_read": (C.c_int, [C.c_int, C.c_char_p, C.c_int, _p, _p, _p, _p]),
+    "hxm_profile_read2": (C.c_int, [C.c_int, C.c_char_p, C.c_int, _p, _p, _p, _p, _p]),
     "hxm_launch_count": (C.c_uint64, []),
 }
 
 
 def profile_read(max_names: int = 64, name_len: int = 64):
-    """{name: (total_ms, launches, work, kind)} for regions recorded since reset."""
+    """{name: (total_ms, launches, work, kind, bytes)} for regions recorded since reset
+    (bytes: algorithmic HBM bytes of FLOP-counted regions, 0 if not stated)."""
     import numpy as np
     names = C.create_string_buffer(max_names * name_len)
     ms = np.zeros(max_names, np.float64)
     n = np.zeros(max_names, np.int64)
     work = np.zeros(max_names, np.float64)
     kind = np.zeros(max_names, np.int32)
-    cnt = lib().hxm_profile_read(max_names, names, name_len, ms.ctypes.data, n.ctypes.data,
-                                 work.ctypes.data, kind.ctypes.data)
+    nbytes = np.zeros(max_names, np.float64)
+    cnt = lib().hxm_profile_read2(max_names, names, name_len, ms.ctypes.data, n.ctypes.data,
+                                  work.ctypes.data, kind.ctypes.data, nbytes.ctypes.data)
     if cnt < 0:
         raise HexaMoeCudaError("hxm_profile_read failed")
     out = {}
     raw = names.raw
     for i in range(cnt):
         nm = raw[i * name_len:(i + 1) * name_len].split(b"\0", 1)[0].decode()
-        out[nm] = (float(ms[i]), int(n[i]), float(work[i]), int(kind[i]))
+        out[nm] = (float(ms[i]), int(n[i]), float(work[i]), int(kind[i]), float(nbytes[i]))
     return out
 
 _lib = None

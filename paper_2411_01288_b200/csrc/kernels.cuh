@@ -43,6 +43,7 @@ enum EpiMode : int {
 struct EsmmArgs {
   const char* label;  // profiling region name (nullable)
   double work;        // algorithmic FLOP (GEMMs) or bytes (ESS) of the launch
+  double bytes;       // GEMMs: algorithmic HBM bytes (operands once, outputs once)
   const void* a;  // A rows, K = d1 columns
   RowMap amap;
   int64_t a_rows;  // rows of the tensor behind `a` (TMA bounds)
@@ -69,6 +70,7 @@ struct EsmmArgs {
 struct EstmmArgs {
   const char* label;  // profiling region name (nullable)
   double work;        // algorithmic FLOP (GEMMs) or bytes (ESS) of the launch
+  double bytes;       // algorithmic HBM bytes (operands once, outputs once)
   const void* x1;  // rows via m1, d1 columns
   RowMap m1;
   const void* x2;  // rows via m2, d2 columns

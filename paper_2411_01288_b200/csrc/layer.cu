@@ -226,6 +226,11 @@ hxm_status hxm_moe_forward(const hxm_layer_desc* d, const void* x, const void* w
   const double kn = static_cast<double>(slots);
   a1.label = "esmm_fwd1";
   a1.work = 2.0 * kn * d->d_in * d->hidden;
+  const double es_ = static_cast<double>(esize(d->dtype));
+  const double wbytes = static_cast<double>(E) * d->d_in * d->hidden * es_;  // W1
+  const double w2bytes = static_cast<double>(E) * d->hidden * d->d_out * es_;
+  // x_s read, W1 read, the two stash outputs written (real slots)
+  a1.bytes = kn * d->d_in * es_ + wbytes + 2.0 * kn * d->hidden * es_;
   a1.act = d->activation;
   a1.omap = slot;
   a1.out1 = w.y1s;
@@ -243,6 +248,8 @@ hxm_status hxm_moe_forward(const hxm_layer_desc* d, const void* x, const void* w
   a2.epi = EPI_ATOMIC;
   a2.label = "esmm_fwd2";
   a2.work = 2.0 * kn * d->hidden * d->d_out;
+  // y2 read, W2 read, y (fp32) written once
+  a2.bytes = kn * d->hidden * es_ + w2bytes + 4.0 * N * d->d_out;
   a2.out_f32 = y;
   a2.omap = slot;
   a2.out1 = a2.out2 = nullptr;
@@ -322,6 +329,8 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
   t2.skip_zero_split = 1;  // done by the backward prologue
   t2.label = "estmm_gw2";
   t2.work = 2.0 * kn * H * Do;
+  // y2 and the sorted g_y read, gW2 (fp32) written
+  t2.bytes = kn * (H + Do) * esz + 4.0 * E * H * Do;
   HXM_RETURN_IF(launch_estmm(dt, t2, st));
   // (6,7) g_y1 = (g_y W2^T) * F'(y1)          (moe_layer.cpp:105-108)
   EsmmArgs b6{};
@@ -340,6 +349,8 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
   b6.epi = EPI_BWD_ACT;
   b6.label = "esmm_bwd_act";
   b6.work = 2.0 * kn * Do * H;
+  // sorted g_y, W2 and F'(y1) read, g_y1 written
+  b6.bytes = kn * (Do + 2.0 * H) * esz + static_cast<double>(E) * H * Do * esz;
   b6.act = d->activation;
   b6.omap = slot;
   b6.out1 = w.g1s;
@@ -383,6 +394,7 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
   t1.out = gw1;
   t1.label = "estmm_gw1";
   t1.work = 2.0 * kn * Di * H;
+  t1.bytes = kn * (Di + H) * esz + 4.0 * E * Di * H;
   HXM_RETURN_IF(launch_estmm(dt, t1, st));
   // (10) gx += g_y1_i W1^T                    (moe_layer.cpp:118)
   EsmmArgs b10 = b6;
@@ -396,6 +408,8 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
   b10.epi = EPI_ATOMIC;
   b10.label = "esmm_bwd_gx";
   b10.work = 2.0 * kn * H * Di;
+  // g_y1 and W1 read, gx (fp32) written
+  b10.bytes = kn * H * esz + static_cast<double>(E) * Di * H * esz + 4.0 * N * Di;
   b10.out_f32 = gx;
   b10.out1 = nullptr;
   b10.y1s = nullptr;

@@ -15,7 +15,7 @@ int esmm_tile_rows(hxm_dtype dt, int64_t d1, int64_t d2) {
 }
 
 hxm_status launch_esmm(hxm_dtype dt, const EsmmArgs& a, cudaStream_t st) {
-  ProfScope ps(st, a.label ? a.label : "esmm", a.work, WORK_FLOP);
+  ProfScope ps(st, a.label ? a.label : "esmm", a.work, WORK_FLOP, a.bytes);
   if (a.tile_rows == kUmmaRows || a.tile_rows == kUmma2Rows) {
     if (dt != HXM_BF16 || !umma_supports_esmm(a.d1, a.d2))
       return invalid_arg("esmm: 128-row tiles need the tcgen05 kernel");
@@ -26,7 +26,7 @@ hxm_status launch_esmm(hxm_dtype dt, const EsmmArgs& a, cudaStream_t st) {
 }
 
 hxm_status launch_estmm(hxm_dtype dt, const EstmmArgs& a, cudaStream_t st) {
-  ProfScope ps(st, a.label ? a.label : "estmm", a.work, WORK_FLOP);
+  ProfScope ps(st, a.label ? a.label : "estmm", a.work, WORK_FLOP, a.bytes);
   if (!a.skip_zero_split)
     HXM_RETURN_IF(zero_split_experts(a.tiles, a.n_tiles, a.max_tiles, a.d1 * a.d2, a.out, st));
   if (dt == HXM_BF16 && umma_supports_estmm(a.d1, a.d2)) return umma_estmm(a, st);

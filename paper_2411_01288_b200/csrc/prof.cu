@@ -21,6 +21,7 @@ struct Rec {
   cudaEvent_t a, b;
   double work;
   int kind;
+  double bytes;
 };
 std::mutex g_mu;
 bool g_on = false;
@@ -53,8 +54,8 @@ static void record(cudaEvent_t e, cudaStream_t st) {
     cudaEventRecord(e, st);
 }
 
-ProfScope::ProfScope(cudaStream_t st, const char* name, double work, int kind)
-    : st_(st), name_(name), work_(work), kind_(kind) {
+ProfScope::ProfScope(cudaStream_t st, const char* name, double work, int kind, double bytes)
+    : st_(st), name_(name), work_(work), kind_(kind), bytes_(bytes) {
   std::lock_guard<std::mutex> l(g_mu);
   if (!g_on) return;
   active_ = true;
@@ -68,7 +69,7 @@ ProfScope::~ProfScope() {
   std::lock_guard<std::mutex> l(g_mu);
   record(static_cast<cudaEvent_t>(b_), st_);
   g_recs.push_back(Rec{name_, static_cast<cudaEvent_t>(a_), static_cast<cudaEvent_t>(b_),
-                       work_, kind_});
+                       work_, kind_, bytes_});
 }
 
 }  // namespace hxm
@@ -93,9 +94,14 @@ void hxm_profile_reset(void) {
 
 int hxm_profile_read(int max, char* names, int name_len, double* total_ms, int64_t* launches,
                      double* work, int32_t* kind) {
+  return hxm_profile_read2(max, names, name_len, total_ms, launches, work, kind, nullptr);
+}
+
+int hxm_profile_read2(int max, char* names, int name_len, double* total_ms, int64_t* launches,
+                      double* work, int32_t* kind, double* bytes) {
   std::lock_guard<std::mutex> l(g_mu);
   struct Agg {
-    double ms = 0, work = 0;
+    double ms = 0, work = 0, bytes = 0;
     int64_t n = 0;
     int kind = 0;
   };
@@ -112,6 +118,7 @@ int hxm_profile_read(int max, char* names, int name_len, double* total_ms, int64
     Agg& a = agg[r.name];
     a.ms += ms;
     a.work += r.work;
+    a.bytes += r.bytes;
     a.n += 1;
     a.kind = r.kind;
   }
@@ -124,6 +131,7 @@ int hxm_profile_read(int max, char* names, int name_len, double* total_ms, int64
     launches[i] = a.n;
     work[i] = a.work;
     kind[i] = a.kind;
+    if (bytes) bytes[i] = a.bytes;
     ++i;
   }
   return i;

@@ -10,7 +10,8 @@ void note_launch();
 
 class ProfScope {
  public:
-  ProfScope(cudaStream_t st, const char* name, double work, int kind);
+  // bytes: algorithmic HBM bytes of a FLOP-counted region (0 = not stated)
+  ProfScope(cudaStream_t st, const char* name, double work, int kind, double bytes = 0.0);
   ~ProfScope();
   ProfScope(const ProfScope&) = delete;
   ProfScope& operator=(const ProfScope&) = delete;
@@ -20,6 +21,7 @@ class ProfScope {
   const char* name_;
   double work_;
   int kind_;
+  double bytes_;
   bool active_ = false;
   void* a_ = nullptr;
   void* b_ = nullptr;
