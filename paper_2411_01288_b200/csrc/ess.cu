@@ -121,40 +121,65 @@ __global__ void __launch_bounds__(NT) ess_partial(EssArgs a) {
   ess_item<T, VEC>(a, blockIdx.x, blockIdx.y);
 }
 
-// out[e][c] = sum of partial rows r0..r1 (in order) -- 8 independent loads in
-// flight per thread instead of one dependent chain
-__device__ __forceinline__ float sum_rows(const float* __restrict__ partial, int64_t r0,
-                                          int64_t r1, int64_t d, int64_t c) {
-  float s = 0.f;
-  int64_t r = r0;
-  for (; r + 8 <= r1; r += 8) {
-    float v[8];
+// out_row[c0 .. c0+128) = column sums of partial rows [r0, r1) (row stride d):
+// the block's W warps split the rows (4 rows in flight per warp, each lane
+// 4 columns), then fixed-order smem combine -> deterministic, and a long
+// reduction (a skewed expert's hundreds of tiles) is W-way parallel.
+template <int W>
+__device__ __forceinline__ void combine_block(const float* __restrict__ partial, int64_t r0,
+                                              int64_t r1, int64_t d, int64_t c0,
+                                              float* __restrict__ out_row) {
+  __shared__ float red[W][128];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t c = c0 + lane * 4;
+  const bool vec = (d % 4 == 0) && c + 4 <= d;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int64_t r = r0 + warp; r < r1; r += 4 * W) {
+    float v[4][4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = partial[(r + u) * d + c];
+    for (int u = 0; u < 4; ++u) {
+      const int64_t rr = r + u * W;
+      const float* row = partial + rr * d;
+      if (rr < r1 && vec) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(row + c));
+        v[u][0] = q.x; v[u][1] = q.y; v[u][2] = q.z; v[u][3] = q.w;
+      } else {
 #pragma unroll
-    for (int u = 0; u < 8; ++u) s += v[u];
+        for (int j = 0; j < 4; ++j) v[u][j] = (rr < r1 && c + j < d) ? __ldg(row + c + j) : 0.f;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[j] += v[u][j];
   }
-  for (; r < r1; ++r) s += partial[r * d + c];
-  return s;
+  __syncthreads();  // red[] reuse across calls
+#pragma unroll
+  for (int j = 0; j < 4; ++j) red[warp][lane * 4 + j] = acc[j];
+  __syncthreads();
+  for (int t = threadIdx.x; t < 128; t += W * 32) {
+    if (c0 + t >= d) continue;
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < W; ++w) s += red[w][t];
+    out_row[c0 + t] = s;
+  }
 }
 
-__global__ void ess_combine(EssArgs a) {
+__global__ void __launch_bounds__(256) ess_combine(EssArgs a) {
   const int e = blockIdx.y;
-  const int64_t d = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (d >= a.d) return;
-  a.out[static_cast<int64_t>(e) * a.d + d] =
-      sum_rows(a.partial, a.tile_off[e], a.tile_off[e + 1], a.d, d);
+  combine_block<8>(a.partial, a.tile_off[e], a.tile_off[e + 1], a.d,
+                   static_cast<int64_t>(blockIdx.x) * 128, a.out + static_cast<int64_t>(e) * a.d);
 }
 
-__global__ void colsum_combine(const float* __restrict__ partial,
-                               const int32_t* __restrict__ tile_off, int parts, int64_t d,
-                               float* __restrict__ out) {
+__global__ void __launch_bounds__(256) colsum_combine(const float* __restrict__ partial,
+                                                      const int32_t* __restrict__ tile_off,
+                                                      int parts, int64_t d,
+                                                      float* __restrict__ out) {
   const int e = blockIdx.y;
-  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (c >= d) return;
-  out[static_cast<int64_t>(e) * d + c] = sum_rows(
-      partial, static_cast<int64_t>(tile_off[e]) * parts,
-      static_cast<int64_t>(tile_off[e + 1]) * parts, d, c);
+  combine_block<8>(partial, static_cast<int64_t>(tile_off[e]) * parts,
+                   static_cast<int64_t>(tile_off[e + 1]) * parts, d,
+                   static_cast<int64_t>(blockIdx.x) * 128, out + static_cast<int64_t>(e) * d);
 }
 
 template <class T>
@@ -169,7 +194,7 @@ hxm_status launch_typed(const EssArgs& a, cudaStream_t st) {
     else ess_partial<T, 1><<<grid, NT, 0, st>>>(a);
     HXM_CHECK_LAUNCH();
   }
-  dim3 grid(static_cast<unsigned>(ceil_div(a.d, 256)), static_cast<unsigned>(a.n_experts));
+  dim3 grid(static_cast<unsigned>(ceil_div(a.d, 128)), static_cast<unsigned>(a.n_experts));
   if (a.d > 0 && a.n_experts > 0 && a.out) {
     ess_combine<<<grid, 256, 0, st>>>(a);
     HXM_CHECK_LAUNCH();
@@ -240,7 +265,7 @@ __global__ void __launch_bounds__(NT) bwd_prologue(BwdPrologue b) {
     for (int64_t i = n4 * 4 + gtid; i < b.gx_elems; i += gthreads) b.gx[i] = 0.f;
   }
   // split experts: 16 block-sized parts of each first chunk's slices
-  constexpr int kParts = 16;
+  constexpr int kParts = 64;
   const int nk = *b.n_ktiles;
   for (int it = blockIdx.x; it < nk * kParts; it += gridDim.x) {
     const int ti = it / kParts, part = it % kParts;
@@ -251,9 +276,16 @@ __global__ void __launch_bounds__(NT) bwd_prologue(BwdPrologue b) {
       const int64_t slice = o == 0 ? b.gw2_slice : b.gw1_slice;
       if (!out) continue;
       out += static_cast<int64_t>(t.expert) * slice;
-      const int64_t per = ceil_div(slice, kParts);
+      // float4 granules (slices are multiples of 4 when d1 or d2 is)
+      const int64_t per = ceil_div(ceil_div(slice, kParts), 4) * 4;
       const int64_t lo = part * per, hi = min(slice, lo + per);
-      for (int64_t i = lo + threadIdx.x; i < hi; i += NT) out[i] = 0.f;
+      const bool v4 = slice % 4 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0;
+      if (v4) {
+        for (int64_t i = lo + 4 * threadIdx.x; i < hi; i += 4 * NT)
+          *reinterpret_cast<float4*>(out + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
+        for (int64_t i = lo + threadIdx.x; i < hi; i += NT) out[i] = 0.f;
+      }
     }
   }
   const EssArgs& a = b.es;
@@ -263,10 +295,12 @@ __global__ void __launch_bounds__(NT) bwd_prologue(BwdPrologue b) {
   for (int it = blockIdx.x; it < items; it += gridDim.x) ess_item<T, VEC>(a, it / slabs, it % slabs);
   if (!a.out) return;
   cgp::this_grid().sync();
-  for (int64_t i = gtid; i < static_cast<int64_t>(a.n_experts) * a.d; i += gthreads) {
-    const int e = static_cast<int>(i / a.d);
-    const int64_t c = i % a.d;
-    a.out[i] = sum_rows(a.partial, a.tile_off[e], a.tile_off[e + 1], a.d, c);
+  const int chunks = static_cast<int>(ceil_div(a.d, 128));
+  for (int it = blockIdx.x; it < a.n_experts * chunks; it += gridDim.x) {
+    const int e = it / chunks;
+    combine_block<NT / 32>(a.partial, a.tile_off[e], a.tile_off[e + 1], a.d,
+                           static_cast<int64_t>(it % chunks) * 128,
+                           a.out + static_cast<int64_t>(e) * a.d);
   }
 }
 
@@ -304,7 +338,7 @@ hxm_status launch_colsum_combine(const float* partial, const int32_t* tile_off, 
   ProfScope ps(st, label ? label : "colsum_combine", work_bytes, WORK_BYTES);
   if (d <= 0 || n_experts <= 0) return HXM_OK;
   dim3 grid(static_cast<unsigned>(ceil_div(d, 128)), static_cast<unsigned>(n_experts));
-  colsum_combine<<<grid, 128, 0, st>>>(partial, tile_off, parts, d, out);
+  colsum_combine<<<grid, 256, 0, st>>>(partial, tile_off, parts, d, out);
   HXM_CHECK_LAUNCH();
   return HXM_OK;
 }
