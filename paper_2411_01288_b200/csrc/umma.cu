@@ -19,6 +19,8 @@
 // full/empty (MMA <-> epilogue), so tile i's epilogue overlaps tile i+1's MMA.
 #include <cuda.h>
 
+#include <cstring>
+
 #include "kernels.cuh"
 
 namespace hxm {
@@ -34,6 +36,24 @@ constexpr uint32_t kTmemCols = 512;
 constexpr int kABytes = BM * BK * 2;  // 16 KB
 
 // ------------------------------------------------------------- PTX layer --
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Debug timeline (build with -DHXM_TRACE_BUILD, run with HXM_TRACE=<label>,
+// read with tools/trace_kernel.py): per-CTA item timestamps and barrier
+// wait totals.  Compiled out otherwise.
+#ifdef HXM_TRACE_BUILD
+constexpr bool kTrace = true;
+#else
+constexpr bool kTrace = false;
+#endif
+#define TRACE(item, slot)                                                              \
+  do {                                                                                 \
+    if (kTrace && p.trace && (item) < 64)                                              \
+      p.trace[(static_cast<size_t>(blockIdx.x) * 64 + (item)) * 8 + (slot)] = gtime(); \
+  } while (0)
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -353,6 +373,8 @@ struct UParams {
   RowMap amap;      // gather map of A (ESMM rows / ESTMM X1 rows)
   RowMap bmap;      // ESTMM X2 rows
   int a_gather, b_gather, b_kmajor;
+  int dbg_noload;
+  unsigned long long* trace;  // debug timeline (HXM_TRACE), null normally
   int b_sw64;  // CG = 2, MN-major B halves of 32-column multiples: 64B-swizzled boxes
   int K, N, M;  // ESMM: K=d1, N=d2 ; ESTMM: M=d1, N=d2
   int n_nt, n_mt;
@@ -367,6 +389,7 @@ struct UParams {
   const void* y1s;
   float* colsum;  // MODE 2: per-(tile, lane group) column sums of the output
   float* est_out;
+  const char* label;
 };
 
 // CG = CTAs per UMMA (cta_group): with CG = 2 a CTA pair runs M = 256 tiles,
@@ -402,8 +425,10 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
   if constexpr (CG == 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   const int cluster = blockIdx.x / CG, n_clusters = gridDim.x / CG;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // 1024-byte aligned (128B-swizzle atoms); pointer arithmetic on the
+  // __shared__ array keeps the address space visible to the compiler, so
+  // staging accesses compile to LDS/STS rather than generic LD/ST
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* staging = smem + C::kStages * C::kStage;  // kEpiWarps x 4 KB
   uint64_t* full = reinterpret_cast<uint64_t*>(staging + C::kStaging);
   uint64_t* empty = full + C::kStages;
@@ -461,7 +486,8 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
     }
     int s = 0;
     uint32_t ph = 0;
-    for (int w = cluster; w < total; w += n_clusters) {
+    int pit_ = 0;
+    for (int w = cluster; w < total; w += n_clusters, ++pit_) {
       const SegTile t = p.tiles[w / per_item];
       const int rem = w % per_item;
       if (!ESTMM) {
@@ -473,8 +499,12 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
           const int q = t.begin + 4 * lane + i;
           rows[i] = (p.a_gather && q < t.end) ? p.amap(q) : -1;
         }
+        unsigned long long pw = 0;
         for (int kb = 0; kb < nk; ++kb) {
+          const unsigned long long tp0 = (kTrace && p.trace) ? gtime() : 0;
           mbar_wait(&empty[s], ph ^ 1);
+          if (kTrace && p.trace) pw += gtime() - tp0;
+          if (kTrace && p.trace && lane == 0 && kb == nk - 1 && pit_ < 64) p.trace[(static_cast<size_t>(blockIdx.x) * 64 + pit_) * 8 + 7] = pw;
           uint8_t* sa = smem + s * C::kStage;
           uint8_t* sb = sa + kABytes;
           if constexpr (CG == 2) {
@@ -482,6 +512,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
             // completion counted on the leader's full barrier
             if (lane == 0) {
               const uint32_t fb = full_lead + 8u * s;
+              if (kTrace && (p.dbg_noload & 1)) { mbar_arrive_cl(fb); __syncwarp(); if (++s == C::kStages) { s = 0; ph ^= 1; } continue; }
               mbar_arrive_tx_cl(fb, C::kStage);
               tma_2d_cg2(sa, &p.tmA, fb, kb * BK, t.begin + static_cast<int>(rank) * BM);
               const int nb = n0 + static_cast<int>(rank) * (BN / 2);
@@ -525,6 +556,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
           if constexpr (CG == 2) {  // dense only (host guarantees)
             if (lane == 0) {
               const uint32_t fb = full_lead + 8u * s;
+              if (kTrace && (p.dbg_noload & 1)) { mbar_arrive_cl(fb); __syncwarp(); if (++s == C::kStages) { s = 0; ph ^= 1; } continue; }
               mbar_arrive_tx_cl(fb, C::kStage);
               // both 64-column chunks of A, all chunks of B: one 3D box each
               tma_3d_cg2(sa, &p.tmA, fb, 0, p0, m0 / 64);
@@ -597,20 +629,27 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
       constexpr uint32_t kStageUnits = C::kStage >> 4;
       int s = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
-      for (int w = cluster; w < total; w += n_clusters) {
+      int it_ = 0;
+      for (int w = cluster; w < total; w += n_clusters, ++it_) {
         const SegTile t = p.tiles[w / per_item];
         const int nk = ESTMM ? (t.end - t.begin + BK - 1) / BK : p.K / BK;
+        TRACE(it_, 0);
         if constexpr (CG == 2) mbar_wait_cl(&tempty[acc], aph ^ 1);
         else mbar_wait(&tempty[acc], aph ^ 1);
+        TRACE(it_, 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
+        unsigned long long wsum = 0;
         for (int kb = 0; kb < nk; ++kb) {
+          const unsigned long long tw0 = (kTrace && p.trace) ? gtime() : 0;
           if constexpr (CG == 2) mbar_wait_cl(&full[s], ph);
           else mbar_wait(&full[s], ph);
+          if (kTrace && p.trace) wsum += gtime() - tw0;
           tc_fence_after();
           const uint64_t da = da0 + s * kStageUnits, db = db0 + s * kStageUnits;
 #pragma unroll
           for (int kk = 0; kk < BK / UK; ++kk) {
+            if (kTrace && (p.dbg_noload & 4)) break;
             if constexpr (CG == 2)
               umma_bf16_cg2(d, da + kk * a_step, db + kk * b_step, idesc, (kb | kk) != 0);
             else
@@ -622,6 +661,8 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
         }
         if constexpr (CG == 2) umma_commit_cg2(&tfull[acc]);
         else umma_commit(&tfull[acc]);
+        TRACE(it_, 2);
+        if (kTrace && p.trace && it_ < 64) p.trace[(static_cast<size_t>(blockIdx.x) * 64 + it_) * 8 + 6] = wsum;
         if (++acc == 2) { acc = 0; aph ^= 1; }
       }
     }
@@ -673,6 +714,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
       }
       return p.omap(qq);
     };
+    int ep_it = 0;
     SegTile t_cur = ESTMM ? SegTile{0, 0, 0, 0} : tile_at(cluster);
     int orow_cur = ESTMM ? -1 : orow_of(t_cur);
     for (int w = cluster; w < total; w += n_clusters) {
@@ -707,8 +749,10 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
         if (has_bias && lane * 4 < HB)
           bl = __ldg(reinterpret_cast<const float4*>(p.bias + static_cast<int64_t>(t.expert) * N +
                                                      n0) + lane);
+        if (warp == 2 && lane == 0) TRACE(ep_it, 3);
         if constexpr (CG == 2) mbar_wait_cl(&tfull[acc], aph);
         else mbar_wait(&tfull[acc], aph);
+        if (warp == 2 && lane == 0) TRACE(ep_it, 4);
         tc_fence_after();
         const uint32_t taddr =
             tmem + (static_cast<uint32_t>(lg * 32) << 16) + acc * BN + half * HB;
@@ -858,7 +902,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
               const int rr = i * 4 + lane / 8, cc = lane % 8;
               const int orr = __shfl_sync(0xffffffffu, orow, rr);
               const float4 val = *reinterpret_cast<const float4*>(stg + rr * 128 + ((cc ^ (rr & 7)) * 16));
-              if (orr < 0) continue;
+              if (orr < 0 || (kTrace && (p.dbg_noload & 2))) continue;
               float* o = p.out_f32 + static_cast<int64_t>(orr) * N + n + cc * 4;
               if (p.epi == EPI_WRITE) {
                 *reinterpret_cast<float4*>(o) = val;
@@ -882,6 +926,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
         }
         t_cur = t_nx;
         orow_cur = orow_nx;
+        if (warp == 2 && lane == 0) TRACE(ep_it, 5);
       } else {
         const int mt = rem / p.n_nt, nt = rem % p.n_nt;
         // first output row of this warp (CG = 2: this CTA's half of 256)
@@ -919,13 +964,14 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
           for (int i = 0; i < 8; ++i) {
             const int rr = i * 4 + lane / 8, cc = lane % 8;
             const float4 val = *reinterpret_cast<const float4*>(stg + rr * 128 + ((cc ^ (rr & 7)) * 16));
-            if (m0 + rr >= p.M) continue;
+            if (m0 + rr >= p.M || (kTrace && (p.dbg_noload & 2))) continue;
             float* o = obase + static_cast<int64_t>(m0 + rr) * p.N + n0 + c0 + cc * 4;
             if (split && !empty_seg) red_add_v4(o, val.x, val.y, val.z, val.w);
             else *reinterpret_cast<float4*>(o) = val;
           }
         }
       }
+      ++ep_it;
       if (++acc == 2) { acc = 0; aph ^= 1; }
     }
     if (lane == 0) bulk_wait0();  // this warp's TMA stores are complete
@@ -1000,8 +1046,24 @@ int pick_bn2(int64_t n, bool b_mn) {
 }
 bool bn2_sw64(int bn, bool b_mn) { return b_mn && (bn / 2) % 64 != 0; }
 
+unsigned long long* g_trace = nullptr;
+unsigned long long* trace_buffer_for(const char* label) {
+  const char* want = std::getenv("HXM_TRACE");
+  if (!want || !label || std::strcmp(want, label) != 0) return nullptr;
+  if (!g_trace) {
+    cudaMalloc(&g_trace, 148 * 64 * 8 * sizeof(unsigned long long));
+  }
+  cudaMemset(g_trace, 0, 148 * 64 * 8 * sizeof(unsigned long long));
+  return g_trace;
+}
+
 template <int BN, int MODE, int CG, int ACT = -1>
-hxm_status launch_bn(const UParams& prm, int max_work, cudaStream_t st) {
+hxm_status launch_bn(const UParams& prm_in, int max_work, cudaStream_t st) {
+  UParams prm = prm_in;
+  prm.trace = kTrace ? trace_buffer_for(prm_in.label) : nullptr;
+  // debug decomposition (HXM_DEBUG_NOLOAD bits: 1 = no operand loads, 2 = no
+  // epilogue stores, 4 = no MMAs); results are garbage, timing only
+  if (kTrace) { const char* e = std::getenv("HXM_DEBUG_NOLOAD"); prm.dbg_noload = e ? std::atoi(e) : 0; }
   using C = Cfg<BN, CG, MODE>;
   auto kern = umma_kernel<BN, MODE, CG, ACT>;
   static bool attr_set = false;
@@ -1126,6 +1188,7 @@ hxm_status umma_esmm(const EsmmArgs& a, cudaStream_t st) {
   prm.n_mt = 1;
   prm.tiles = a.tiles;
   prm.n_tiles = a.n_tiles;
+  prm.label = a.label;
   prm.epi = a.epi;
   prm.act = a.act;
   prm.bias = a.bias;
@@ -1220,9 +1283,15 @@ hxm_status umma_estmm(const EstmmArgs& a, cudaStream_t st) {
   prm.tiles = a.tiles;
   prm.n_tiles = a.n_tiles;
   prm.est_out = a.out;
+  prm.label = a.label;
   const int work = a.max_tiles * prm.n_mt * prm.n_nt;
   if (CG == 2) return launch_bn_any<3, 2>(bn, prm, work, st);
   return launch_bn_any<3, 1>(bn, prm, work, st);
 }
 
 }  // namespace hxm
+
+extern "C" void hxm_debug_trace(unsigned long long* out) {
+  if (hxm::g_trace)
+    cudaMemcpy(out, hxm::g_trace, 148 * 64 * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+}
