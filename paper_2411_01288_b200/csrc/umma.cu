@@ -399,10 +399,10 @@ struct Cfg {
   static constexpr int kBBytes = (BN / CG) * BK * 2;
   static constexpr int kStage = kABytes + kBBytes;
   // 227 KB opt-in smem = stages + epilogue staging + 1 KB alignment slack +
-  // barriers.  Staging: 4 KB per epilogue warp (MODE 0 / 3); per column half,
+  // barriers.  Staging: 2 KB per epilogue warp (MODE 0 / 3); per column half,
   // MODE 1 double-buffers its two 8 KB output boxes (32 KB), MODE 2
   // double-buffers its output box and keeps a 3-deep F'(y1) ring (40 KB).
-  static constexpr int kStaging = MODE == 2 ? 81920 : MODE == 1 ? 65536 : kEpiWarps * 4096;
+  static constexpr int kStaging = MODE == 2 ? 81920 : MODE == 1 ? 65536 : kEpiWarps * 2048;
   static constexpr int kBudget = 232448 - 1024 - 256 - kStaging;
   static constexpr int kStages = kBudget / kStage > 8 ? 8 : kBudget / kStage;
   static constexpr int kSmem = kStages * kStage + kStaging + 1024 /*align*/ + 256 /*barriers*/;
@@ -678,7 +678,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
     constexpr int HB = BN / 2;
     const int lg = warp & 3;
     const int half = (warp - 2) / 4;
-    uint8_t* stg = staging + (warp - 2) * 4096;
+    uint8_t* stg = staging + (warp - 2) * 2048;
     // accumulator drained by this warp: arrive on the (leader's) tempty
     auto release_acc = [&](int a) {
       if constexpr (CG == 2) mbar_arrive_cl(tempty_lead + 8u * a);
@@ -890,28 +890,36 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
             }
             ++dchunk;
           } else {
-            // fp32 rows scattered to token order: stage 4 KB (32 x 128 B)
-            __syncwarp();
+            // fp32 rows scattered to token order: two 16-column halves through
+            // a 2 KB per-warp staging tile (32 rows x 64 B, 16-byte chunks
+            // XOR-swizzled by (row >> 1) & 3: conflict-free both ways), so a
+            // store / reduction instruction covers 8 row segments of 64 B
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              *reinterpret_cast<float4*>(stg + lane * 128 + ((j ^ (lane & 7)) * 16)) =
-                  make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-            __syncwarp();
+            for (int h2 = 0; h2 < 2; ++h2) {
+              __syncwarp();
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int rr = i * 4 + lane / 8, cc = lane % 8;
-              const int orr = __shfl_sync(0xffffffffu, orow, rr);
-              const float4 val = *reinterpret_cast<const float4*>(stg + rr * 128 + ((cc ^ (rr & 7)) * 16));
-              if (orr < 0 || (kTrace && (p.dbg_noload & 2))) continue;
-              float* o = p.out_f32 + static_cast<int64_t>(orr) * N + n + cc * 4;
-              if (p.epi == EPI_WRITE) {
-                *reinterpret_cast<float4*>(o) = val;
-              } else if (p.epi == EPI_ACCUM) {
-                float4 c = *reinterpret_cast<float4*>(o);
-                c.x += val.x; c.y += val.y; c.z += val.z; c.w += val.w;
-                *reinterpret_cast<float4*>(o) = c;
-              } else {
-                red_add_v4(o, val.x, val.y, val.z, val.w);
+              for (int j = 0; j < 4; ++j)
+                *reinterpret_cast<float4*>(stg + lane * 64 + ((j ^ ((lane >> 1) & 3)) * 16)) =
+                    make_float4(v[16 * h2 + 4 * j], v[16 * h2 + 4 * j + 1], v[16 * h2 + 4 * j + 2],
+                                v[16 * h2 + 4 * j + 3]);
+              __syncwarp();
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int rr = i * 8 + lane / 4, cc = lane % 4;
+                const int orr = __shfl_sync(0xffffffffu, orow, rr);
+                const float4 val =
+                    *reinterpret_cast<const float4*>(stg + rr * 64 + ((cc ^ ((rr >> 1) & 3)) * 16));
+                if (orr < 0 || (kTrace && (p.dbg_noload & 2))) continue;
+                float* o = p.out_f32 + static_cast<int64_t>(orr) * N + n + 16 * h2 + cc * 4;
+                if (p.epi == EPI_WRITE) {
+                  *reinterpret_cast<float4*>(o) = val;
+                } else if (p.epi == EPI_ACCUM) {
+                  float4 c = *reinterpret_cast<float4*>(o);
+                  c.x += val.x; c.y += val.y; c.z += val.z; c.w += val.w;
+                  *reinterpret_cast<float4*>(o) = c;
+                } else {
+                  red_add_v4(o, val.x, val.y, val.z, val.w);
+                }
               }
             }
           }
@@ -954,20 +962,25 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
             __syncwarp();
             if (lane == 0) release_acc(acc);
           }
-          __syncwarp();
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            *reinterpret_cast<uint4*>(stg + lane * 128 + ((j ^ (lane & 7)) * 16)) =
-                make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
-          __syncwarp();
+          for (int h2 = 0; h2 < 2; ++h2) {
+            __syncwarp();
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int rr = i * 4 + lane / 8, cc = lane % 8;
-            const float4 val = *reinterpret_cast<const float4*>(stg + rr * 128 + ((cc ^ (rr & 7)) * 16));
-            if (m0 + rr >= p.M || (kTrace && (p.dbg_noload & 2))) continue;
-            float* o = obase + static_cast<int64_t>(m0 + rr) * p.N + n0 + c0 + cc * 4;
-            if (split && !empty_seg) red_add_v4(o, val.x, val.y, val.z, val.w);
-            else *reinterpret_cast<float4*>(o) = val;
+            for (int j = 0; j < 4; ++j)
+              *reinterpret_cast<uint4*>(stg + lane * 64 + ((j ^ ((lane >> 1) & 3)) * 16)) =
+                  make_uint4(r[16 * h2 + 4 * j], r[16 * h2 + 4 * j + 1], r[16 * h2 + 4 * j + 2],
+                             r[16 * h2 + 4 * j + 3]);
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int rr = i * 8 + lane / 4, cc = lane % 4;
+              const float4 val =
+                  *reinterpret_cast<const float4*>(stg + rr * 64 + ((cc ^ ((rr >> 1) & 3)) * 16));
+              if (m0 + rr >= p.M || (kTrace && (p.dbg_noload & 2))) continue;
+              float* o = obase + static_cast<int64_t>(m0 + rr) * p.N + n0 + c0 + 16 * h2 + cc * 4;
+              if (split && !empty_seg) red_add_v4(o, val.x, val.y, val.z, val.w);
+              else *reinterpret_cast<float4*>(o) = val;
+            }
           }
         }
       }
