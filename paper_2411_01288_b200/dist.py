@@ -101,32 +101,56 @@ def unshard_params(s: ShardedParams):
 
 
 class PipelineSharedCache:
-    """One full-layer parameter buffer per device (dist_sim.hpp:60-82)."""
+    """Full-layer parameter buffers per device (dist_sim.hpp:60-82).
 
-    def __init__(self, capacity_elements: int):
+    ``slots=1`` is the reference's cache: at most one layer resident, fill()
+    replaces it.  The multi-layer pipeline uses ``slots=2`` (current layer +
+    the one being prefetched by the side-stream all-gather): fill() replaces
+    the least recently filled slot.  ``capacity_elements`` bounds one slot
+    (CacheError on overflow or on reading a layer that is not resident)."""
+
+    def __init__(self, capacity_elements: int, slots: int = 1):
+        if slots < 1:
+            raise ValueError("PipelineSharedCache: slots must be >= 1")
         self.capacity = capacity_elements
-        self._params = None
-        self.layer = -1
+        self.slots = slots
+        self._res = []  # [(layer_id, params)], oldest first
         self.fills = 0
+
+    @property
+    def layer(self) -> int:
+        return self._res[-1][0] if self._res else -1
 
     def fill(self, layer_id: int, params) -> None:
         n = params.param_elements()
         if n > self.capacity:
             raise CacheError(f"pipeline-shared cache: layer parameters ({n} elements) exceed "
                              f"cache capacity ({self.capacity})")
-        self._params, self.layer = params, layer_id
+        self._res = [r for r in self._res if r[0] != layer_id]
+        if len(self._res) >= self.slots:
+            self._res.pop(0)
+        self._res.append((layer_id, params))
         self.fills += 1
 
     def clear(self) -> None:
-        self._params, self.layer = None, -1
+        self._res = []
 
     def filled(self) -> bool:
-        return self._params is not None
+        return bool(self._res)
 
-    def params(self):
-        if self._params is None:
+    def resident(self) -> List[int]:
+        return [r[0] for r in self._res]
+
+    def params(self, layer_id: Optional[int] = None):
+        if not self._res:
             raise CacheError("pipeline-shared cache: read before fill")
-        return self._params
+        if layer_id is None:
+            return self._res[-1][1]
+        for lid, p in self._res:
+            if lid == layer_id:
+                return p
+        raise CacheError(f"pipeline-shared cache: layer {layer_id} is not resident "
+                         f"(resident: {self.resident()})")
 
 
 # ------------------------------------------------------------- compute ----
@@ -263,39 +287,9 @@ def data_centric_step(local_x, local_assign, local_gy, shard: ParamShard, b2, hi
     p = cache.params()
     y, stash = compute.forward(local_x, p, local_assign, True)
     g = compute.backward(stash, p, local_gy)
-    if grad_reduce == "all_reduce":
-        for t in (g.gw1, g.gb1, g.gw2, g.gb2):
-            dist.all_reduce(t, group=group)
-        log.append("grad_all_reduce")
-        return DistStepResult(y, g, log)
-    # reduce-scatter along H to the shard owners (half the traffic)
-    P, r = _ws(group), _rank(group)
-    off = shard.hidden_offset
-    h = hidden_sizes[r]
-    hmax = max(hidden_sizes)
-    from .moe_layer import MoeGrads
-    outs = []
-    for t, dim in ((g.gw1, 2), (g.gb1, 1), (g.gw2, 1)):
-        parts = []
-        o = 0
-        for hr in hidden_sizes:
-            sl = t.narrow(dim, o, hr)
-            if hr < hmax:
-                shp = list(sl.shape)
-                shp[dim] = hmax - hr
-                sl = torch.cat([sl, torch.zeros(shp, dtype=t.dtype, device=t.device)], dim=dim)
-            parts.append(sl.movedim(dim, 0).contiguous())
-            o += hr
-        inp = torch.cat(parts)  # [P*hmax, ...] rank-major
-        out = torch.empty_like(parts[0])
-        dist.reduce_scatter_tensor(out, inp, group=group)
-        outs.append(out[:h].movedim(0, dim).contiguous())
-    dist.reduce(g.gb2, dst=dist.get_global_rank(group, 0) if group is not None else 0,
-                group=group)
-    log.append("grad_reduce_scatter")
-    del off
-    return DistStepResult(y, MoeGrads(outs[0], outs[1], outs[2], g.gb2 if r == 0 else None,
-                                      g.gx), log)
+    g = _reduce_param_grads(g, shard, hidden_sizes, group, grad_reduce)
+    log.append("grad_all_reduce" if grad_reduce == "all_reduce" else "grad_reduce_scatter")
+    return DistStepResult(y, g, log)
 
 
 def model_centric_step(local_x, local_assign, local_gy, shard: ParamShard, b2, activation: str,
@@ -398,6 +392,126 @@ class DataCentricRunner:
         if g.gb2 is not None:
             dist.all_reduce(g.gb2, group=self.group)
         return self.runner.y
+
+
+# ------------------------------------------- multi-layer data-centric ------
+@dataclass
+class PipelineResult:
+    y: torch.Tensor            # this rank's output rows of the last layer
+    grads: List[object]        # per layer: gw1, gb1, gw2, gb2, gx (gx: this rank's rows)
+    gathers: int               # parameter all-gathers issued (2L - 1)
+    log: List[str] = field(default_factory=list)
+
+
+def data_centric_pipeline(local_x, local_assigns: Sequence, local_gy,
+                          shards: Sequence[ParamShard], b2s: Sequence, hidden_sizes,
+                          activation: str, cache: PipelineSharedCache, compute: LocalCompute,
+                          group=None, grad_reduce: str = "all_reduce",
+                          side_stream: Optional[torch.cuda.Stream] = None) -> PipelineResult:
+    """L stacked MoE layers (d_in == d_out), data-centric TP along H, with
+    the pipeline-shared cache schedule of dist_sim.cpp:410-433 executed for
+    real instead of accounted: forward all-gathers layer l + 1's shards (on
+    ``side_stream`` with NCCL, overlapping layer l's compute) while layer l
+    runs from the cache; backward starts from the still-resident last layer
+    (no re-gather) and prefetches layer l - 1 while layer l runs -- 2L - 1
+    gathers in total (test_dist_sim.cpp:329-336).  Layer l + 1's input is
+    layer l's output cast to the input dtype; layer l's g_y is layer l + 1's
+    g_x, likewise.  The cache needs two slots (current + prefetch).
+
+    Returns the last layer's local y and every layer's gradients reduced as
+    in data_centric_step (all_reduce: full tensors; reduce_scatter: each
+    rank's H-slices, gb2 on rank 0)."""
+    L = len(shards)
+    if L < 1 or len(local_assigns) != L or len(b2s) != L:
+        raise ValueError("data_centric_pipeline: one shard, routing and b2 per layer")
+    if cache.slots < 2 and L > 1:
+        raise CacheError("data_centric_pipeline: the prefetching schedule needs a two-slot "
+                         "pipeline-shared cache")
+    log: List[str] = []
+    gathers = 0
+    cur = torch.cuda.current_stream() if side_stream is not None else None
+
+    def gather(l):
+        nonlocal gathers
+        gathers += 1
+        log.append(f"param_gather_layer{l}")
+        p = gather_params(shards[l], b2s[l], hidden_sizes, activation, group, side_stream)
+        ev = None
+        if side_stream is not None:
+            ev = torch.cuda.Event()
+            ev.record(side_stream)
+        return l, p, ev
+
+    def land(pending):
+        l, p, ev = pending
+        if ev is not None:
+            cur.wait_event(ev)
+        cache.fill(l, p)
+        return p
+
+    # ---- forward: layer l computes while layer l + 1 is gathered ----------
+    stashes = []
+    x = local_x
+    pending = gather(0)
+    for l in range(L):
+        p = land(pending)
+        if l + 1 < L:
+            if side_stream is not None:
+                side_stream.wait_stream(cur)  # the slot being refilled is idle
+            pending = gather(l + 1)
+        y, stash = compute.forward(x, p, local_assigns[l], True)
+        stashes.append(stash)
+        log.append(f"forward_layer{l}")
+        x = y.to(local_x.dtype) if l + 1 < L else y
+    y_out = x
+    # ---- backward: the last layer is still resident -----------------------
+    grads = [None] * L
+    g_in = local_gy
+    pending = None
+    for l in reversed(range(L)):
+        if l == L - 1:
+            p = cache.params(l)
+            log.append(f"reuse_cached_layer{l}")
+        else:
+            p = land(pending)
+        if l > 0:
+            if side_stream is not None:
+                side_stream.wait_stream(cur)
+            pending = gather(l - 1)
+        g = compute.backward(stashes[l], p, g_in)
+        log.append(f"backward_layer{l}")
+        grads[l] = _reduce_param_grads(g, shards[l], hidden_sizes, group, grad_reduce)
+        log.append(f"grad_{grad_reduce}_layer{l}")
+        if l > 0:
+            g_in = g.gx.to(local_gy.dtype)
+    return PipelineResult(y_out, grads, gathers, log)
+
+
+def _reduce_param_grads(g, shard: ParamShard, hidden_sizes, group, how: str):
+    from .moe_layer import MoeGrads
+    if how == "all_reduce":
+        for t in (g.gw1, g.gb1, g.gw2, g.gb2):
+            dist.all_reduce(t, group=group)
+        return g
+    r = _rank(group)
+    h, hmax = hidden_sizes[r], max(hidden_sizes)
+    outs = []
+    for t, dim in ((g.gw1, 2), (g.gb1, 1), (g.gw2, 1)):
+        parts, o = [], 0
+        for hr in hidden_sizes:
+            sl = t.narrow(dim, o, hr)
+            if hr < hmax:
+                shp = list(sl.shape)
+                shp[dim] = hmax - hr
+                sl = torch.cat([sl, torch.zeros(shp, dtype=t.dtype, device=t.device)], dim=dim)
+            parts.append(sl.movedim(dim, 0).contiguous())
+            o += hr
+        out = torch.empty_like(parts[0])
+        dist.reduce_scatter_tensor(out, torch.cat(parts), group=group)
+        outs.append(out[:h].movedim(0, dim).contiguous())
+    dist.reduce(g.gb2, dst=dist.get_global_rank(group, 0) if group is not None else 0,
+                group=group)
+    return MoeGrads(outs[0], outs[1], outs[2], g.gb2 if r == 0 else None, g.gx)
 
 
 def _reduce_rows(t: torch.Tensor, counts: Sequence[int], group, how: str) -> torch.Tensor:

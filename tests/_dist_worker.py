@@ -125,3 +125,71 @@ def run(rank, world, port, batches, hidden_alloc, out_q):
         out_q.put((rank, errs))
     finally:
         dist.destroy_process_group()
+
+
+def run_pipeline(rank, world, port, batches, hidden_alloc, n_layers, out_q):
+    """Multi-layer data-centric pipeline (dist_sim.cpp:410-433) vs the
+    single-device sequential stack: y, every layer's gradients, 2L - 1 gathers."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2411_01288_b200 import dist as D
+        comp = oracle_compute()
+        total = sum(batches)
+        H = sum(hidden_alloc)
+        layers, assigns = [], []
+        x = gy = None
+        for l in range(n_layers):
+            p, xl, a, gyl = problem(777 + 13 * l, total, din=5, hid=H, dout=5)
+            layers.append(p)
+            assigns.append(a)
+            if l == 0:
+                x, gy = xl, gyl
+        # single-device sequential reference
+        stashes, h = [], x
+        for l in range(n_layers):
+            h, st = comp.forward(h, layers[l], assigns[l], True)
+            stashes.append(st)
+        y_ref = h
+        g_ref = [None] * n_layers
+        g = gy
+        for l in reversed(range(n_layers)):
+            g_ref[l] = comp.backward(stashes[l], layers[l], g)
+            g = g_ref[l].gx
+        lo = sum(batches[:rank])
+        hi = lo + batches[rank]
+        sps = [D.shard_params(p, hidden_alloc) for p in layers]
+        shards = [sp.shards[rank] for sp in sps]
+        b2s = [sp.b2 if rank == 0 else None for sp in sps]
+        la = [a[:, lo:hi] for a in assigns]
+        errs = {}
+        for how in ("all_reduce", "reduce_scatter"):
+            cache = D.PipelineSharedCache(sps[0].full_param_elements(), slots=2)
+            r = D.data_centric_pipeline(x[lo:hi], la, gy[lo:hi], shards, b2s, hidden_alloc,
+                                        "gelu", cache, comp, grad_reduce=how)
+            errs[f"{how}_gathers"] = 0.0 if r.gathers == 2 * n_layers - 1 else 1.0
+            errs[f"{how}_y"] = scaled(r.y, y_ref[lo:hi])
+            off, hh = shards[0].hidden_offset, hidden_alloc[rank]
+            for l in range(n_layers):
+                gl, gr = r.grads[l], g_ref[l]
+                if how == "all_reduce":
+                    for key in ("gw1", "gb1", "gw2", "gb2"):
+                        errs[f"{how}_{key}{l}"] = scaled(getattr(gl, key), getattr(gr, key))
+                else:
+                    errs[f"{how}_gw1{l}"] = scaled(gl.gw1, gr.gw1[:, :, off:off + hh])
+                    errs[f"{how}_gb1{l}"] = scaled(gl.gb1, gr.gb1[:, off:off + hh])
+                    errs[f"{how}_gw2{l}"] = scaled(gl.gw2, gr.gw2[:, off:off + hh, :])
+                    if rank == 0:
+                        errs[f"{how}_gb2{l}"] = scaled(gl.gb2, gr.gb2)
+                errs[f"{how}_gx{l}"] = scaled(gl.gx, gr.gx[lo:hi])
+        # the prefetching schedule refuses a one-slot cache
+        try:
+            D.data_centric_pipeline(x[lo:hi], la, gy[lo:hi], shards, b2s, hidden_alloc, "gelu",
+                                    D.PipelineSharedCache(sps[0].full_param_elements()), comp)
+            errs["one_slot_rejected"] = 1.0 if n_layers > 1 else 0.0
+        except D.CacheError:
+            errs["one_slot_rejected"] = 0.0
+        out_q.put((rank, errs))
+    finally:
+        dist.destroy_process_group()

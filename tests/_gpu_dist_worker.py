@@ -66,6 +66,35 @@ def main():
     errs["mc_gw2"] = scaled(res.grads.gw2, gref.gw2[:, off:off + h, :])
     if r == 0:
         errs["mc_gb2"] = scaled(res.grads.gb2, gref.gb2)
+    # multi-layer pipeline (two-slot cache, NCCL gathers on a side stream)
+    # vs the single-GPU sequential stack of the same layers
+    L = 3
+    layers = [p] + [H.make_random_params(E, Dm, Hd, Dm, "gelu", seed=20 + l, n_tokens=N)[0]
+                    for l in range(1, L)]
+    routs = [rt] + [H.synthesize_routing(N, E, k, "uniform", 30 + l) for l in range(1, L)]
+    hcur, stashes = x, []
+    for l in range(L):
+        f = H.moe_forward(hcur, layers[l], routs[l])
+        stashes.append(f.stash)
+        hcur = f.y.to(torch.bfloat16) if l + 1 < L else f.y
+    y_seq = hcur
+    g_seq, gcur = [None] * L, gy
+    for l in reversed(range(L)):
+        g_seq[l] = H.moe_backward(stashes[l], layers[l], gcur)
+        gcur = g_seq[l].gx.to(torch.bfloat16)
+    sps = [D.shard_params(q, D.even_split(Hd, P)) for q in layers]
+    cache2 = D.PipelineSharedCache(sps[0].full_param_elements(), slots=2)
+    pr = D.data_centric_pipeline(lx, [rr.to_device()[:, lo:hi].contiguous() for rr in routs], lgy,
+                                 [s.shards[r] for s in sps],
+                                 [s.b2 if r == 0 else None for s in sps], sps[0].hidden_sizes,
+                                 "gelu", cache2, comp, side_stream=torch.cuda.Stream())
+    errs["pipe_gathers"] = 0.0 if pr.gathers == 2 * L - 1 else 1.0
+    errs["pipe_y"] = scaled(pr.y, y_seq[lo:hi])
+    for l in range(L):
+        errs[f"pipe_gw1_{l}"] = scaled(pr.grads[l].gw1, g_seq[l].gw1)
+        errs[f"pipe_gw2_{l}"] = scaled(pr.grads[l].gw2, g_seq[l].gw2)
+        errs[f"pipe_gb1_{l}"] = scaled(pr.grads[l].gb1, g_seq[l].gb1)
+        errs[f"pipe_gx_{l}"] = scaled(pr.grads[l].gx, g_seq[l].gx[lo:hi])
     bad = {k_: v for k_, v in errs.items() if not v <= 2e-2}
     print(f"rank {r}: worst {max(errs.values()):.2e}", "FAIL" if bad else "OK", bad or "")
     dist.destroy_process_group()

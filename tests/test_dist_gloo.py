@@ -64,3 +64,50 @@ def test_shard_params_errors():
         c.params()
     with pytest.raises(CacheError):
         c.fill(0, p)
+
+
+@pytest.mark.parametrize("batches,hidden_alloc,n_layers", [
+    ([9, 6], [7, 5], 3),
+    ([5, 5, 4, 6], [4, 4, 3, 1], 2),
+    ([8, 8], [6, 6], 1),
+])
+def test_pipeline_matches_sequential_stack(batches, hidden_alloc, n_layers):
+    """dist_sim.cpp:410-433 executed for real: L layers through the two-slot
+    pipeline-shared cache reproduce the single-device sequential stack at
+    1e-10 and issue 2L - 1 parameter gathers (test_dist_sim.cpp:329-336)."""
+    world = len(batches)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=W.run_pipeline,
+                         args=(r, world, port, batches, hidden_alloc, n_layers, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = {}
+    for _ in range(world):
+        rank, errs = q.get(timeout=180)
+        results[rank] = errs
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, errs in results.items():
+        bad = {k: v for k, v in errs.items() if not v <= 1e-10}
+        assert not bad, (rank, bad)
+
+
+def test_two_slot_cache_eviction():
+    import torch
+    from paper_2411_01288_b200 import CacheError, MoeLayerParams
+    from paper_2411_01288_b200 import dist as D
+    p = MoeLayerParams(torch.zeros(2, 3, 4), torch.zeros(2, 4), torch.zeros(2, 4, 3),
+                       torch.zeros(2, 3))
+    c = D.PipelineSharedCache(p.param_elements(), slots=2)
+    c.fill(0, p)
+    c.fill(1, p)
+    assert c.resident() == [0, 1] and c.layer == 1
+    c.fill(2, p)  # evicts layer 0 (least recently filled)
+    assert c.resident() == [1, 2]
+    with pytest.raises(CacheError):
+        c.params(0)
+    assert c.params(1) is p and c.fills == 3
