@@ -215,6 +215,17 @@ def run_reference(args, cfg, rank, ws):
     print(json.dumps(out))
 
 
+def _redundancy(args, r, D, Hd):
+    """count_redundancy (gemm_oracle.cpp:251-285) of the baseline run."""
+    from paper_2411_01288_b200 import conventional as CV
+    rep = CV.count_redundancy(r, D, Hd, D, args.capacity_factor)
+    out = dict(rep.__dict__)
+    out["capacity_factor"] = args.capacity_factor
+    out["device_capacity_rows"] = CV.capacity_rows(r.n_tokens, r.n_experts, r.k,
+                                                   args.capacity_factor)
+    return out
+
+
 def run_ours(args, cfg, rank, ws, local):
     import numpy as np
     import torch
@@ -261,7 +272,11 @@ def run_ours(args, cfg, rank, ws, local):
         torch.cuda.synchronize()
         y_out = mc_out["y"]
     elif mode == "single":
-        run = LayerRunner(p, N, k, dev, dtype)
+        cap = 0
+        if args.capacity_factor > 0:
+            from paper_2411_01288_b200.moe_layer import capacity_rows
+            cap = capacity_rows(N, E, k, args.capacity_factor)
+        run = LayerRunner(p, N, k, dev, dtype, capacity=cap)
         # warm-up (also validates routing once)
         status = torch.zeros(1, dtype=torch.int32, device=dev)
         run.forward(x, a, status=status)
@@ -438,6 +453,9 @@ def run_ours(args, cfg, rank, ws, local):
         "config": {"workload": args.config, "desc": cfg["desc"], "E": E, "k": k, "d": D,
                    "ffn": Hd, "tokens_per_gpu": N, "routing": cfg["dist"],
                    "parallelism": f"{mode}_tp{ws}" if mode != "single" else "single",
+                   "formulation": (f"conventional dispatch/combine, capacity factor "
+                                   f"{args.capacity_factor}") if args.capacity_factor > 0
+                   else "expert-specific (no padding, no dropping)",
                    "cuda_graph": use_graph,
                    "kernel_times": "second K-step pass of the same step captured with per-kernel "
                                    "event nodes" if use_graph else "events around each launch",
@@ -450,6 +468,7 @@ def run_ours(args, cfg, rank, ws, local):
         "e2e": {"value": e2e_val, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps},
         "gpu_launches": int(launches),
+        "redundancy": _redundancy(args, r, D, Hd) if args.capacity_factor > 0 else None,
         "clocks": clocks.summary(),
     }
     print(json.dumps(out))
@@ -468,6 +487,9 @@ def main():
                     help="auto: single GPU at N=1, data-centric TP along H at N>1")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the step eagerly instead of replaying its CUDA graph")
+    ap.add_argument("--capacity-factor", type=float, default=0.0,
+                    help="> 0: the conventional dispatch/combine baseline with this capacity "
+                         "factor (gemm_oracle.cpp) instead of the expert-specific path")
     ap.add_argument("--shape", default=None,
                     help="experiment override E,k,D,H,N of the chosen config (not a bench line)")
     args = ap.parse_args()

@@ -152,7 +152,15 @@ typedef struct hxm_layer_desc {
   int32_t dtype;      /* hxm_dtype                           */
   int32_t add_b2;     /* 1: add b2 (rank 0 under model-centric TP,
                          dist_sim.cpp:486); 0: skip b2 / gb2 */
-  int32_t reserved;
+  int32_t capacity;   /* 0: expert-specific (every routed slot computed,
+                         nothing padded or dropped).  > 0: the conventional
+                         dispatch/combine baseline (gemm_oracle.cpp:75-139,
+                         count_redundancy gemm_oracle.cpp:251-285): every
+                         expert computes exactly `capacity` rows -- all k*N
+                         (token, choice) slots compete, lowest slot ids are
+                         kept, overflow is dropped (zero contribution),
+                         shortfall rows are zero padding that the GEMMs
+                         process.  Must be a multiple of 64. */
 } hxm_layer_desc;
 
 size_t hxm_layer_workspace_bytes(const hxm_layer_desc* desc);
@@ -184,8 +192,10 @@ hxm_status hxm_moe_stash_export(const hxm_layer_desc* desc,
                                 const void* workspace, int64_t choice,
                                 float* dact, float* y2, hxm_stream_t stream);
 
-/* Algorithmic work counters of the last layer call (OpStats, es_ops.hpp:17-24):
- * MACs on real tokens only = k*N*(D_i*H + H*D_o) per direction. */
+/* Algorithmic work counters (OpStats, es_ops.hpp:17-24), MACs per direction:
+ * expert-specific (capacity 0) = k*N*(D_i*H + H*D_o) on real tokens only;
+ * conventional baseline = E*capacity*(D_i*H + H*D_o), padding included
+ * (count_redundancy's token_macs_oracle, gemm_oracle.cpp:281-282). */
 uint64_t hxm_layer_forward_macs(const hxm_layer_desc* desc);
 
 /* ------------------------------------------------------------------------

@@ -36,7 +36,7 @@ class LayerDesc(C.Structure):
     _fields_ = [("n_tokens", C.c_int64), ("n_experts", C.c_int64), ("k", C.c_int64),
                 ("d_in", C.c_int64), ("hidden", C.c_int64), ("d_out", C.c_int64),
                 ("activation", C.c_int32), ("dtype", C.c_int32), ("add_b2", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("capacity", C.c_int32)]
 
 
 _p = C.c_void_p

@@ -61,7 +61,10 @@ size_t esize(int32_t dt) { return dt == HXM_BF16 ? 2 : 4; }
 LayerWs carve(Arena& ar, const hxm_layer_desc& d) {
   LayerWs w{};
   const int64_t slots = d.k * d.n_tokens;
-  w.bound = slots + d.n_experts * (kSortedBlk - 1);
+  // expert-specific: every slot plus < 64 pad rows per expert; conventional
+  // baseline: exactly `capacity` rows per expert
+  w.bound = d.capacity > 0 ? d.n_experts * static_cast<int64_t>(d.capacity)
+                           : slots + d.n_experts * (kSortedBlk - 1);
   const hxm_dtype dt = static_cast<hxm_dtype>(d.dtype);
   // all four layer GEMMs share one tile table, so they must agree on the
   // tile rows: 128 (tcgen05) when every shape is TMA-describable
@@ -118,6 +121,10 @@ hxm_status check_desc(const hxm_layer_desc* d) {
     return shape_error("moe layer: extents must be positive");
   if (d->k * d->n_tokens + d->n_experts * kSortedBlk > 0x7fffffffLL)
     return invalid_arg("moe layer: k*N exceeds int32 slot range");
+  if (d->capacity < 0 || d->capacity % kSortedBlk != 0)
+    return invalid_arg("moe layer: capacity must be 0 or a positive multiple of 64");
+  if (static_cast<int64_t>(d->capacity) * d->n_experts > 0x7fffffffLL)
+    return invalid_arg("moe layer: capacity * E exceeds int32 row range");
   return HXM_OK;
 }
 
@@ -153,8 +160,11 @@ size_t hxm_layer_workspace_bytes(const hxm_layer_desc* d) {
 }
 
 uint64_t hxm_layer_forward_macs(const hxm_layer_desc* d) {
-  return static_cast<uint64_t>(d->k) * d->n_tokens *
-         (d->d_in * d->hidden + d->hidden * d->d_out);
+  // rows the GEMMs compute per weight: every routed slot (expert-specific)
+  // or E x capacity (conventional baseline, padding included)
+  const uint64_t rows = d->capacity > 0 ? static_cast<uint64_t>(d->n_experts) * d->capacity
+                                        : static_cast<uint64_t>(d->k) * d->n_tokens;
+  return rows * (d->d_in * d->hidden + d->hidden * d->d_out);
 }
 
 hxm_status hxm_moe_forward(const hxm_layer_desc* d, const void* x, const void* w1,
@@ -183,6 +193,7 @@ hxm_status hxm_moe_forward(const hxm_layer_desc* d, const void* x, const void* w
     pro.k = static_cast<int>(d->k);
     pro.E = static_cast<int>(E);
     pro.blk = kSortedBlk;
+    pro.capacity = d->capacity;
     pro.v = w.v;
     pro.idx = w.idx;
     pro.s0 = {w.rows_a, 0, w.tiles_a, w.tiles_a_off, w.n_tiles_a};

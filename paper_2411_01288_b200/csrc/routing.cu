@@ -78,7 +78,7 @@ __global__ void scan_experts(const int32_t* __restrict__ cnt, int E, int nchunks
 // Exclusive scan of padded segment sizes into smem idx[0..E].
 template <class IdxT>
 __device__ void block_idx(const int32_t* __restrict__ total, int E, int64_t blk,
-                          IdxT* sidx) {
+                          IdxT* sidx, int64_t capacity = 0) {
   using Scan = cub::BlockScan<int64_t, kThreads>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int64_t carry;
@@ -87,7 +87,9 @@ __device__ void block_idx(const int32_t* __restrict__ total, int E, int64_t blk,
   for (int e0 = 0; e0 < E; e0 += kThreads) {
     const int e = e0 + threadIdx.x;
     int64_t padded = 0;
-    if (e < E) padded = blk * ((static_cast<int64_t>(total[e]) + blk - 1) / blk);
+    if (e < E)
+      padded = capacity > 0 ? capacity  // conventional: fixed per-expert buffers
+                            : blk * ((static_cast<int64_t>(total[e]) + blk - 1) / blk);
     int64_t excl, agg;
     Scan(tmp).ExclusiveSum(padded, excl, agg);
     if (e < E) sidx[e] = static_cast<IdxT>(carry + excl);
@@ -380,11 +382,13 @@ __global__ void __launch_bounds__(kThreads) fwd_prologue(FwdPrologue a) {
   int32_t* sidx = reinterpret_cast<int32_t*>(smem_raw);  // E+1
   {
     int32_t* cursor = sidx + align_up(E + 1, 4);  // [kWarps][E]
-    block_idx<int32_t>(a.total, E, a.blk, sidx);
+    block_idx<int32_t>(a.total, E, a.blk, sidx, a.capacity);
     if (blockIdx.x == 0)
       for (int e = threadIdx.x; e <= E; e += kThreads) a.idx[e] = sidx[e];
     for (int e = gwarp; e < E; e += nwarps) {
-      const int64_t s0 = static_cast<int64_t>(sidx[e]) + a.total[e];
+      const int64_t tot = a.total[e];
+      const int64_t kept = (a.capacity > 0 && tot > a.capacity) ? a.capacity : tot;
+      const int64_t s0 = static_cast<int64_t>(sidx[e]) + kept;
       for (int64_t p = s0 + lane; p < sidx[e + 1]; p += 32) a.v[p] = -1;
     }
     int32_t* cur = cursor + warp * E;
@@ -399,7 +403,12 @@ __global__ void __launch_bounds__(kThreads) fwd_prologue(FwdPrologue a) {
         int e = t < t1 ? a.a[t] : -1;
         if (e >= E) e = -1;  // out of range: reported in phase 1, skipped
         const unsigned peers = __match_any_sync(0xffffffffu, e);
-        if (e >= 0) a.v[cur[e] + __popc(peers & lt)] = static_cast<int32_t>(t);
+        if (e >= 0) {
+          const int64_t pos = cur[e] + __popc(peers & lt);
+          // conventional baseline: slots past the expert's capacity are
+          // dropped (keep-lowest slot ids, gemm_oracle.cpp:91-94)
+          if (a.capacity <= 0 || pos - sidx[e] < a.capacity) a.v[pos] = static_cast<int32_t>(t);
+        }
         __syncwarp();
         if (e >= 0 && (__ffs(peers) - 1) == lane) cur[e] += __popc(peers);
         __syncwarp();

@@ -42,6 +42,7 @@ struct FwdPrologue {
   int64_t n_slots, n_tok;
   int k, E;
   int64_t blk;
+  int64_t capacity;  // > 0: fixed per-expert segments, overflow dropped
   int32_t* v;
   int32_t* idx;
   TileSpec s0, s1, s2;

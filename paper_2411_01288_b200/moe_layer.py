@@ -8,6 +8,8 @@ All compute is the C ABI hxm_moe_forward / hxm_moe_backward (layer.cu).
 """
 from __future__ import annotations
 
+import math
+
 import ctypes as C
 from dataclasses import dataclass
 from typing import Optional
@@ -114,14 +116,27 @@ def _dtype_code(t):
 
 
 def make_desc(n_tokens, n_experts, k, d_in, hidden, d_out, activation="gelu",
-              dtype=torch.bfloat16, add_b2=True) -> LayerDesc:
+              dtype=torch.bfloat16, add_b2=True, capacity: int = 0) -> LayerDesc:
+    """capacity > 0 selects the conventional dispatch/combine baseline
+    (per-expert buffers of exactly ``capacity`` rows; see capacity_rows())."""
     d = LayerDesc()
     d.n_tokens, d.n_experts, d.k = n_tokens, n_experts, k
     d.d_in, d.hidden, d.d_out = d_in, hidden, d_out
     d.activation = ACT[activation]
     d.dtype = _lib.HXM_BF16 if dtype == torch.bfloat16 else _lib.HXM_F32
     d.add_b2 = int(add_b2)
+    d.capacity = int(capacity)
     return d
+
+
+def capacity_rows(n_tokens: int, n_experts: int, k: int, capacity_factor: float) -> int:
+    """Per-expert rows of the conventional formulation: ceil(cf * k * N / E)
+    (gemm_oracle.cpp:268-271), rounded up to the 64-row segment granule of
+    the device layout (the extra rows are padding too)."""
+    if capacity_factor <= 0.0:
+        raise ValueError("count_redundancy: capacity_factor must be > 0")
+    c = int(math.ceil(capacity_factor * k * n_tokens / n_experts))
+    return max(64, (c + 63) // 64 * 64)
 
 
 def layer_workspace(desc: LayerDesc, device="cuda") -> torch.Tensor:
@@ -134,7 +149,7 @@ def layer_workspace(desc: LayerDesc, device="cuda") -> torch.Tensor:
 def moe_forward(x: torch.Tensor, p: MoeLayerParams, r, blk: int = 8,
                 scheme: str = "memory_efficient", validate: bool = True,
                 workspace: Optional[torch.Tensor] = None,
-                y: Optional[torch.Tensor] = None) -> MoeForwardResult:
+                y: Optional[torch.Tensor] = None, capacity: int = 0) -> MoeForwardResult:
     """y = sum_i ESMM(F(ESMM(x, W1, b1, R_i)), W2, b2, R_i) (moe_layer.cpp:30-67).
 
     ``r`` is a RoutingChoice (host) or a device int32 k x N tensor.  Both
@@ -142,6 +157,10 @@ def moe_forward(x: torch.Tensor, p: MoeLayerParams, r, blk: int = 8,
     memory-efficient scheme, moe_layer.cpp:61-63).  ``blk`` is the reference
     re-index tile size; results do not depend on it (padding neutrality,
     test_es_ops.cpp:250-268) and it is only validated.
+
+    ``capacity`` > 0 runs the conventional dispatch/combine baseline instead
+    (fixed per-expert buffers of ``capacity`` rows, overflow dropped; see
+    conventional.py) -- for measurement against the expert-specific path.
     """
     p.validate()
     moe_scheme_from_name(scheme)
@@ -164,7 +183,7 @@ def moe_forward(x: torch.Tensor, p: MoeLayerParams, r, blk: int = 8,
     if n_experts != p.experts():
         raise ShapeError("moe_forward: routing expert count != layer experts")
     desc = make_desc(n, p.experts(), k, p.d_in(), p.hidden(), p.d_out(), p.activation,
-                     x.dtype, p.b2 is not None)
+                     x.dtype, p.b2 is not None, capacity)
     ws = workspace if workspace is not None else layer_workspace(desc, x.device)
     if y is None:
         y = torch.empty(n, p.d_out(), dtype=torch.float32, device=x.device)

@@ -17,12 +17,12 @@ from .moe_layer import MoeGrads, MoeLayerParams, layer_workspace, make_desc
 
 class LayerRunner:
     def __init__(self, p: MoeLayerParams, n_tokens: int, k: int, device="cuda",
-                 dtype=torch.bfloat16, add_b2: bool = True):
+                 dtype=torch.bfloat16, add_b2: bool = True, capacity: int = 0):
         p.validate()
         self.p = p
         self.dtype = dtype
         self.desc = make_desc(n_tokens, p.experts(), k, p.d_in(), p.hidden(), p.d_out(),
-                              p.activation, dtype, add_b2 and p.b2 is not None)
+                              p.activation, dtype, add_b2 and p.b2 is not None, capacity)
         self.ws = layer_workspace(self.desc, device)
         f = dict(dtype=torch.float32, device=device)
         E, Di, H, Do = p.experts(), p.d_in(), p.hidden(), p.d_out()
