@@ -202,51 +202,75 @@ hxm_status launch_typed(const EssArgs& a, cudaStream_t st) {
   return HXM_OK;
 }
 
-template <class T, int VEC>
+// dst[p] = src[map(p)] (pads -> zero rows) for p < idx[E].  Each warp owns a
+// contiguous run of positions: one coalesced load of its indices, then
+// batches of 8 rows whose 16-byte units are all loaded before any store.
+template <class T, class IdxT>
 __global__ void __launch_bounds__(NT) gather_rows(const T* __restrict__ src, RowMap map,
-                                                  int64_t d, const int32_t* __restrict__ idx,
+                                                  int64_t d, const IdxT* __restrict__ idx,
                                                   int E, T* __restrict__ dst) {
   const int64_t np = idx[E];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int64_t groups = d / VEC;
-  for (int64_t p = static_cast<int64_t>(blockIdx.x) * (NT / 32) + warp; p < np;
-       p += static_cast<int64_t>(gridDim.x) * (NT / 32)) {
-    const int row = map(p);
-    T* o = dst + p * d;
-    if (row < 0) {
-      float z[VEC];
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (NT / 32);
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * (NT / 32) + warp;
+  const int64_t rb = d * static_cast<int64_t>(sizeof(T));
+  const bool vec = rb % 16 == 0 && reinterpret_cast<uintptr_t>(src) % 16 == 0 &&
+                   reinterpret_cast<uintptr_t>(dst) % 16 == 0;
+  const int64_t per = (ceil_div(np, nwarps) + 7) / 8 * 8;
+  const int64_t pb = gw * per, pe = min(np, pb + per);
+  const char* S = reinterpret_cast<const char*>(src);
+  char* Dst = reinterpret_cast<char*>(dst);
+  for (int64_t q0 = pb; q0 < pe; q0 += 32) {
+    const int row_l = q0 + lane < pe ? map(q0 + lane) : -1;
+    for (int r0 = 0; r0 < 32 && q0 + r0 < pe; r0 += 8) {
+      int rows[8];
 #pragma unroll
-      for (int i = 0; i < VEC; ++i) z[i] = 0.f;
-      for (int64_t g = lane; g < groups; g += 32) store_vec<T, VEC>(o + g * VEC, z);
-      continue;
-    }
-    const T* s = src + static_cast<int64_t>(row) * d;
-    for (int64_t g = lane; g < groups; g += 32) {
-      float v[VEC];
-      load_vec<T, VEC>(s + g * VEC, v);
-      store_vec<T, VEC>(o + g * VEC, v);
+      for (int u = 0; u < 8; ++u) rows[u] = __shfl_sync(0xffffffffu, row_l, r0 + u);
+      if (vec) {
+        const int64_t upr = rb / 16;
+        for (int64_t c0 = 0; c0 < upr; c0 += 64) {
+          uint4 buf[8][2];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int m = 0; m < 2; ++m) {
+              const int64_t o = c0 + m * 32 + lane;
+              buf[u][m] = (rows[u] >= 0 && o < upr)
+                              ? __ldg(reinterpret_cast<const uint4*>(S + rows[u] * rb) + o)
+                              : make_uint4(0u, 0u, 0u, 0u);
+            }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (q0 + r0 + u >= pe) break;
+            uint4* o4 = reinterpret_cast<uint4*>(Dst + (q0 + r0 + u) * rb);
+#pragma unroll
+            for (int m = 0; m < 2; ++m) {
+              const int64_t o = c0 + m * 32 + lane;
+              if (o < upr) o4[o] = buf[u][m];
+            }
+          }
+        }
+      } else {
+        for (int u = 0; u < 8 && q0 + r0 + u < pe; ++u) {
+          T* o = dst + (q0 + r0 + u) * d;
+          for (int64_t c = lane; c < d; c += 32)
+            o[c] = rows[u] >= 0 ? src[static_cast<int64_t>(rows[u]) * d + c] : from_f32<T>(0.f);
+        }
+      }
     }
   }
 }
 
-template <class T>
-hxm_status gather_typed(const void* src, RowMap map, int64_t d, const int32_t* idx, int E,
+template <class T, class IdxT>
+hxm_status gather_typed(const void* src, RowMap map, int64_t d, const IdxT* idx, int E,
                         int64_t bound, void* dst, cudaStream_t st) {
-  constexpr int V = 16 / sizeof(T);
   const int blocks = static_cast<int>(std::max<int64_t>(
-      1, std::min<int64_t>(ceil_div(bound, NT / 32), static_cast<int64_t>(sm_count()) * 8)));
-  const bool vec_ok = d % V == 0 && reinterpret_cast<uintptr_t>(src) % 16 == 0 &&
-                      reinterpret_cast<uintptr_t>(dst) % 16 == 0;
-  if (vec_ok)
-    gather_rows<T, V><<<blocks, NT, 0, st>>>(static_cast<const T*>(src), map, d, idx, E,
-                                             static_cast<T*>(dst));
-  else
-    gather_rows<T, 1><<<blocks, NT, 0, st>>>(static_cast<const T*>(src), map, d, idx, E,
-                                             static_cast<T*>(dst));
+      1, std::min<int64_t>(ceil_div(bound, 8 * (NT / 32)), static_cast<int64_t>(sm_count()) * 4)));
+  gather_rows<T, IdxT><<<blocks, NT, 0, st>>>(static_cast<const T*>(src), map, d, idx, E,
+                                              static_cast<T*>(dst));
   HXM_CHECK_LAUNCH();
   return HXM_OK;
 }
-
 
 // ------------------------------------------------ fused backward prologue --
 // One cooperative launch before the backward GEMMs: g_x = 0, zeroed gW
@@ -328,8 +352,18 @@ hxm_status launch_gather_rows(hxm_dtype dt, const void* src, RowMap map, int64_t
                               const int32_t* idx, int n_experts, int64_t bound, void* dst,
                               cudaStream_t st, double work_bytes) {
   ProfScope ps(st, "gather_rows", work_bytes, WORK_BYTES);
-  return dt == HXM_BF16 ? gather_typed<__nv_bfloat16>(src, map, d, idx, n_experts, bound, dst, st)
-                        : gather_typed<float>(src, map, d, idx, n_experts, bound, dst, st);
+  return dt == HXM_BF16
+             ? gather_typed<__nv_bfloat16, int32_t>(src, map, d, idx, n_experts, bound, dst, st)
+             : gather_typed<float, int32_t>(src, map, d, idx, n_experts, bound, dst, st);
+}
+
+hxm_status launch_gather_rows64(hxm_dtype dt, const void* src, RowMap map, int64_t d,
+                                const int64_t* idx, int n_experts, int64_t bound, void* dst,
+                                cudaStream_t st) {
+  ProfScope ps(st, "gather_rows", 0.0, WORK_BYTES);
+  return dt == HXM_BF16
+             ? gather_typed<__nv_bfloat16, int64_t>(src, map, d, idx, n_experts, bound, dst, st)
+             : gather_typed<float, int64_t>(src, map, d, idx, n_experts, bound, dst, st);
 }
 
 hxm_status launch_colsum_combine(const float* partial, const int32_t* tile_off, int n_experts,

@@ -107,6 +107,9 @@ struct EssArgs {
 hxm_status launch_gather_rows(hxm_dtype dt, const void* src, RowMap map, int64_t d,
                               const int32_t* idx, int n_experts, int64_t bound, void* dst,
                               cudaStream_t st, double work_bytes = 0.0);
+hxm_status launch_gather_rows64(hxm_dtype dt, const void* src, RowMap map, int64_t d,
+                                const int64_t* idx, int n_experts, int64_t bound, void* dst,
+                                cudaStream_t st);
 
 // out[e] = sum over e's tiles t (tile_off[e]..tile_off[e+1]) and the
 // `parts` partial rows of each tile of partial[(t * parts + r) x d]: the

@@ -46,6 +46,7 @@ struct OpWs {
   int32_t* etile_off;
   int32_t* n_etiles;
   float* partial;
+  void* sorted;  // bf16 ESMM: the expert-sorted copy of the A rows (np_bound x d1)
   int max_tiles, max_ktiles, max_etiles;
 };
 
@@ -64,6 +65,9 @@ OpWs carve(Arena& ar, int64_t np_bound, int64_t E, int64_t d1, int64_t d2) {
   w.etile_off = ar.take<int32_t>(E + 1);
   w.n_etiles = ar.take<int32_t>(1);
   w.partial = ar.take<float>(static_cast<size_t>(w.max_etiles) * std::max(d1, d2));
+  // 2-byte rows: only the bf16 tcgen05 path sorts its A operand
+  w.sorted = ar.take<char>(static_cast<size_t>(std::max<int64_t>(np_bound, 1)) *
+                           std::max(d1, d2) * 2);
   return w;
 }
 
@@ -109,6 +113,17 @@ hxm_status hxm_esmm(hxm_dtype dt, const void* x, int64_t n, int64_t d1, const vo
   a.a = x;
   a.amap = map_v64(v);
   a.a_rows = n;
+  if (rows == kUmmaRows) {
+    // tcgen05 path: one bandwidth-bound gather of the routed rows into
+    // expert-sorted order, then dense TMA tiles (a TMA gather4 request per
+    // 4 rows is request-rate bound); rows past a segment's end
+    // belong to the next expert and are masked by the epilogue's row map
+    HXM_RETURN_IF(launch_gather_rows64(dt, x, map_v64(v), d1, idx, static_cast<int>(E),
+                                       np_bound, o.sorted, st));
+    a.a = o.sorted;
+    a.amap = map_dense();
+    a.a_rows = std::max<int64_t>(np_bound, 1);
+  }
   a.n_experts = E;
   a.w = w;
   a.w_trans = w_trans;
