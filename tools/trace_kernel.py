@@ -24,8 +24,11 @@ L = _lib.lib()
 buf = (ctypes.c_ulonglong * (148 * 64 * 8))()
 L.hxm_debug_trace(buf)
 t = np.frombuffer(buf, dtype=np.uint64).reshape(148, 64, 8).astype(np.int64)
-t0 = t[t > 0].min()
-print("label", os.environ.get("HXM_TRACE"), "kernel span us", (t[t > 0].max() - t0) / 1e3)
+ts = t[:, :, :6]
+if not (ts > 0).any():
+    sys.exit("no trace recorded: build with -DHXM_TRACE_BUILD (python tools/trace_build.py)")
+t0 = ts[ts > 0].min()
+print("label", os.environ.get("HXM_TRACE"), "kernel span us", (ts[ts > 0].max() - t0) / 1e3)
 for cta in (0, 2, 74):
     print(f"CTA {cta}: item  mma[wait_tempty->got, loop_end]   epi[wait_tfull->got, end]  (us from start)")
     for i in range(64):
