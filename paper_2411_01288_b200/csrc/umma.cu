@@ -30,8 +30,14 @@ namespace {
 constexpr int BM = 128;  // UMMA M (rows per tile, TMEM lanes)
 constexpr int BK = 64;   // one 128-byte swizzle atom of bf16 per k-block
 constexpr int UK = 16;   // UMMA K for kind::f16
-constexpr int kEpiWarps = 8;
-constexpr int kThreads = 64 + 32 * kEpiWarps;  // producer, MMA, 8 epilogue warps
+// Epilogue warps per CTA: 8 (two per TMEM lane group), or 16 for the
+// stash-writing MODE 1 / 2 kernels at BN = 256, whose epilogue (activation,
+// F' multiply, column sums, TMA stores) is the bottleneck at K = 384 and needs
+// more warps to hide its latencies.  Threads = producer + MMA + epilogue.
+__host__ __device__ constexpr int epi_warps(int bn, int mode) {
+  return (mode == 1 || mode == 2) && bn == 256 ? 16 : 8;
+}
+__host__ __device__ constexpr int kthreads(int bn, int mode) { return 64 + 32 * epi_warps(bn, mode); }
 constexpr uint32_t kTmemCols = 512;
 constexpr int kABytes = BM * BK * 2;  // 16 KB
 
@@ -296,27 +302,6 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
 }
-// F(x) and F'(x) together (tensor.cpp:39-53, 62-72): GELU-tanh shares one
-// tanh.approx between the value and its exact derivative.
-__device__ __forceinline__ void act_both(int act, float x, float& f, float& df) {
-  if (act == HXM_ACT_GELU) {
-    const float x2 = x * x;
-    const float u = x * fmaf(0.7978845608028654f * 0.044715f, x2, 0.7978845608028654f);
-    float t;
-    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
-    const float hx = 0.5f * x;
-    f = fmaf(hx, t, hx);
-    const float du = fmaf(0.7978845608028654f * 3.f * 0.044715f, x2, 0.7978845608028654f);
-    df = fmaf(0.5f, t, 0.5f) + hx * fmaf(-t, t, 1.f) * du;
-  } else if (act == HXM_ACT_RELU) {
-    f = x > 0.f ? x : 0.f;
-    df = x > 0.f ? 1.f : 0.f;
-  } else {
-    f = x;
-    df = 1.f;
-  }
-}
-
 // ---- packed fp32x2 math (FFMA2 / FMUL2 on sm_100): two lanes per issue ----
 __device__ __forceinline__ float2 f2_fma(float2 a, float2 b, float2 c) {
   uint64_t d;
@@ -394,15 +379,23 @@ struct UParams {
 
 // CG = CTAs per UMMA (cta_group): with CG = 2 a CTA pair runs M = 256 tiles,
 // each CTA holding 128 rows of A / D and half (BN/2) of the B columns.
-template <int BN, int CG = 1, int MODE = 0>
+template <int BN, int CG = 1, int MODE = 0, int EW = 8>
 struct Cfg {
   static constexpr int kBBytes = (BN / CG) * BK * 2;
   static constexpr int kStage = kABytes + kBBytes;
+  static constexpr int kEW = EW;
+  static constexpr int kGroups = kEW / 4;  // column groups of 4 warps (one per lane group)
+  // MODE 1 / 2 staging per column group: kOutBufs output boxes (MODE 1: two
+  // 8 KB boxes F', F; MODE 2: one 8 KB g_y1 box) + a kYRing-deep F'(y1) ring
+  // (MODE 2); 16 epilogue warps trade depth for the extra groups.
+  static constexpr int kOutBufs = kEW == 16 ? 1 : 2;
+  static constexpr int kYRing = kEW == 16 ? 2 : 3;
+  static constexpr int kOutBox = MODE == 1 ? 16384 : 8192;
+  static constexpr int kGroupBytes =
+      MODE == 1 ? kOutBufs * kOutBox : MODE == 2 ? kOutBufs * kOutBox + kYRing * 8192 : 4 * 2048;
   // 227 KB opt-in smem = stages + epilogue staging + 1 KB alignment slack +
-  // barriers.  Staging: 2 KB per epilogue warp (MODE 0 / 3); per column half,
-  // MODE 1 double-buffers its two 8 KB output boxes (32 KB), MODE 2
-  // double-buffers its output box and keeps a 3-deep F'(y1) ring (40 KB).
-  static constexpr int kStaging = MODE == 2 ? 81920 : MODE == 1 ? 65536 : kEpiWarps * 2048;
+  // barriers.  Staging: 2 KB per epilogue warp (MODE 0 / 3).
+  static constexpr int kStaging = kGroups * kGroupBytes;
   static constexpr int kBudget = 232448 - 1024 - 256 - kStaging;
   static constexpr int kStages = kBudget / kStage > 8 ? 8 : kBudget / kStage;
   static constexpr int kSmem = kStages * kStage + kStaging + 1024 /*align*/ + 256 /*barriers*/;
@@ -417,10 +410,11 @@ struct Cfg {
 // issues tcgen05.mma.cta_group::2 with M = 256; both CTAs' TMA loads signal
 // the leader's full barrier; commits multicast to both CTAs' empty / tfull
 // barriers; both CTAs' epilogues arrive on the leader's tempty barrier.
-template <int BN, int MODE, int CG = 1, int ACT = -1>
-__global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant__ UParams p) {
+template <int BN, int MODE, int CG = 1, int ACT = -1, int EW = 8>
+__global__ void __launch_bounds__(64 + 32 * EW, 1)
+    umma_kernel(const __grid_constant__ UParams p) {
   constexpr bool ESTMM = MODE == 3;
-  using C = Cfg<BN, CG, MODE>;
+  using C = Cfg<BN, CG, MODE, EW>;
   uint32_t rank = 0;
   if constexpr (CG == 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   const int cluster = blockIdx.x / CG, n_clusters = gridDim.x / CG;
@@ -429,13 +423,13 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
   // __shared__ array keeps the address space visible to the compiler, so
   // staging accesses compile to LDS/STS rather than generic LD/ST
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* staging = smem + C::kStages * C::kStage;  // kEpiWarps x 4 KB
+  uint8_t* staging = smem + C::kStages * C::kStage;
   uint64_t* full = reinterpret_cast<uint64_t*>(staging + C::kStaging);
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + 2;
-  uint64_t* dbar = tempty + 2;  // MODE 2: F'(y1) box loads, [half][ring slot]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dbar + 6);
+  uint64_t* dbar = tempty + 2;  // MODE 2: F'(y1) box loads, [group][ring slot]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dbar + C::kGroups * C::kYRing);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
@@ -445,9 +439,9 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], kEpiWarps * CG);
+      mbar_init(&tempty[a], C::kEW * CG);
     }
-    for (int b = 0; b < 6; ++b) mbar_init(&dbar[b], 1);
+    for (int b = 0; b < C::kGroups * C::kYRing; ++b) mbar_init(&dbar[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -669,15 +663,14 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
     __syncwarp();
   } else {
     // ================================ epilogue ============================
-    // 8 warps: warp w reads TMEM lane group (w % 4) -- the hardware rule --
-    // and column half (w - 2) / 4 of the accumulator, so two warps per SMSP
-    // overlap TMEM loads, math and global traffic.  Each 32-row x 32-column
-    // chunk is transposed through a 4 KB per-warp staging buffer (16-byte
-    // chunks XOR-swizzled, conflict-free) so global stores / reductions
-    // cover whole row segments instead of 32 rows x 16 B per instruction.
-    constexpr int HB = BN / 2;
+    // kEW warps: warp w reads TMEM lane group (w % 4) -- the hardware rule --
+    // and column group (w - 2) / 4 of the accumulator (HB columns), so
+    // kEW / 4 warps per SMSP overlap TMEM loads, math and global traffic.
+    // fp32 outputs: each 32-row x 32-column chunk is transposed through a
+    // per-warp staging tile so stores / reductions cover row segments.
+    constexpr int HB = BN / C::kGroups;
     const int lg = warp & 3;
-    const int half = (warp - 2) / 4;
+    const int half = (warp - 2) / 4;  // column group
     uint8_t* stg = staging + (warp - 2) * 2048;
     // accumulator drained by this warp: arrive on the (leader's) tempty
     auto release_acc = [&](int a) {
@@ -686,15 +679,15 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
     };
     int acc = 0;
     uint32_t aph = 0;
-    int dchunk = 0;  // MODE 1/2: running chunk count of this half-group (buffers / phases)
-    constexpr int kYRing = 3;  // MODE 2: F'(y1) boxes in flight per half-group
+    int dchunk = 0;  // MODE 1/2: running chunk count of this group (buffers / phases)
+    constexpr int kYRing = C::kYRing;  // MODE 2: F'(y1) boxes in flight per group
     constexpr bool bwd = MODE == 2;
     constexpr bool dense_out = MODE == 1 || MODE == 2;
     constexpr int kNch = HB / 32;  // 32-column chunks per warp per tile
     const bool elect = ((warp - 2) & 3) == 0 && lane == 0;
-    // this half-group's staging: MODE 1 = 2 x (out1, out2) boxes, MODE 2 =
-    // 2 x out1 box + kYRing F'(y1) boxes (8 KB each: 128 rows x 32 bf16)
-    uint8_t* hstage = staging + half * (C::kStaging / 2);
+    // this group's staging: kOutBufs output boxes, then (MODE 2) the F'(y1)
+    // ring (8 KB per box: 128 rows x 32 bf16)
+    uint8_t* hstage = staging + half * C::kGroupBytes;
     // ESMM: the next work item's tile and this lane's output row are loaded
     // one item ahead, so an epilogue that finds its accumulator already full
     // does not wait on the tile table / index latency.
@@ -733,11 +726,13 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
         // every 32-row warp slice is entirely valid or entirely past the end.
         const int qbase = t.begin + static_cast<int>(rank) * BM;  // row 0 of the box
         const int rows_here = t.end - qbase;
-        auto ybox = [&](int gchunk) { return hstage + 16384 + (gchunk % kYRing) * 8192; };
+        auto ybox = [&](int gchunk) {
+          return hstage + C::kOutBufs * C::kOutBox + (gchunk % kYRing) * 8192;
+        };
         auto ybar = [&](int gchunk) { return &dbar[half * kYRing + gchunk % kYRing]; };
-        if (bwd && elect) {  // F'(y1) boxes of chunks 0 and 1, overlapping the MMA
+        if (bwd && elect) {  // F'(y1) boxes of the first chunks, overlapping the MMA
 #pragma unroll
-          for (int j = 0; j < (kNch < 2 ? kNch : 2); ++j) {
+          for (int j = 0; j < (kNch < kYRing - 1 ? kNch : kYRing - 1); ++j) {
             mbar_arrive_tx(ybar(dchunk + j), 8192);
             tma_2d(ybox(dchunk + j), &p.tmY, ybar(dchunk + j), n0 + 32 * j, qbase);
           }
@@ -789,14 +784,20 @@ __global__ void __launch_bounds__(kThreads, 1) umma_kernel(const __grid_constant
             const bool pad = orow < 0;  // padding slot -> zero row
             const int hrow = lg * 32 + lane;  // this thread's row in the 128-row box
             const int swz = (hrow >> 1) & 3;  // TMA 64B swizzle: chunk ^= (row >> 1) & 3
-            uint8_t* obox = hstage + (dchunk & 1) * (bwd ? 8192 : 16384);
-            // (1) the store of two chunks ago (same box) has read its smem, and
+            uint8_t* obox = hstage + (dchunk % C::kOutBufs) * C::kOutBox;
+            // (1) the store that last used this box has read its smem, and
             //     every thread is past the previous chunk's F'(y1) reads
-            if (elect) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            if (elect) {
+              if constexpr (C::kOutBufs == 2)
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+              else
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            }
             named_bar_sync(1 + half, 128);
-            if (bwd && elect && c0 + 64 < HB) {  // F'(y1) box two chunks ahead
-              mbar_arrive_tx(ybar(dchunk + 2), 8192);
-              tma_2d(ybox(dchunk + 2), &p.tmY, ybar(dchunk + 2), n + 64, qbase);
+            if (bwd && elect && c0 + 32 * (kYRing - 1) < HB) {  // F'(y1) kYRing-1 chunks ahead
+              const int ga = dchunk + kYRing - 1;
+              mbar_arrive_tx(ybar(ga), 8192);
+              tma_2d(ybox(ga), &p.tmY, ybar(ga), n + 32 * (kYRing - 1), qbase);
             }
             uint4 dv[4];
             if (bwd) {  // this row's F'(y1) chunk from the staged box
@@ -1070,15 +1071,16 @@ unsigned long long* trace_buffer_for(const char* label) {
   return g_trace;
 }
 
-template <int BN, int MODE, int CG, int ACT = -1>
-hxm_status launch_bn(const UParams& prm_in, int max_work, cudaStream_t st) {
+template <int BN, int MODE, int CG, int ACT = -1, int EW = 8>
+hxm_status launch_bn_ew(const UParams& prm_in, int max_work, cudaStream_t st) {
   UParams prm = prm_in;
   prm.trace = kTrace ? trace_buffer_for(prm_in.label) : nullptr;
   // debug decomposition (HXM_DEBUG_NOLOAD bits: 1 = no operand loads, 2 = no
   // epilogue stores, 4 = no MMAs); results are garbage, timing only
   if (kTrace) { const char* e = std::getenv("HXM_DEBUG_NOLOAD"); prm.dbg_noload = e ? std::atoi(e) : 0; }
-  using C = Cfg<BN, CG, MODE>;
-  auto kern = umma_kernel<BN, MODE, CG, ACT>;
+  using C = Cfg<BN, CG, MODE, EW>;
+  auto kern = umma_kernel<BN, MODE, CG, ACT, EW>;
+  constexpr int kThreads = 64 + 32 * EW;
   static bool attr_set = false;
   if (!attr_set) {
     HXM_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
@@ -1115,6 +1117,24 @@ hxm_status launch_bn(const UParams& prm_in, int max_work, cudaStream_t st) {
   HXM_TRY_CUDA(cudaLaunchKernelEx(&cfg, kern, prm));
   HXM_CHECK_LAUNCH();
   return HXM_OK;
+}
+
+// 16 epilogue warps where epi_warps() asks for them (HXM_EPI16=0: always 8)
+bool epi16_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("HXM_EPI16");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+template <int BN, int MODE, int CG, int ACT = -1>
+hxm_status launch_bn(const UParams& prm, int max_work, cudaStream_t st) {
+  // only where the epilogue bounds the kernel: short K (<= 512, e.g. c2's
+  // D = 384); at long K the MMA bounds it and 8 warps keep more ring stages
+  if constexpr (epi_warps(BN, MODE) == 16) {
+    if (epi16_on() && prm.K <= 512) return launch_bn_ew<BN, MODE, CG, ACT, 16>(prm, max_work, st);
+  }
+  return launch_bn_ew<BN, MODE, CG, ACT, 8>(prm, max_work, st);
 }
 
 template <int MODE, int CG, int ACT = -1>
