@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhexamoe.so")
+# HXM_LIB: an alternative in-tree build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("HXM_LIB") or os.path.join(HERE, "libhexamoe.so")
 
 HXM_OK, HXM_ERR_SHAPE, HXM_ERR_INVALID_ARG, HXM_ERR_CUDA = 0, 1, 2, 3
 HXM_ERR_NCCL, HXM_ERR_CACHE, HXM_ERR_UNSUPPORTED = 4, 5, 6
