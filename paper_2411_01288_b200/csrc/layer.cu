@@ -372,7 +372,14 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
   b6.colsum = w.colsum;
   HXM_RETURN_IF(launch_esmm(dt, b6, st));
   SideStream side{};
-  if (w.colsum) {
+  const char* se = std::getenv("HXM_SIDE");
+  const bool use_side = !(se && se[0] == '0');
+  if (w.colsum && !use_side) {
+    const int parts = (w.rows_a / kUmmaRows) * 4;
+    HXM_RETURN_IF(launch_colsum_combine(
+        w.colsum, w.tiles_a_off, static_cast<int>(E), parts, H, gb1, st, "gb1_combine",
+        (static_cast<double>(max_tiles(w.bound, E, w.rows_a)) * parts + E) * H * 4.0));
+  } else if (w.colsum) {
     // the gb1 combine is independent of gW1 / gx: it runs on the side
     // stream beside them (a parallel branch of the captured graph)
     side = side_stream();
