@@ -175,6 +175,25 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
       "r"(c0), "r"(c1), "r"(smem_u32(src))
       : "memory");
 }
+// the same store with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* map, const void* src, int c0,
+                                                  int c1, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint"
+      " [%0, {%1, %2}], [%3], %4;" ::"l"(map),
+      "r"(c0), "r"(c1), "r"(smem_u32(src)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
@@ -361,6 +380,7 @@ struct UParams {
   int dbg_noload;
   unsigned long long* trace;  // debug timeline (HXM_TRACE), null normally
   int b_sw64;  // CG = 2, MN-major B halves of 32-column multiples: 64B-swizzled boxes
+  int l2hint;  // MODE 1/2: L2 eviction-priority hints on the stash stores
   int K, N, M;  // ESMM: K=d1, N=d2 ; ESTMM: M=d1, N=d2
   int n_nt, n_mt;
   const SegTile* tiles;
@@ -842,8 +862,20 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
             named_bar_sync(1 + half, 128);
             if (elect) {
               if (rows_here >= BM) {
-                tma_store_2d(&p.tmO1, obox, n, qbase);
-                if (!bwd) tma_store_2d(&p.tmO2, obox + 8192, n, qbase);
+                // L2 policy: what the NEXT kernel reads stays (MODE 1: F(y1)
+                // for ESMM fwd2; MODE 2: g_y1 for ESTMM gW1 / ESMM gx), what
+                // is read only much later goes first (MODE 1: F'(y1))
+                if (p.l2hint) {
+                  if (!bwd) {
+                    tma_store_2d_hint(&p.tmO1, obox, n, qbase, policy_evict_first());
+                    tma_store_2d_hint(&p.tmO2, obox + 8192, n, qbase, policy_evict_last());
+                  } else {
+                    tma_store_2d_hint(&p.tmO1, obox, n, qbase, policy_evict_last());
+                  }
+                } else {
+                  tma_store_2d(&p.tmO1, obox, n, qbase);
+                  if (!bwd) tma_store_2d(&p.tmO2, obox + 8192, n, qbase);
+                }
               } else {
                 for (int sl = 0; sl * 32 < rows_here; ++sl) {
                   tma_store_2d(&p.tmO1s, obox + sl * 2048, n, qbase + sl * 32);
@@ -1075,6 +1107,13 @@ template <int BN, int MODE, int CG, int ACT = -1, int EW = 8>
 hxm_status launch_bn_ew(const UParams& prm_in, int max_work, cudaStream_t st) {
   UParams prm = prm_in;
   prm.trace = kTrace ? trace_buffer_for(prm_in.label) : nullptr;
+  {
+    static const bool hint = [] {
+      const char* e = std::getenv("HXM_L2HINT");
+      return !(e && e[0] == '0');
+    }();
+    prm.l2hint = hint;
+  }
   // debug decomposition (HXM_DEBUG_NOLOAD bits: 1 = no operand loads, 2 = no
   // epilogue stores, 4 = no MMAs); results are garbage, timing only
   if (kTrace) { const char* e = std::getenv("HXM_DEBUG_NOLOAD"); prm.dbg_noload = e ? std::atoi(e) : 0; }
