@@ -63,6 +63,7 @@ struct EsmmArgs {
   void* out1;      // FWD_ACT / BWD_ACT dense outputs (dtype), row stride d2
   void* out2;
   const void* y1s;  // BWD_ACT: pre-activation stash (dtype), row stride d2
+  int reverse;      // tcgen05: work items last to first (see umma.cu)
   float* colsum;    // BWD_ACT (tcgen05): per-(tile, CTA, lane group) column sums of out1,
                     // [((tile * CG + cta) * 4 + group) x d2] -> colsum_combine
 };
@@ -82,6 +83,7 @@ struct EstmmArgs {
   int max_tiles;
   int n_experts;
   float* out;  // E x d1 x d2
+  int reverse;      // tcgen05: work items last to first
   int skip_zero_split;  // split experts' slices already zeroed by the caller
 };
 

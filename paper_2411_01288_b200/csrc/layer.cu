@@ -263,6 +263,7 @@ hxm_status hxm_moe_forward(const hxm_layer_desc* d, const void* x, const void* w
   a2.bytes = kn * d->hidden * es_ + w2bytes + 4.0 * N * d->d_out;
   a2.out_f32 = y;
   a2.omap = slot;
+  a2.reverse = 1;  // y2 rows written last by fwd1 are still in L2
   a2.out1 = a2.out2 = nullptr;
   return launch_esmm(dt, a2, st);
 }
@@ -410,6 +411,7 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
   t1.d1 = Di;
   t1.d2 = H;
   t1.out = gw1;
+  t1.reverse = 1;  // g_y1 rows written last by bwd_act are still in L2
   t1.label = "estmm_gw1";
   t1.work = 2.0 * kn * Di * H;
   t1.bytes = kn * (Di + H) * esz + 4.0 * E * Di * H;

@@ -381,6 +381,7 @@ struct UParams {
   unsigned long long* trace;  // debug timeline (HXM_TRACE), null normally
   int b_sw64;  // CG = 2, MN-major B halves of 32-column multiples: 64B-swizzled boxes
   int l2hint;  // MODE 1/2: L2 eviction-priority hints on the stash stores
+  int reverse; // walk the work items last to first
   int K, N, M;  // ESMM: K=d1, N=d2 ; ESTMM: M=d1, N=d2
   int n_nt, n_mt;
   const SegTile* tiles;
@@ -491,6 +492,9 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
   const int n_items = *p.n_tiles;
   const int per_item = ESTMM ? p.n_mt * p.n_nt : p.n_nt;
   const int total = n_items * per_item;
+  // p.reverse: walk the items last to first, so a kernel that consumes the
+  // previous kernel's output starts on the rows written last (L2-resident)
+  auto wmap = [&](int wl) { return p.reverse ? total - 1 - wl : wl; };
 
   if (warp == 0) {
     // ================================ TMA producer =======================
@@ -501,7 +505,8 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
     int s = 0;
     uint32_t ph = 0;
     int pit_ = 0;
-    for (int w = cluster; w < total; w += n_clusters, ++pit_) {
+    for (int wl = cluster; wl < total; wl += n_clusters, ++pit_) {
+      const int w = wmap(wl);
       const SegTile t = p.tiles[w / per_item];
       const int rem = w % per_item;
       if (!ESTMM) {
@@ -644,7 +649,8 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
       int s = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
       int it_ = 0;
-      for (int w = cluster; w < total; w += n_clusters, ++it_) {
+      for (int wl = cluster; wl < total; wl += n_clusters, ++it_) {
+        const int w = wmap(wl);
         const SegTile t = p.tiles[w / per_item];
         const int nk = ESTMM ? (t.end - t.begin + BK - 1) / BK : p.K / BK;
         TRACE(it_, 0);
@@ -728,13 +734,15 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
       return p.omap(qq);
     };
     int ep_it = 0;
-    SegTile t_cur = ESTMM ? SegTile{0, 0, 0, 0} : tile_at(cluster);
+    SegTile t_cur = ESTMM || cluster >= total ? SegTile{0, 0, 0, 0} : tile_at(wmap(cluster));
     int orow_cur = ESTMM ? -1 : orow_of(t_cur);
-    for (int w = cluster; w < total; w += n_clusters) {
+    for (int wl = cluster; wl < total; wl += n_clusters) {
+      const int w = wmap(wl);
       const SegTile t = ESTMM ? p.tiles[w / per_item] : t_cur;
       const int rem = w % per_item;
       if (!ESTMM) {
-        const SegTile t_nx = tile_at(w + n_clusters);  // prefetch (consumed next item)
+        const bool has_nx = wl + n_clusters < total;
+        const SegTile t_nx = has_nx ? tile_at(wmap(wl + n_clusters)) : SegTile{0, 0, 0, 0};  // prefetch
         int orow_nx = -1;
         const int n0 = rem * BN + half * HB;
         const int orow = orow_cur;
@@ -785,7 +793,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
           // next chunk's TMEM load overlaps this chunk's math
           if (c0 + 32 < HB) tmem_ld32_async(taddr + c0 + 32, rbuf[((c0 / 32) + 1) & 1]);
           // the next item's output row (its tile was loaded at this item's start)
-          if (c0 == 0 && w + n_clusters < total) orow_nx = orow_of(t_nx);
+          if (c0 == 0 && has_nx) orow_nx = orow_of(t_nx);
           const int n = n0 + c0;
           float v[32];
 #pragma unroll
@@ -1159,6 +1167,14 @@ hxm_status launch_bn_ew(const UParams& prm_in, int max_work, cudaStream_t st) {
 }
 
 // 16 epilogue warps where epi_warps() asks for them (HXM_EPI16=0: always 8)
+bool rev_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("HXM_REVERSE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool epi16_on() {
   static const bool on = [] {
     const char* e = std::getenv("HXM_EPI16");
@@ -1261,6 +1277,7 @@ hxm_status umma_esmm(const EsmmArgs& a, cudaStream_t st) {
   prm.tiles = a.tiles;
   prm.n_tiles = a.n_tiles;
   prm.label = a.label;
+  prm.reverse = a.reverse && rev_on();
   prm.epi = a.epi;
   prm.act = a.act;
   prm.bias = a.bias;
@@ -1356,6 +1373,7 @@ hxm_status umma_estmm(const EstmmArgs& a, cudaStream_t st) {
   prm.n_tiles = a.n_tiles;
   prm.est_out = a.out;
   prm.label = a.label;
+  prm.reverse = a.reverse && rev_on();
   const int work = a.max_tiles * prm.n_mt * prm.n_nt;
   if (CG == 2) return launch_bn_any<3, 2>(bn, prm, work, st);
   return launch_bn_any<3, 1>(bn, prm, work, st);
