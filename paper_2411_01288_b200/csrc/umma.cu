@@ -1091,12 +1091,13 @@ int pick_bn(int64_t n) {
 // CTA-pair tiles: an MN-major B half must be whole swizzle atoms -- 64
 // columns (128B swizzle), or 32 columns with 64B-swizzled boxes (BN = 192)
 int pick_bn2(int64_t n, bool b_mn) {
-  if (b_mn) {
-    for (int bn : {256, 192, 128})
-      if (n % bn == 0) return bn;
-    return 0;
-  }
-  return pick_bn(n);
+  static const int bn_max = [] {  // HXM_BN2_MAX: experiment override
+    const char* e = std::getenv("HXM_BN2_MAX");
+    return e ? std::atoi(e) : 256;
+  }();
+  for (int bn : {256, 192, 128, 64})
+    if (bn <= bn_max && n % bn == 0 && (!b_mn || bn >= 128)) return bn;
+  return 0;
 }
 bool bn2_sw64(int bn, bool b_mn) { return b_mn && (bn / 2) % 64 != 0; }
 
