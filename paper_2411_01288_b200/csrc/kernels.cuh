@@ -142,7 +142,10 @@ constexpr int kEssRows = 128;
 constexpr int kSimtRows = 64;     // SIMT ESMM tile rows
 constexpr int kUmmaRows = 128;    // tcgen05 ESMM tile rows (UMMA M)
 constexpr int kUmma2Rows = 256;   // CTA-pair (cta_group::2) ESMM tile rows
-constexpr int kEstmmChunk = 2048; // ESTMM split-K chunk (positions)
+constexpr int kEstmmChunk = 8192;  // ESTMM: an expert up to this many positions is one
+                                   // K chunk; longer (skewed) experts are split into
+constexpr int kEstmmSplit = 2048;  // chunks of this many, reduced with fp32 red.add
+                                   // into their zeroed gW slices
 
 hxm_status launch_esmm(hxm_dtype dt, const EsmmArgs& a, cudaStream_t st);
 hxm_status launch_estmm(hxm_dtype dt, const EstmmArgs& a, cudaStream_t st);

@@ -89,7 +89,7 @@ LayerWs carve(Arena& ar, const hxm_layer_desc& d) {
   w.tiles_a = ar.take<SegTile>(w.max_tiles_a);
   w.tiles_a_off = ar.take<int32_t>(d.n_experts + 1);
   w.n_tiles_a = ar.take<int32_t>(1);
-  w.max_ktiles = static_cast<int>(max_tiles(w.bound, d.n_experts, kEstmmChunk));
+  w.max_ktiles = static_cast<int>(max_tiles(w.bound, d.n_experts, kEstmmSplit));
   w.ktiles = ar.take<SegTile>(w.max_ktiles);
   w.ktiles_off = ar.take<int32_t>(d.n_experts + 1);
   w.n_ktiles = ar.take<int32_t>(1);
@@ -197,7 +197,7 @@ hxm_status hxm_moe_forward(const hxm_layer_desc* d, const void* x, const void* w
     pro.v = w.v;
     pro.idx = w.idx;
     pro.s0 = {w.rows_a, 0, w.tiles_a, w.tiles_a_off, w.n_tiles_a};
-    pro.s1 = {kEstmmChunk, 1, w.ktiles, w.ktiles_off, w.n_ktiles};
+    pro.s1 = {kEstmmChunk, 1, w.ktiles, w.ktiles_off, w.n_ktiles, kEstmmSplit};
     pro.s2 = {kEssRows, 0, w.etiles, w.etiles_off, w.n_etiles};
     pro.x = N > 0 ? x : nullptr;
     pro.xs = w.xs;

@@ -53,7 +53,7 @@ struct OpWs {
 OpWs carve(Arena& ar, int64_t np_bound, int64_t E, int64_t d1, int64_t d2) {
   OpWs w{};
   w.max_tiles = static_cast<int>(max_tiles(np_bound, E, kSimtRows));
-  w.max_ktiles = static_cast<int>(max_tiles(np_bound, E, kEstmmChunk));
+  w.max_ktiles = static_cast<int>(max_tiles(np_bound, E, kEstmmSplit));
   w.max_etiles = static_cast<int>(max_tiles(np_bound, E, kEssRows));
   w.tiles = ar.take<SegTile>(w.max_tiles);
   w.tile_off = ar.take<int32_t>(E + 1);

@@ -203,7 +203,8 @@ hxm_status build_impl(const int32_t* a, int64_t n, int64_t E, int64_t blk,
 template <class IdxT, int NT = 1024>
 __device__ void tile_pass(const IdxT* __restrict__ idx, int E, int rows, int min_one,
                           SegTile* __restrict__ tiles, int32_t* __restrict__ tile_off,
-                          int32_t* __restrict__ n_tiles, const int32_t* counts = nullptr) {
+                          int32_t* __restrict__ n_tiles, const int32_t* counts = nullptr,
+                          int split_rows = 0) {
   using Scan = cub::BlockScan<int32_t, NT>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int32_t carry;
@@ -213,11 +214,12 @@ __device__ void tile_pass(const IdxT* __restrict__ idx, int E, int rows, int min
   for (int e0 = 0; e0 < E; e0 += NT) {
     const int e = e0 + threadIdx.x;
     int32_t nt = 0;
-    int64_t b = 0, len = 0;
+    int64_t b = 0, len = 0, re = rows;
     if (e < E) {
       b = idx[e];
       len = static_cast<int64_t>(idx[e + 1]) - b;
-      nt = static_cast<int32_t>((len + rows - 1) / rows);
+      if (split_rows > 0 && len > rows) re = split_rows;
+      nt = static_cast<int32_t>((len + re - 1) / re);
       if (nt == 0 && min_one) nt = 1;
     }
     int32_t excl, agg;
@@ -230,8 +232,8 @@ __device__ void tile_pass(const IdxT* __restrict__ idx, int E, int rows, int min
       for (int j = 0; j < nt; ++j) {
         SegTile t;
         t.expert = e;
-        t.begin = static_cast<int>(b + static_cast<int64_t>(j) * rows);
-        const int64_t hi = b + static_cast<int64_t>(j + 1) * rows;
+        t.begin = static_cast<int>(b + static_cast<int64_t>(j) * re);
+        const int64_t hi = b + static_cast<int64_t>(j + 1) * re;
         t.end = static_cast<int>(hi < b + len ? hi : b + len);
         if (len == 0) t.end = t.begin;
         t.flags = split | empty;
@@ -256,9 +258,14 @@ __device__ void tile_pass(const IdxT* __restrict__ idx, int E, int rows, int min
 template <class IdxT>
 __global__ void build_tiles(const IdxT* __restrict__ idx, int E, TileSpec a, TileSpec b,
                             TileSpec c, int count) {
-  tile_pass<IdxT>(idx, E, a.rows, a.min_one, a.tiles, a.tile_off, a.n_tiles);
-  if (count > 1) tile_pass<IdxT>(idx, E, b.rows, b.min_one, b.tiles, b.tile_off, b.n_tiles);
-  if (count > 2) tile_pass<IdxT>(idx, E, c.rows, c.min_one, c.tiles, c.tile_off, c.n_tiles);
+  tile_pass<IdxT>(idx, E, a.rows, a.min_one, a.tiles, a.tile_off, a.n_tiles, nullptr,
+                  a.split_rows);
+  if (count > 1)
+    tile_pass<IdxT>(idx, E, b.rows, b.min_one, b.tiles, b.tile_off, b.n_tiles, nullptr,
+                    b.split_rows);
+  if (count > 2)
+    tile_pass<IdxT>(idx, E, c.rows, c.min_one, c.tiles, c.tile_off, c.n_tiles, nullptr,
+                    c.split_rows);
 }
 
 // ------------------------------------------------- fused layer prologue --
@@ -416,11 +423,11 @@ __global__ void __launch_bounds__(kThreads) fwd_prologue(FwdPrologue a) {
     }
     if (blockIdx.x == gridDim.x - 1) {
       tile_pass<int32_t, kThreads>(sidx, E, a.s0.rows, a.s0.min_one, a.s0.tiles, a.s0.tile_off,
-                                   a.s0.n_tiles, a.total);
+                                   a.s0.n_tiles, a.total, a.s0.split_rows);
       tile_pass<int32_t, kThreads>(sidx, E, a.s1.rows, a.s1.min_one, a.s1.tiles, a.s1.tile_off,
-                                   a.s1.n_tiles, a.total);
+                                   a.s1.n_tiles, a.total, a.s1.split_rows);
       tile_pass<int32_t, kThreads>(sidx, E, a.s2.rows, a.s2.min_one, a.s2.tiles, a.s2.tile_off,
-                                   a.s2.n_tiles, a.total);
+                                   a.s2.n_tiles, a.total, a.s2.split_rows);
     }
   }
   pro_ts(5);

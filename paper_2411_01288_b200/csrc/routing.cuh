@@ -27,6 +27,9 @@ struct TileSpec {
   SegTile* tiles;
   int32_t* tile_off;
   int32_t* n_tiles;
+  int split_rows = 0;  // > 0: segments longer than `rows` are cut into
+                       // split_rows-position tiles instead (ESTMM chunks: one
+                       // chunk per expert unless it is heavily skewed)
 };
 template <class IdxT>
 hxm_status launch_tiles3(const IdxT* idx, int64_t E, const TileSpec* specs, int count,

@@ -298,10 +298,10 @@ def test_layer_bf16_vs_oracle(E, k, din, hid, dout, n, act, dist):
 
 def test_layer_skewed_split_k():
     """c5-style skew: most slots on two experts, so their ESTMM is split over
-    several 2048-position chunks (fp32 reductions into zeroed slices), others
+    several 8192-position chunks (fp32 reductions into zeroed slices), others
     have a few tokens or none."""
     H = hx()
-    E, k, D, Hd, N = 16, 2, 128, 256, 3000
+    E, k, D, Hd, N = 16, 2, 128, 256, 20000
     p, x = H.make_random_params(E, D, Hd, D, "gelu", seed=5, n_tokens=N)
     r = H.synthesize_routing(N, E, k, "uniform", 6)
     a = r.assignments.copy()
