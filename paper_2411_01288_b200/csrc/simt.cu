@@ -9,7 +9,9 @@
 // ESMM: 64-row segment tile x 64 columns per CTA, K in steps of 16, 4x4
 // outputs per thread; A rows are gathered through the row map (padding slots
 // read as zeros), B is W[e] or W[e]^T.  ESTMM: 64x64 output tile per CTA,
-// K = the chunk's token positions in steps of 16.
+// K = the chunk's token positions in steps of 16.  Small grids are split
+// along K (blockIdx.z) with fp32 atomic reductions, so the fp32 layer at
+// c1's sizes (a few hundred CTAs of long K loops) fills the 148 SMs.
 #include "kernels.cuh"
 
 namespace hxm {
@@ -22,18 +24,95 @@ __device__ __forceinline__ float ld(const T* p, int64_t i) {
   return to_f32(p[i]);
 }
 
-template <class T>
+// Tile loaders.  VEC (fp32 with every extent a multiple of 4 and 16-byte
+// aligned bases): one float4 per thread per operand per k-step; otherwise
+// scalar loads (tiny / unaligned test shapes, bf16 fallback shapes).
+template <class T, bool VEC>
+__device__ __forceinline__ void load_rows_kmajor(float (&S)[BK][BM], const T* A, const int* arow,
+                                                 int64_t K, int64_t kend, int64_t k0) {
+  // S[kk][r] = A[arow[r]][k0 + kk] for k < kend (row stride K)
+  const int tid = threadIdx.x;
+  if constexpr (VEC) {
+    const int r = tid / 4, k4 = (tid % 4) * 4;
+    const int row = arow[r];
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (row >= 0 && k0 + k4 < kend)
+      v = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(A) +
+                                                static_cast<int64_t>(row) * K + k0 + k4));
+    S[k4][r] = v.x; S[k4 + 1][r] = v.y; S[k4 + 2][r] = v.z; S[k4 + 3][r] = v.w;
+  } else {
+    for (int i = tid; i < BM * BK; i += NT) {
+      const int r = i / BK, kk = i % BK;
+      const int row = arow[r];
+      const int64_t k = k0 + kk;
+      S[kk][r] = (row >= 0 && k < kend) ? ld(A, static_cast<int64_t>(row) * K + k) : 0.f;
+    }
+  }
+}
+
+template <class T, bool VEC>
+__device__ __forceinline__ void load_w(float (&S)[BK][BN], const T* W, int w_trans, int64_t K,
+                                       int64_t kend, int64_t N, int64_t k0, int n0) {
+  // S[kk][c] = B(k0 + kk, n0 + c): W[k][n] (w_trans = 0) or W[n][k] (W^T use)
+  const int tid = threadIdx.x;
+  if constexpr (VEC) {
+    if (!w_trans) {
+      const int kk = tid / 16, c4 = (tid % 16) * 4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (k0 + kk < kend && n0 + c4 < N)
+        v = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(W) +
+                                                  (k0 + kk) * N + n0 + c4));
+      S[kk][c4] = v.x; S[kk][c4 + 1] = v.y; S[kk][c4 + 2] = v.z; S[kk][c4 + 3] = v.w;
+    } else {
+      const int c = tid / 4, k4 = (tid % 4) * 4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (n0 + c < N && k0 + k4 < kend)
+        v = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(W) +
+                                                  (n0 + c) * K + k0 + k4));
+      S[k4][c] = v.x; S[k4 + 1][c] = v.y; S[k4 + 2][c] = v.z; S[k4 + 3][c] = v.w;
+    }
+  } else {
+    for (int i = tid; i < BM * BK; i += NT) {
+      const int kk = i / BN, c = i % BN;
+      const int64_t k = k0 + kk, n = n0 + c;
+      float val = 0.f;
+      if (k < kend && n < N) val = w_trans ? ld(W, n * K + k) : ld(W, k * N + n);
+      S[kk][c] = val;
+    }
+  }
+}
+
+__device__ __forceinline__ void mma_tile(const float (&As)[BK][BM], const float (&Bs)[BK][BN],
+                                         float (&acc)[4][4], int ty, int tx) {
+#pragma unroll
+  for (int kk = 0; kk < BK; ++kk) {
+    const float4 av = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+    const float4 bv = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+    const float a4[4] = {av.x, av.y, av.z, av.w}, b4[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a4[i], b4[j], acc[i][j]);
+  }
+}
+
+// ESMM: 64-row segment tile x 64 columns per CTA (blockIdx.x = column block,
+// y = tile); blockIdx.z splits K for the fp32 reduction epilogue (EPI_ATOMIC:
+// the partial sums add up in the destination; the bias goes with split 0).
+// Double-buffered smem: the next k-step's tiles load while this one computes.
+template <class T, bool VEC>
 __global__ void __launch_bounds__(NT) esmm_simt_kernel(EsmmArgs a) {
   const int ti = blockIdx.y;
   if (ti >= *a.n_tiles) return;
   const SegTile tile = a.tiles[ti];
   const int n0 = blockIdx.x * BN;
   const int64_t K = a.d1, N = a.d2;
+  const int64_t kper = ceil_div(ceil_div(K, BK), gridDim.z) * BK;
+  const int64_t kb = blockIdx.z * kper, ke = min(K, kb + kper);
   const T* A = static_cast<const T*>(a.a);
   const T* W = static_cast<const T*>(a.w) + static_cast<int64_t>(tile.expert) * K * N;
-
-  __shared__ float As[BK][BM];
-  __shared__ float Bs[BK][BN];
+  __shared__ __align__(16) float As[2][BK][BM];
+  __shared__ __align__(16) float Bs[2][BK][BN];
   __shared__ int arow[BM];
   const int tid = threadIdx.x;
   if (tid < BM) {
@@ -43,36 +122,23 @@ __global__ void __launch_bounds__(NT) esmm_simt_kernel(EsmmArgs a) {
   __syncthreads();
   const int ty = tid / 16, tx = tid % 16;
   float acc[4][4] = {};
-  for (int64_t k0 = 0; k0 < K; k0 += BK) {
-    for (int i = tid; i < BM * BK; i += NT) {
-      const int r = i / BK, kk = i % BK;
-      const int row = arow[r];
-      const int64_t k = k0 + kk;
-      As[kk][r] = (row >= 0 && k < K) ? ld(A, static_cast<int64_t>(row) * K + k) : 0.f;
+  int buf = 0;
+  if (kb < ke) {
+    load_rows_kmajor<T, VEC>(As[0], A, arow, K, ke, kb);
+    load_w<T, VEC>(Bs[0], W, a.w_trans, K, ke, N, kb, n0);
+  }
+  __syncthreads();
+  for (int64_t k0 = kb; k0 < ke; k0 += BK) {
+    if (k0 + BK < ke) {  // prefetch the next k-step into the other buffer
+      load_rows_kmajor<T, VEC>(As[buf ^ 1], A, arow, K, ke, k0 + BK);
+      load_w<T, VEC>(Bs[buf ^ 1], W, a.w_trans, K, ke, N, k0 + BK, n0);
     }
-    for (int i = tid; i < BM * BK; i += NT) {
-      const int kk = i / BN, c = i % BN;
-      const int64_t k = k0 + kk, n = n0 + c;
-      float val = 0.f;
-      if (k < K && n < N) val = a.w_trans ? ld(W, n * K + k) : ld(W, k * N + n);
-      Bs[kk][c] = val;
-    }
+    mma_tile(As[buf], Bs[buf], acc, ty, tx);
     __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < BK; ++kk) {
-      float av[4], bv[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) av[i] = As[kk][ty * 4 + i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx * 4 + j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
-    }
-    __syncthreads();
+    buf ^= 1;
   }
   // epilogue
+  const bool lead = blockIdx.z == 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int r = ty * 4 + i;
@@ -83,7 +149,8 @@ __global__ void __launch_bounds__(NT) esmm_simt_kernel(EsmmArgs a) {
     for (int j = 0; j < 4; ++j) {
       const int64_t n = n0 + tx * 4 + j;
       if (n >= N) continue;
-      const float bias = a.bias ? a.bias[static_cast<int64_t>(tile.expert) * N + n] : 0.f;
+      const float bias =
+          (a.bias && lead) ? a.bias[static_cast<int64_t>(tile.expert) * N + n] : 0.f;
       const float v = acc[i][j] + bias;
       switch (a.epi) {
         case EPI_WRITE:
@@ -117,7 +184,10 @@ __global__ void __launch_bounds__(NT) esmm_simt_kernel(EsmmArgs a) {
   }
 }
 
-template <class T>
+// ESTMM: 64 x 64 output tile per CTA, K = the chunk's token positions in
+// steps of 16; blockIdx.z splits the positions (the output is then pre-zeroed
+// and every split reduces with atomicAdd).
+template <class T, bool VEC>
 __global__ void __launch_bounds__(NT) estmm_simt_kernel(EstmmArgs a) {
   const int ti = blockIdx.y;
   if (ti >= *a.n_tiles) return;
@@ -127,44 +197,50 @@ __global__ void __launch_bounds__(NT) estmm_simt_kernel(EstmmArgs a) {
   const int m0 = (blockIdx.x % mt) * BM, n0 = (blockIdx.x / mt) * BN;
   const T* X1 = static_cast<const T*>(a.x1);
   const T* X2 = static_cast<const T*>(a.x2);
-  __shared__ float As[BK][BM];
-  __shared__ float Bs[BK][BN];
+  const int64_t len = tile.end - tile.begin;
+  const int64_t per = ceil_div(ceil_div(len, BK), gridDim.z) * BK;
+  const int64_t pb = tile.begin + blockIdx.z * per, pe = pb + per < tile.end ? pb + per : static_cast<int64_t>(tile.end);
+  __shared__ __align__(16) float As[BK][BM];
+  __shared__ __align__(16) float Bs[BK][BN];
   __shared__ int r1[BK], r2[BK];
   const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
   float acc[4][4] = {};
-  for (int64_t p0 = tile.begin; p0 < tile.end; p0 += BK) {
+  for (int64_t p0 = pb; p0 < pe; p0 += BK) {
     if (tid < BK) {
       const int64_t p = p0 + tid;
-      r1[tid] = p < tile.end ? a.m1(p) : -1;
-      r2[tid] = p < tile.end ? a.m2(p) : -1;
+      r1[tid] = p < pe ? a.m1(p) : -1;
+      r2[tid] = p < pe ? a.m2(p) : -1;
     }
     __syncthreads();
-    for (int i = tid; i < BK * BM; i += NT) {
-      const int kk = i / BM, c = i % BM;
-      const int row = r1[kk];
-      const int64_t m = m0 + c;
-      As[kk][c] = (row >= 0 && m < D1) ? ld(X1, static_cast<int64_t>(row) * D1 + m) : 0.f;
-      const int row2 = r2[kk];
-      const int64_t n = n0 + c;
-      Bs[kk][c] = (row2 >= 0 && n < D2) ? ld(X2, static_cast<int64_t>(row2) * D2 + n) : 0.f;
+    if constexpr (VEC) {
+      const int kk = tid / 16, c4 = (tid % 16) * 4;
+      float4 va = make_float4(0.f, 0.f, 0.f, 0.f), vb = va;
+      const int row = r1[kk], row2 = r2[kk];
+      if (row >= 0 && m0 + c4 < D1)
+        va = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(X1) +
+                                                   static_cast<int64_t>(row) * D1 + m0 + c4));
+      if (row2 >= 0 && n0 + c4 < D2)
+        vb = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(X2) +
+                                                   static_cast<int64_t>(row2) * D2 + n0 + c4));
+      *reinterpret_cast<float4*>(&As[kk][c4]) = va;
+      *reinterpret_cast<float4*>(&Bs[kk][c4]) = vb;
+    } else {
+      for (int i = tid; i < BK * BM; i += NT) {
+        const int kk = i / BM, c = i % BM;
+        const int row = r1[kk];
+        const int64_t m = m0 + c;
+        As[kk][c] = (row >= 0 && m < D1) ? ld(X1, static_cast<int64_t>(row) * D1 + m) : 0.f;
+        const int row2 = r2[kk];
+        const int64_t n = n0 + c;
+        Bs[kk][c] = (row2 >= 0 && n < D2) ? ld(X2, static_cast<int64_t>(row2) * D2 + n) : 0.f;
+      }
     }
     __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < BK; ++kk) {
-      float av[4], bv[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) av[i] = As[kk][ty * 4 + i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx * 4 + j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
-    }
+    mma_tile(As, Bs, acc, ty, tx);
     __syncthreads();
   }
   float* out = a.out + static_cast<int64_t>(tile.expert) * D1 * D2;
-  const bool split = tile.flags & 1;
+  const bool reduce = (tile.flags & 1) || gridDim.z > 1;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int64_t m = m0 + ty * 4 + i;
@@ -173,7 +249,7 @@ __global__ void __launch_bounds__(NT) estmm_simt_kernel(EstmmArgs a) {
     for (int j = 0; j < 4; ++j) {
       const int64_t n = n0 + tx * 4 + j;
       if (n >= D2) continue;
-      if (split) atomicAdd(out + m * D2 + n, acc[i][j]);
+      if (reduce) atomicAdd(out + m * D2 + n, acc[i][j]);
       else out[m * D2 + n] = acc[i][j];
     }
   }
@@ -199,21 +275,38 @@ __global__ void zero_split_kernel(const SegTile* tiles, const int32_t* n_tiles,
 
 }  // namespace
 
+bool vec_ok(const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; }
+
 hxm_status simt_esmm(hxm_dtype dt, const EsmmArgs& a, cudaStream_t st) {
   if (a.max_tiles <= 0) return HXM_OK;
-  dim3 grid(static_cast<unsigned>(ceil_div(a.d2, BN)), static_cast<unsigned>(a.max_tiles));
-  if (dt == HXM_BF16) esmm_simt_kernel<__nv_bfloat16><<<grid, NT, 0, st>>>(a);
-  else esmm_simt_kernel<float><<<grid, NT, 0, st>>>(a);
+  // split K for the reduction epilogue when the grid would not fill the GPU
+  int kz = 1;
+  if (a.epi == EPI_ATOMIC) {
+    const int64_t ctas = ceil_div(a.d2, BN) * a.max_tiles;
+    while (kz < 8 && ctas * kz < 2LL * sm_count() && ceil_div(a.d1, BK) >= 8 * kz) kz *= 2;
+  }
+  dim3 grid(static_cast<unsigned>(ceil_div(a.d2, BN)), static_cast<unsigned>(a.max_tiles), kz);
+  const bool vec = dt == HXM_F32 && a.d1 % 4 == 0 && a.d2 % 4 == 0 && vec_ok(a.a) && vec_ok(a.w);
+  if (dt == HXM_BF16) esmm_simt_kernel<__nv_bfloat16, false><<<grid, NT, 0, st>>>(a);
+  else if (vec) esmm_simt_kernel<float, true><<<grid, NT, 0, st>>>(a);
+  else esmm_simt_kernel<float, false><<<grid, NT, 0, st>>>(a);
   HXM_CHECK_LAUNCH();
   return HXM_OK;
 }
 
 hxm_status simt_estmm(hxm_dtype dt, const EstmmArgs& a, cudaStream_t st) {
   if (a.max_tiles <= 0) return HXM_OK;
+  const int64_t ctas = ceil_div(a.d1, BM) * ceil_div(a.d2, BN) * a.max_tiles;
+  int kz = 1;
+  while (kz < 8 && ctas * kz < 2LL * sm_count()) kz *= 2;
+  if (kz > 1)  // every split reduces into a zeroed output
+    HXM_TRY_CUDA(cudaMemsetAsync(a.out, 0, sizeof(float) * a.n_experts * a.d1 * a.d2, st));
   dim3 grid(static_cast<unsigned>(ceil_div(a.d1, BM) * ceil_div(a.d2, BN)),
-            static_cast<unsigned>(a.max_tiles));
-  if (dt == HXM_BF16) estmm_simt_kernel<__nv_bfloat16><<<grid, NT, 0, st>>>(a);
-  else estmm_simt_kernel<float><<<grid, NT, 0, st>>>(a);
+            static_cast<unsigned>(a.max_tiles), kz);
+  const bool vec = dt == HXM_F32 && a.d1 % 4 == 0 && a.d2 % 4 == 0 && vec_ok(a.x1) && vec_ok(a.x2);
+  if (dt == HXM_BF16) estmm_simt_kernel<__nv_bfloat16, false><<<grid, NT, 0, st>>>(a);
+  else if (vec) estmm_simt_kernel<float, true><<<grid, NT, 0, st>>>(a);
+  else estmm_simt_kernel<float, false><<<grid, NT, 0, st>>>(a);
   HXM_CHECK_LAUNCH();
   return HXM_OK;
 }
