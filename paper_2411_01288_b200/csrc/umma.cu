@@ -1176,19 +1176,21 @@ bool rev_on() {
   return on;
 }
 
-bool epi16_on() {
-  static const bool on = [] {
+int epi16_mode() {  // HXM_EPI16: 0 = never, 2 = always, default = short K only
+  static const int m = [] {
     const char* e = std::getenv("HXM_EPI16");
-    return !(e && e[0] == '0');
+    return e ? std::atoi(e) : 1;
   }();
-  return on;
+  return m;
 }
 template <int BN, int MODE, int CG, int ACT = -1>
 hxm_status launch_bn(const UParams& prm, int max_work, cudaStream_t st) {
   // only where the epilogue bounds the kernel: short K (<= 512, e.g. c2's
   // D = 384); at long K the MMA bounds it and 8 warps keep more ring stages
   if constexpr (epi_warps(BN, MODE) == 16) {
-    if (epi16_on() && prm.K <= 512) return launch_bn_ew<BN, MODE, CG, ACT, 16>(prm, max_work, st);
+    const int m = epi16_mode();
+    if (m == 2 || (m == 1 && prm.K <= 512))
+      return launch_bn_ew<BN, MODE, CG, ACT, 16>(prm, max_work, st);
   }
   return launch_bn_ew<BN, MODE, CG, ACT, 8>(prm, max_work, st);
 }
