@@ -290,6 +290,8 @@ def test_layer_c1_fp32_full_size():
     (16, 3, 128, 256, 192, 500, "identity", "zipf:1.3"),
     (64, 2, 128, 192, 128, 600, "gelu", "uniform"),    # many empty experts
     (4, 2, 12, 20, 6, 50, "gelu", "uniform"),          # unaligned dims
+    (8, 2, 640, 512, 640, 512, "gelu", "uniform"),     # K > 512: 8-warp stash epilogues
+    (8, 2, 128, 256, 256, 300, "relu", "uniform"),     # K <= 512: 16-warp stash epilogues
 ])
 def test_layer_bf16_vs_oracle(E, k, din, hid, dout, n, act, dist):
     p, x, r, gy = _layer_case(E, k, din, hid, dout, n, act, torch.bfloat16, E + n, dist)
