@@ -346,6 +346,60 @@ hxm_status bwd_prologue_typed(BwdPrologue& b, cudaStream_t st) {
   return HXM_OK;
 }
 
+
+// ---------------------------------------------- ESTMM operator relayout --
+// The operator API's ReIndex pads segments to the reference's blk (8); the
+// dense tcgen05 ESTMM reads 64-position k-blocks, which must not cross a
+// segment.  idx64[e] = sum_{e' < e} roundup64(len_e') (one block scan), then
+// both operands are gathered into that layout (pads -> zero rows).
+__global__ void relayout_index(const int64_t* __restrict__ idx, int E, int32_t* __restrict__ idx64) {
+  __shared__ int64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int e0 = 0; e0 < E; e0 += blockDim.x) {
+    // serial prefix over a block-sized slice (E is at most a few thousand)
+    __shared__ int64_t seg[1024];
+    const int e = e0 + threadIdx.x;
+    seg[threadIdx.x] = e < E ? (idx[e + 1] - idx[e] + 63) / 64 * 64 : 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < static_cast<int>(blockDim.x) && e0 + i < E; ++i) {
+        idx64[e0 + i] = static_cast<int32_t>(carry);
+        carry += seg[i];
+      }
+      if (e0 + static_cast<int>(blockDim.x) >= E) idx64[E] = static_cast<int32_t>(carry);
+    }
+    __syncthreads();
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(NT) gather_relayout(const T* __restrict__ x1, int64_t d1,
+                                                      const T* __restrict__ x2, int64_t d2,
+                                                      const int64_t* __restrict__ v,
+                                                      const int64_t* __restrict__ idx,
+                                                      const int32_t* __restrict__ idx64, int E,
+                                                      T* __restrict__ o1, T* __restrict__ o2) {
+  // one warp per new position; the expert by binary search over idx64
+  const int64_t np = idx64[E];
+  const int lane = threadIdx.x % 32;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (NT / 32);
+  for (int64_t p = static_cast<int64_t>(blockIdx.x) * (NT / 32) + threadIdx.x / 32; p < np;
+       p += nw) {
+    int lo = 0, hi = E;  // last e with idx64[e] <= p
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) / 2;
+      if (idx64[mid] <= p) lo = mid; else hi = mid;
+    }
+    const int64_t off = p - idx64[lo];
+    const int64_t src = off < idx[lo + 1] - idx[lo] ? v[idx[lo] + off] : -1;
+    for (int64_t c = lane; c < d1; c += 32)
+      o1[p * d1 + c] = src >= 0 ? x1[src * d1 + c] : from_f32<T>(0.f);
+    for (int64_t c = lane; c < d2; c += 32)
+      o2[p * d2 + c] = src >= 0 ? x2[src * d2 + c] : from_f32<T>(0.f);
+  }
+}
+
 }  // namespace
 
 hxm_status launch_gather_rows(hxm_dtype dt, const void* src, RowMap map, int64_t d,
@@ -355,6 +409,21 @@ hxm_status launch_gather_rows(hxm_dtype dt, const void* src, RowMap map, int64_t
   return dt == HXM_BF16
              ? gather_typed<__nv_bfloat16, int32_t>(src, map, d, idx, n_experts, bound, dst, st)
              : gather_typed<float, int32_t>(src, map, d, idx, n_experts, bound, dst, st);
+}
+
+hxm_status launch_estmm_relayout(const void* x1, int64_t d1, const void* x2, int64_t d2,
+                                  const int64_t* v, const int64_t* idx, int E, int64_t bound,
+                                  int32_t* idx64, void* o1, void* o2, cudaStream_t st) {
+  ProfScope ps(st, "estmm_relayout", 0.0, WORK_BYTES);
+  relayout_index<<<1, 1024, 0, st>>>(idx, E, idx64);
+  HXM_CHECK_LAUNCH();
+  const int blocks = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>(ceil_div(bound, NT / 32), static_cast<int64_t>(sm_count()) * 8)));
+  gather_relayout<__nv_bfloat16><<<blocks, NT, 0, st>>>(
+      static_cast<const __nv_bfloat16*>(x1), d1, static_cast<const __nv_bfloat16*>(x2), d2, v,
+      idx, idx64, E, static_cast<__nv_bfloat16*>(o1), static_cast<__nv_bfloat16*>(o2));
+  HXM_CHECK_LAUNCH();
+  return HXM_OK;
 }
 
 hxm_status launch_gather_rows64(hxm_dtype dt, const void* src, RowMap map, int64_t d,

@@ -42,12 +42,16 @@ struct OpWs {
   SegTile* ktiles;  // estmm chunks
   int32_t* ktile_off;
   int32_t* n_ktiles;
+  SegTile* ktiles64;  // bf16 ESTMM chunks over the relayout
   SegTile* etiles;  // ess tiles
   int32_t* etile_off;
   int32_t* n_etiles;
   float* partial;
   void* sorted;  // bf16 ESMM: the expert-sorted copy of the A rows (np_bound x d1)
-  int max_tiles, max_ktiles, max_etiles;
+  void* sorted2;   // bf16 ESTMM: the second operand, 64-position relayout
+  int32_t* idx64;  // bf16 ESTMM: segment offsets of the relayout
+  int64_t bound64;
+  int max_tiles, max_ktiles, max_etiles, max_ktiles64;
 };
 
 OpWs carve(Arena& ar, int64_t np_bound, int64_t E, int64_t d1, int64_t d2) {
@@ -65,9 +69,15 @@ OpWs carve(Arena& ar, int64_t np_bound, int64_t E, int64_t d1, int64_t d2) {
   w.etile_off = ar.take<int32_t>(E + 1);
   w.n_etiles = ar.take<int32_t>(1);
   w.partial = ar.take<float>(static_cast<size_t>(w.max_etiles) * std::max(d1, d2));
-  // 2-byte rows: only the bf16 tcgen05 path sorts its A operand
-  w.sorted = ar.take<char>(static_cast<size_t>(std::max<int64_t>(np_bound, 1)) *
+  // 2-byte rows: only the bf16 tcgen05 path sorts its operands.  The ESTMM
+  // relayout pads every segment to 64 positions: at most np_bound + 63 E rows.
+  w.bound64 = np_bound + 63 * E;
+  w.sorted = ar.take<char>(static_cast<size_t>(std::max<int64_t>(w.bound64, 1)) *
                            std::max(d1, d2) * 2);
+  w.sorted2 = ar.take<char>(static_cast<size_t>(std::max<int64_t>(w.bound64, 1)) * d2 * 2);
+  w.idx64 = ar.take<int32_t>(E + 1);
+  w.max_ktiles64 = static_cast<int>(max_tiles(w.bound64, E, kEstmmSplit));
+  w.ktiles64 = ar.take<SegTile>(w.max_ktiles64);
   return w;
 }
 
@@ -181,6 +191,30 @@ hxm_status hxm_estmm(hxm_dtype dt, const void* x1, const void* x2, int64_t n, in
   OpWs o = carve(ar, np_bound, E, d1, d2);
   if (ar.overflow) return invalid_arg("estmm: workspace too small");
   if (d1 == 0 || d2 == 0) return HXM_OK;
+  if (dt == HXM_BF16 && umma_supports_estmm(d1, d2)) {
+    // tcgen05 path: both operands gathered into a 64-position segment
+    // layout (one bandwidth-bound pass), then dense TMA tiles instead of a
+    // gather4 request per 4 rows
+    HXM_RETURN_IF(launch_estmm_relayout(x1, d1, x2, d2, v, idx, static_cast<int>(E), o.bound64,
+                                        o.idx64, o.sorted, o.sorted2, st));
+    HXM_RETURN_IF(launch_tiles<int32_t>(o.idx64, E, kEstmmChunk, true, o.ktiles64, o.ktile_off,
+                                        o.n_ktiles, st, kEstmmSplit));
+    EstmmArgs a{};
+    a.x1 = o.sorted;
+    a.m1 = map_dense();
+    a.x2 = o.sorted2;
+    a.m2 = map_dense();
+    a.x1_rows = o.bound64;
+    a.x2_rows = o.bound64;
+    a.d1 = d1;
+    a.d2 = d2;
+    a.tiles = o.ktiles64;
+    a.n_tiles = o.n_ktiles;
+    a.max_tiles = o.max_ktiles64;
+    a.n_experts = static_cast<int>(E);
+    a.out = out;
+    return launch_estmm(dt, a, st);
+  }
   HXM_RETURN_IF(launch_tiles<int64_t>(idx, E, kEstmmChunk, true, o.ktiles, o.ktile_off,
                                       o.n_ktiles, st));
   EstmmArgs a{};

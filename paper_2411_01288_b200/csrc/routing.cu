@@ -533,16 +533,16 @@ hxm_status build_reindex_slots(const int32_t* a, int64_t n_slots, int64_t E,
 template <class IdxT>
 hxm_status launch_tiles(const IdxT* idx, int64_t E, int rows, bool min_one,
                         SegTile* tiles, int32_t* tile_off, int32_t* n_tiles,
-                        cudaStream_t st) {
-  const TileSpec s{rows, min_one ? 1 : 0, tiles, tile_off, n_tiles};
+                        cudaStream_t st, int split_rows) {
+  const TileSpec s{rows, min_one ? 1 : 0, tiles, tile_off, n_tiles, split_rows};
   build_tiles<IdxT><<<1, 1024, 0, st>>>(idx, static_cast<int>(E), s, s, s, 1);
   HXM_CHECK_LAUNCH();
   return HXM_OK;
 }
 template hxm_status launch_tiles<int32_t>(const int32_t*, int64_t, int, bool, SegTile*,
-                                          int32_t*, int32_t*, cudaStream_t);
+                                          int32_t*, int32_t*, cudaStream_t, int);
 template hxm_status launch_tiles<int64_t>(const int64_t*, int64_t, int, bool, SegTile*,
-                                          int32_t*, int32_t*, cudaStream_t);
+                                          int32_t*, int32_t*, cudaStream_t, int);
 
 hxm_status launch_fwd_prologue(FwdPrologue a, cudaStream_t st) {
   a.chunk = pick_chunk(a.n_slots);

@@ -17,7 +17,7 @@ hxm_status build_reindex_slots(const int32_t* a, int64_t n_slots, int64_t E,
 template <class IdxT>
 hxm_status launch_tiles(const IdxT* idx, int64_t E, int rows, bool min_one,
                         SegTile* tiles, int32_t* tile_off, int32_t* n_tiles,
-                        cudaStream_t st);
+                        cudaStream_t st, int split_rows = 0);
 
 // Up to three tilings of the same index in one launch (the layer builds its
 // ESMM, ESTMM-chunk and ESS tables together).
