@@ -555,20 +555,25 @@ hxm_status launch_fwd_prologue(FwdPrologue a, cudaStream_t st) {
   const size_t smem = std::max(static_cast<size_t>(kWarps) * a.E * sizeof(int32_t),
                                (align_up(a.E + 1, 4) + static_cast<size_t>(kWarps) * a.E) *
                                    sizeof(int32_t));
-  static int occ_cache = 0;
-  static size_t occ_smem = 0;
-  if (smem > 48 * 1024 || occ_smem != smem) {
+  // per-device cache of the kernel attribute / occupancy query
+  static int occ_cache[64] = {0};
+  static size_t occ_smem[64] = {0};
+  int dev = 0;
+  HXM_TRY_CUDA(cudaGetDevice(&dev));
+  dev = dev < 64 ? dev : 63;
+  if (occ_smem[dev] != smem) {
     if (smem > 48 * 1024)
       HXM_TRY_CUDA(cudaFuncSetAttribute(fwd_prologue, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
-    HXM_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cache, fwd_prologue, kThreads,
-                                                               smem));
-    occ_smem = smem;
+    HXM_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cache[dev], fwd_prologue,
+                                                               kThreads, smem));
+    occ_smem[dev] = smem;
   }
-  if (occ_cache < 1) return invalid_arg("layer prologue: cannot be resident");
+  const int occ = occ_cache[dev];
+  if (occ < 1) return invalid_arg("layer prologue: cannot be resident");
   const char* ge = std::getenv("HXM_PRO_BLOCKS");
   const int per_sm = ge ? std::max(1, std::atoi(ge)) : 2;
-  const int grid = sm_count() * std::min(occ_cache, per_sm);
+  const int grid = sm_count() * std::min(occ, per_sm);
   void* args[] = {&a};
   HXM_TRY_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fwd_prologue), dim3(grid),
                                            dim3(kThreads), args, smem, st));

@@ -1129,10 +1129,13 @@ hxm_status launch_bn_ew(const UParams& prm_in, int max_work, cudaStream_t st) {
   using C = Cfg<BN, CG, MODE, EW>;
   auto kern = umma_kernel<BN, MODE, CG, ACT, EW>;
   constexpr int kThreads = 64 + 32 * EW;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static bool attr_set[64] = {false};  // kernel attributes are per device
+  int dev = 0;
+  HXM_TRY_CUDA(cudaGetDevice(&dev));
+  dev = dev < 64 ? dev : 63;
+  if (!attr_set[dev]) {
     HXM_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
-    attr_set = true;
+    attr_set[dev] = true;
   }
   const int sms = sm_count();
   if (sms <= 0) return invalid_arg("tcgen05 path: no CUDA device");
