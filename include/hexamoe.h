@@ -215,6 +215,62 @@ void hxm_make_layer_inputs(uint64_t seed, int64_t n_experts, int64_t d_in,
                            float* b2, float* x);
 
 /* ------------------------------------------------------------------------
+ * Fused GEMM -> reduce-scatter over peer memory (tensor parallelism along H).
+ *
+ * Under model-centric TP every rank computes the partial y (forward) and the
+ * partial g_x (backward) of ALL tokens on its H-slice; the reference sums
+ * them with an all-reduce (dist_sim.cpp:483-487, 542).  Here the ESMM
+ * epilogues reduce each output row straight into the buffer of the rank that
+ * owns the token -- row t goes to rank t / rows_per_rank, local row
+ * t % rows_per_rank -- through peer-mapped pointers (NVLink P2P / CUDA IPC),
+ * so the reduce-scatter overlaps the GEMM tile by tile and no collective runs
+ * afterwards.  Every rank's buffer must be zero before any rank launches, and
+ * complete (all ranks' kernels done) before its owner reads it:
+ * hxm_peer_barrier orders both over peer flags.
+ * ---------------------------------------------------------------------- */
+#define HXM_MAX_PEERS 8
+typedef struct hxm_peer_rows {
+  int32_t n_ranks;          /* P <= HXM_MAX_PEERS                          */
+  int32_t reserved;
+  int64_t rows_per_rank;    /* token rows owned per rank                   */
+  float* ptrs[HXM_MAX_PEERS]; /* rank r's rows_per_rank x D fp32 buffer, as
+                               mapped in this process                      */
+} hxm_peer_rows;
+
+/* hxm_moe_forward / hxm_moe_backward with y (resp. g_x) reduce-scattered to
+ * the owners instead of written to a local N x D buffer. */
+hxm_status hxm_moe_forward_tp(const hxm_layer_desc* desc, const void* x,
+                              const void* w1, const float* b1, const void* w2,
+                              const float* b2, const int32_t* assignments,
+                              const hxm_peer_rows* y_rows, void* workspace,
+                              size_t workspace_bytes, int32_t* status_dev,
+                              hxm_stream_t stream);
+hxm_status hxm_moe_backward_tp(const hxm_layer_desc* desc, const void* x,
+                               const void* w1, const void* w2, const void* g_y,
+                               void* workspace, size_t workspace_bytes,
+                               float* gw1, float* gb1, float* gw2, float* gb2,
+                               const hxm_peer_rows* gx_rows, hxm_stream_t stream);
+
+/* Peer-shareable device memory and its IPC handles (64 bytes). */
+hxm_status hxm_peer_malloc(size_t bytes, void** ptr);
+hxm_status hxm_peer_free(void* ptr);
+hxm_status hxm_ipc_get_handle(void* ptr, unsigned char handle[64]);
+hxm_status hxm_ipc_open_handle(const unsigned char handle[64], void** ptr);
+hxm_status hxm_ipc_close_handle(void* ptr);
+
+/* Device-side barrier over peer flags: flags.ptrs[r] is rank r's int32 flag
+ * array (HXM_MAX_PEERS entries, zero-initialised, mapped here).  Rank `rank`
+ * publishes `epoch` into every rank's slot [rank] (release, system scope) and
+ * waits until its own slots all reach `epoch` (acquire).  Epochs increase. */
+typedef struct hxm_peer_flags {
+  int32_t n_ranks;
+  int32_t rank;
+  int32_t* ptrs[HXM_MAX_PEERS];
+} hxm_peer_flags;
+hxm_status hxm_peer_barrier(const hxm_peer_flags* flags, int32_t epoch,
+                            hxm_stream_t stream);
+
+/* ------------------------------------------------------------------------
  * Live kernel timing (bench.py roofline) and launch counting.  When enabled,
  * every kernel region is bracketed by CUDA events on its launch stream.
  * ---------------------------------------------------------------------- */

@@ -40,6 +40,20 @@ class LayerDesc(C.Structure):
                 ("capacity", C.c_int32)]
 
 
+MAX_PEERS = 8
+
+
+class PeerRows(C.Structure):
+    """hxm_peer_rows (include/hexamoe.h): the token owners' receive buffers."""
+    _fields_ = [("n_ranks", C.c_int32), ("reserved", C.c_int32), ("rows_per_rank", C.c_int64),
+                ("ptrs", C.c_void_p * MAX_PEERS)]
+
+
+class PeerFlags(C.Structure):
+    """hxm_peer_flags (include/hexamoe.h): every rank's barrier flag array."""
+    _fields_ = [("n_ranks", C.c_int32), ("rank", C.c_int32), ("ptrs", C.c_void_p * MAX_PEERS)]
+
+
 _p = C.c_void_p
 _i64 = C.c_int64
 _sz = C.c_size_t
@@ -75,6 +89,16 @@ SIGNATURES = {
     "hxm_profile_read": (C.c_int, [C.c_int, C.c_char_p, C.c_int, _p, _p, _p, _p]),
     "hxm_profile_read2": (C.c_int, [C.c_int, C.c_char_p, C.c_int, _p, _p, _p, _p, _p]),
     "hxm_launch_count": (C.c_uint64, []),
+    "hxm_moe_forward_tp": (C.c_int, [C.POINTER(LayerDesc), _p, _p, _p, _p, _p, _p,
+                                     C.POINTER(PeerRows), _p, _sz, _p, _p]),
+    "hxm_moe_backward_tp": (C.c_int, [C.POINTER(LayerDesc), _p, _p, _p, _p, _p, _sz, _p, _p, _p,
+                                      _p, C.POINTER(PeerRows), _p]),
+    "hxm_peer_malloc": (C.c_int, [_sz, C.POINTER(C.c_void_p)]),
+    "hxm_peer_free": (C.c_int, [_p]),
+    "hxm_ipc_get_handle": (C.c_int, [_p, C.c_char_p]),
+    "hxm_ipc_open_handle": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
+    "hxm_ipc_close_handle": (C.c_int, [_p]),
+    "hxm_peer_barrier": (C.c_int, [C.POINTER(PeerFlags), C.c_int32, _p]),
 }
 
 

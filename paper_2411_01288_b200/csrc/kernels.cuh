@@ -64,6 +64,7 @@ struct EsmmArgs {
   void* out2;
   const void* y1s;  // BWD_ACT: pre-activation stash (dtype), row stride d2
   int reverse;      // tcgen05: work items last to first (see umma.cu)
+  const hxm_peer_rows* peer;  // EPI_ATOMIC: rows reduced into their owners' buffers
   float* colsum;    // BWD_ACT (tcgen05): per-(tile, CTA, lane group) column sums of out1,
                     // [((tile * CG + cta) * 4 + group) x d2] -> colsum_combine
 };

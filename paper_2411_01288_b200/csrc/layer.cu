@@ -167,18 +167,38 @@ uint64_t hxm_layer_forward_macs(const hxm_layer_desc* d) {
   return rows * (d->d_in * d->hidden + d->hidden * d->d_out);
 }
 
-hxm_status hxm_moe_forward(const hxm_layer_desc* d, const void* x, const void* w1,
-                           const float* b1, const void* w2, const float* b2,
-                           const int32_t* assignments, float* y, void* ws, size_t ws_bytes,
-                           int32_t* status, hxm_stream_t stream) {
+}  // extern "C"
+
+namespace hxm {
+namespace {
+hxm_status check_peer(const hxm_peer_rows* pr, const hxm_layer_desc* d, const LayerWs& w,
+                      const char* what) {
+  if (!pr) return HXM_OK;
+  if (pr->n_ranks < 1 || pr->n_ranks > HXM_MAX_PEERS || pr->rows_per_rank < 1 ||
+      pr->rows_per_rank * pr->n_ranks < d->n_tokens)
+    return invalid_arg(std::string(what) + ": peer rows must cover the N tokens on 1..8 ranks");
+  for (int r = 0; r < pr->n_ranks; ++r)
+    if (!pr->ptrs[r]) return invalid_arg(std::string(what) + ": null peer buffer");
+  if (w.rows_a < kUmmaRows)
+    return invalid_arg(std::string(what) + ": the fused reduce-scatter needs the bf16 tcgen05 path");
+  return HXM_OK;
+}
+}  // namespace
+
+// y (or, with `yp`, the owners' peer rows) = the layer forward
+hxm_status layer_forward(const hxm_layer_desc* d, const void* x, const void* w1,
+                         const float* b1, const void* w2, const float* b2,
+                         const int32_t* assignments, float* y, const hxm_peer_rows* yp,
+                         void* ws, size_t ws_bytes, int32_t* status, hxm_stream_t stream) {
   HXM_RETURN_IF(check_desc(d));
   const bool tok = d->n_tokens > 0;  // token tensors may be empty (null) when N == 0
-  if ((tok && (!x || !assignments || !y)) || !w1 || !b1 || !w2 || (d->add_b2 && !b2))
+  if ((tok && (!x || !assignments || (!y && !yp))) || !w1 || !b1 || !w2 || (d->add_b2 && !b2))
     return invalid_arg("moe_forward: null tensor");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   Arena ar(ws, ws_bytes);
   LayerWs w = carve(ar, *d);
   if (ar.overflow) return invalid_arg("moe_forward: workspace too small");
+  HXM_RETURN_IF(check_peer(yp, d, w, "moe_forward_tp"));
   const hxm_dtype dt = static_cast<hxm_dtype>(d->dtype);
   const int64_t N = d->n_tokens, E = d->n_experts, slots = d->k * N;
   // (0) one cooperative launch: routing validation, the k-choice slot index
@@ -205,7 +225,7 @@ hxm_status hxm_moe_forward(const hxm_layer_desc* d, const void* x, const void* w
     pro.unit = (pro.row_bytes % 16 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0) ? 16
                : (pro.row_bytes % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 4 == 0) ? 4 : 2;
     pro.y = y;
-    pro.y_elems = N * d->d_out;
+    pro.y_elems = yp ? 0 : N * d->d_out;  // peer rows: each owner zeroes its own
     pro.status = status;
     pro.ws = w.rws;
     pro.ws_bytes = w.rws_bytes;
@@ -262,25 +282,27 @@ hxm_status hxm_moe_forward(const hxm_layer_desc* d, const void* x, const void* w
   // y2 read, W2 read, y (fp32) written once
   a2.bytes = kn * d->hidden * es_ + w2bytes + 4.0 * N * d->d_out;
   a2.out_f32 = y;
+  a2.peer = yp;  // fused reduce-scatter into the token owners' rows
   a2.omap = slot;
   a2.reverse = 1;  // y2 rows written last by fwd1 are still in L2
   a2.out1 = a2.out2 = nullptr;
   return launch_esmm(dt, a2, st);
 }
 
-hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* w1,
-                            const void* w2, const void* g_y, void* ws, size_t ws_bytes,
-                            float* gw1, float* gb1, float* gw2, float* gb2, float* gx,
-                            hxm_stream_t stream) {
+hxm_status layer_backward(const hxm_layer_desc* d, const void* x, const void* w1,
+                          const void* w2, const void* g_y, void* ws, size_t ws_bytes,
+                          float* gw1, float* gb1, float* gw2, float* gb2, float* gx,
+                          const hxm_peer_rows* gxp, hxm_stream_t stream) {
   HXM_RETURN_IF(check_desc(d));
   const bool tok = d->n_tokens > 0;  // token tensors may be empty (null) when N == 0
-  if ((tok && (!x || !g_y || !gx)) || !w1 || !w2 || !gw1 || !gb1 || !gw2 ||
+  if ((tok && (!x || !g_y || (!gx && !gxp))) || !w1 || !w2 || !gw1 || !gb1 || !gw2 ||
       (d->add_b2 && !gb2))
     return invalid_arg("moe_backward: null tensor");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   Arena ar(ws, ws_bytes);
   LayerWs w = carve(ar, *d);
   if (ar.overflow) return invalid_arg("moe_backward: workspace too small");
+  HXM_RETURN_IF(check_peer(gxp, d, w, "moe_backward_tp"));
   const hxm_dtype dt = static_cast<hxm_dtype>(d->dtype);
   const int64_t N = d->n_tokens, E = d->n_experts;
   const int64_t Di = d->d_in, H = d->hidden, Do = d->d_out;
@@ -310,7 +332,7 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
     bp.label = "bwd_prologue";
     bp.es = es;
     bp.gx = gx;
-    bp.gx_elems = N * Di;
+    bp.gx_elems = gxp ? 0 : N * Di;  // peer rows: each owner zeroes its own
     bp.ktiles = w.ktiles;
     bp.n_ktiles = w.n_ktiles;
     bp.gw2 = gw2;
@@ -431,11 +453,50 @@ hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* 
   // g_y1 and W1 read, gx (fp32) written
   b10.bytes = kn * H * esz + static_cast<double>(E) * Di * H * esz + 4.0 * N * Di;
   b10.out_f32 = gx;
+  b10.peer = gxp;  // fused reduce-scatter into the token owners' rows
   b10.out1 = nullptr;
   b10.y1s = nullptr;
   HXM_RETURN_IF(launch_esmm(dt, b10, st));
   if (side.st) HXM_TRY_CUDA(cudaStreamWaitEvent(st, side.join, 0));
   return HXM_OK;
+}
+
+}  // namespace hxm
+
+extern "C" {
+
+hxm_status hxm_moe_forward(const hxm_layer_desc* d, const void* x, const void* w1,
+                           const float* b1, const void* w2, const float* b2,
+                           const int32_t* assignments, float* y, void* ws, size_t ws_bytes,
+                           int32_t* status, hxm_stream_t stream) {
+  return layer_forward(d, x, w1, b1, w2, b2, assignments, y, nullptr, ws, ws_bytes, status,
+                       stream);
+}
+
+hxm_status hxm_moe_forward_tp(const hxm_layer_desc* d, const void* x, const void* w1,
+                              const float* b1, const void* w2, const float* b2,
+                              const int32_t* assignments, const hxm_peer_rows* y_rows, void* ws,
+                              size_t ws_bytes, int32_t* status, hxm_stream_t stream) {
+  if (!y_rows) return invalid_arg("moe_forward_tp: null peer rows");
+  return layer_forward(d, x, w1, b1, w2, b2, assignments, nullptr, y_rows, ws, ws_bytes,
+                       status, stream);
+}
+
+hxm_status hxm_moe_backward(const hxm_layer_desc* d, const void* x, const void* w1,
+                            const void* w2, const void* g_y, void* ws, size_t ws_bytes,
+                            float* gw1, float* gb1, float* gw2, float* gb2, float* gx,
+                            hxm_stream_t stream) {
+  return layer_backward(d, x, w1, w2, g_y, ws, ws_bytes, gw1, gb1, gw2, gb2, gx, nullptr,
+                        stream);
+}
+
+hxm_status hxm_moe_backward_tp(const hxm_layer_desc* d, const void* x, const void* w1,
+                               const void* w2, const void* g_y, void* ws, size_t ws_bytes,
+                               float* gw1, float* gb1, float* gw2, float* gb2,
+                               const hxm_peer_rows* gx_rows, hxm_stream_t stream) {
+  if (!gx_rows) return invalid_arg("moe_backward_tp: null peer rows");
+  return layer_backward(d, x, w1, w2, g_y, ws, ws_bytes, gw1, gb1, gw2, gb2, nullptr, gx_rows,
+                        stream);
 }
 
 hxm_status hxm_moe_stash_export(const hxm_layer_desc* d, const void* ws, int64_t choice,

@@ -22,6 +22,7 @@ hxm_status launch_esmm(hxm_dtype dt, const EsmmArgs& a, cudaStream_t st) {
     return umma_esmm(a, st);
   }
   if (a.tile_rows > kSimtRows) return invalid_arg("esmm: bad tile rows");
+  if (a.peer) return invalid_arg("esmm: the fused reduce-scatter needs the tcgen05 path");
   return simt_esmm(dt, a, st);
 }
 

@@ -301,6 +301,11 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
                : "memory");
 }
 
+// scalar fp32 reduction that is valid on peer-mapped memory (NVLink / IPC)
+__device__ __forceinline__ void red_add_sys(float* p, float v) {
+  asm volatile("red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
 // UMMA shared-memory descriptor (sm100): start>>4 [0,14), LBO>>4 [16,30),
 // SBO>>4 [32,46), version=1 [46,48), layout SWIZZLE_128B=2 [61,64).
 // layout 2 = SWIZZLE_128B, 4 = SWIZZLE_64B.
@@ -382,6 +387,9 @@ struct UParams {
   int b_sw64;  // CG = 2, MN-major B halves of 32-column multiples: 64B-swizzled boxes
   int l2hint;  // MODE 1/2: L2 eviction-priority hints on the stash stores
   int reverse; // walk the work items last to first
+  int n_peer;            // EPI_ATOMIC: > 0 -> row t reduces into peer[t / peer_rows]
+  long long peer_rows;
+  float* peer[HXM_MAX_PEERS];
   int K, N, M;  // ESMM: K=d1, N=d2 ; ESTMM: M=d1, N=d2
   int n_nt, n_mt;
   const SegTile* tiles;
@@ -951,6 +959,16 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
                 const float4 val =
                     *reinterpret_cast<const float4*>(stg + rr * 64 + ((cc ^ ((rr >> 1) & 3)) * 16));
                 if (orr < 0 || (kTrace && (p.dbg_noload & 2))) continue;
+                if (p.n_peer > 0) {
+                  // fused reduce-scatter: the token's owner rank, over peer memory
+                  const int owner = static_cast<int>(orr / p.peer_rows);
+                  float* o = p.peer[owner] + (orr - owner * p.peer_rows) * N + n + 16 * h2 + cc * 4;
+                  red_add_sys(o, val.x);
+                  red_add_sys(o + 1, val.y);
+                  red_add_sys(o + 2, val.z);
+                  red_add_sys(o + 3, val.w);
+                  continue;
+                }
                 float* o = p.out_f32 + static_cast<int64_t>(orr) * N + n + 16 * h2 + cc * 4;
                 if (p.epi == EPI_WRITE) {
                   *reinterpret_cast<float4*>(o) = val;
@@ -1284,6 +1302,14 @@ hxm_status umma_esmm(const EsmmArgs& a, cudaStream_t st) {
   prm.n_tiles = a.n_tiles;
   prm.label = a.label;
   prm.reverse = a.reverse && rev_on();
+  if (a.peer) {
+    if (a.epi != EPI_ATOMIC || a.peer->n_ranks < 1 || a.peer->n_ranks > HXM_MAX_PEERS ||
+        a.peer->rows_per_rank < 1)
+      return invalid_arg("esmm: peer rows need the reduction epilogue and 1..8 ranks");
+    prm.n_peer = a.peer->n_ranks;
+    prm.peer_rows = a.peer->rows_per_rank;
+    for (int r = 0; r < prm.n_peer; ++r) prm.peer[r] = a.peer->ptrs[r];
+  }
   prm.epi = a.epi;
   prm.act = a.act;
   prm.bias = a.bias;

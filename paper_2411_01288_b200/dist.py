@@ -26,6 +26,7 @@ the CUDA layer in production and with a CPU reference in the gloo tests.
 """
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass, field
 from typing import Callable, List, Optional, Sequence
 
@@ -534,3 +535,174 @@ def _reduce_rows(t: torch.Tensor, counts: Sequence[int], group, how: str) -> tor
     out = torch.empty((m,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
     dist.reduce_scatter_tensor(out, torch.cat(parts), group=group)
     return out[:counts[r]]
+
+
+# ------------------------------------ fused GEMM -> reduce-scatter (peer) ---
+class _CudaArray:
+    """__cuda_array_interface__ view of a raw device pointer (torch.as_tensor)."""
+
+    def __init__(self, ptr: int, shape, typestr="<f4"):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3}
+
+
+class PeerBuffers:
+    """Per-rank receive buffers (rows x cols fp32) mapped into every rank, plus
+    a barrier flag array: the targets of hxm_moe_forward_tp /
+    hxm_moe_backward_tp, whose ESMM epilogues reduce each token's output row
+    into its owner's buffer over NVLink peer memory (CUDA IPC handles
+    exchanged through ``group``).  ``PeerBuffers.local`` builds the same table
+    from buffers of one process (single-GPU tests, no IPC)."""
+
+    def __init__(self, rows_per_rank: int, cols: int, group=None):
+        from ._lib import PeerFlags, PeerRows, check, lib
+        L = lib()
+        self.rows, self.cols = rows_per_rank, cols
+        self.P, self.rank = _ws(group), _rank(group)
+        if self.P > 8:
+            raise ValueError("PeerBuffers: at most 8 ranks (HXM_MAX_PEERS)")
+        self._own = []
+        buf, flg = C.c_void_p(), C.c_void_p()
+        check(L.hxm_peer_malloc(rows_per_rank * cols * 4, C.byref(buf)), "peer_malloc")
+        check(L.hxm_peer_malloc(8 * 4, C.byref(flg)), "peer_malloc")
+        self._own = [buf.value, flg.value]
+        hb, hf = C.create_string_buffer(64), C.create_string_buffer(64)
+        check(L.hxm_ipc_get_handle(buf, hb), "ipc_get_handle")
+        check(L.hxm_ipc_get_handle(flg, hf), "ipc_get_handle")
+        handles = [None] * self.P
+        dist.all_gather_object(handles, (hb.raw, hf.raw), group=group)
+        self._opened = []
+        bufs, flags = [], []
+        for r, (b, f) in enumerate(handles):
+            if r == self.rank:
+                bufs.append(buf.value)
+                flags.append(flg.value)
+                continue
+            pb, pf = C.c_void_p(), C.c_void_p()
+            check(L.hxm_ipc_open_handle(b, C.byref(pb)), "ipc_open_handle")
+            check(L.hxm_ipc_open_handle(f, C.byref(pf)), "ipc_open_handle")
+            self._opened += [pb.value, pf.value]
+            bufs.append(pb.value)
+            flags.append(pf.value)
+        self._tables(bufs, flags, PeerRows, PeerFlags)
+
+    @classmethod
+    def local(cls, tensors: Sequence[torch.Tensor], rank: int = 0):
+        """Table over same-process fp32 buffers (simulated ranks on one GPU)."""
+        from ._lib import PeerFlags, PeerRows
+        self = cls.__new__(cls)
+        self.rows, self.cols = tensors[0].shape
+        self.P, self.rank = len(tensors), rank
+        self._own, self._opened = [], []
+        self._keep = list(tensors)
+        self._flags = torch.zeros(self.P, 8, dtype=torch.int32, device=tensors[0].device)
+        self._tables([t.data_ptr() for t in tensors],
+                     [self._flags[r].data_ptr() for r in range(self.P)], PeerRows, PeerFlags)
+        return self
+
+    def _tables(self, bufs, flags, PeerRows, PeerFlags):
+        self.bufs = bufs
+        self.rows_struct = PeerRows()
+        self.rows_struct.n_ranks, self.rows_struct.rows_per_rank = self.P, self.rows
+        self.flags_struct = PeerFlags()
+        self.flags_struct.n_ranks, self.flags_struct.rank = self.P, self.rank
+        for r in range(self.P):
+            self.rows_struct.ptrs[r] = bufs[r]
+            self.flags_struct.ptrs[r] = flags[r]
+        self.epoch = 0
+
+    def view(self, rank: Optional[int] = None) -> torch.Tensor:
+        """torch view of rank's buffer (default: this rank's own rows)."""
+        r = self.rank if rank is None else rank
+        return torch.as_tensor(_CudaArray(self.bufs[r], (self.rows, self.cols)), device="cuda")
+
+    def barrier(self, stream=None) -> None:
+        from ._lib import check, lib
+        self.epoch += 1
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        check(lib().hxm_peer_barrier(C.byref(self.flags_struct), self.epoch, st), "peer_barrier")
+
+    def close(self) -> None:
+        from ._lib import lib
+        L = lib()
+        for p in self._opened:
+            L.hxm_ipc_close_handle(C.c_void_p(p))
+        for p in self._own:
+            L.hxm_peer_free(C.c_void_p(p))
+        self._opened, self._own = [], []
+
+
+def layer_forward_tp(x, params, assignments, y_rows: "PeerBuffers", add_b2: bool,
+                     workspace=None, dtype=torch.bfloat16):
+    """One rank's model-centric forward with y reduce-scattered inside the
+    ESMM epilogue (hxm_moe_forward_tp).  Returns the stash handle for
+    layer_backward_tp.  The caller orders the owners' zeroing and reads with
+    PeerBuffers.barrier."""
+    from ._lib import check, lib
+    from .moe_layer import ForwardStash, layer_workspace, make_desc
+    k, n = assignments.shape
+    p = params
+    desc = make_desc(n, p.experts(), k, p.d_in(), p.hidden(), p.d_out(), p.activation, dtype,
+                     add_b2 and p.b2 is not None)
+    ws = workspace if workspace is not None else layer_workspace(desc, x.device)
+    b1 = p.b1.to(torch.float32).contiguous()
+    b2 = p.b2.to(torch.float32).contiguous() if (add_b2 and p.b2 is not None) else None
+    check(lib().hxm_moe_forward_tp(C.byref(desc), x.contiguous().data_ptr(), p.w1.data_ptr(),
+                                   b1.data_ptr(), p.w2.data_ptr(),
+                                   None if b2 is None else b2.data_ptr(),
+                                   assignments.to(torch.int32).contiguous().data_ptr(),
+                                   C.byref(y_rows.rows_struct), ws.data_ptr(), ws.numel(), None,
+                                   torch.cuda.current_stream().cuda_stream), "moe_forward_tp")
+    return ForwardStash(desc, ws, x, "memory_efficient", 8)
+
+
+def layer_backward_tp(stash, params, g_y, gx_rows: "PeerBuffers"):
+    """The matching backward: parameter gradients of this rank's H-slice
+    (local), g_x reduce-scattered to the token owners inside the ESMM epilogue."""
+    from ._lib import check, lib
+    from .moe_layer import MoeGrads
+    p, d = params, stash.desc
+    f = dict(dtype=torch.float32, device=g_y.device)
+    E, Di, H, Do = p.experts(), p.d_in(), p.hidden(), p.d_out()
+    g = MoeGrads(torch.empty(E, Di, H, **f), torch.empty(E, H, **f), torch.empty(E, H, Do, **f),
+                 torch.empty(E, Do, **f) if d.add_b2 else None, None)
+    check(lib().hxm_moe_backward_tp(C.byref(d), stash.x.data_ptr(), p.w1.data_ptr(),
+                                    p.w2.data_ptr(), g_y.contiguous().data_ptr(),
+                                    stash.workspace.data_ptr(), stash.workspace.numel(),
+                                    g.gw1.data_ptr(), g.gb1.data_ptr(), g.gw2.data_ptr(),
+                                    None if g.gb2 is None else g.gb2.data_ptr(),
+                                    C.byref(gx_rows.rows_struct),
+                                    torch.cuda.current_stream().cuda_stream), "moe_backward_tp")
+    return g
+
+
+def model_centric_step_fused(local_x, local_assign, local_gy, shard: ParamShard, b2,
+                             activation: str, ybuf: "PeerBuffers", gxbuf: "PeerBuffers",
+                             group=None) -> DistStepResult:
+    """dist_sim.cpp:454-601 with the two activation reductions fused into the
+    GEMMs: every rank computes the global batch on its H-slice and its ESMM
+    epilogues reduce y (forward) and g_x (backward) straight into the token
+    owners' buffers over peer memory -- no NCCL reduce-scatter afterwards.
+    Token shares must be even (rows_per_rank = local batch)."""
+    from .moe_layer import MoeGrads, MoeLayerParams
+    r = _rank(group)
+    counts = _row_counts(local_x.shape[0], group, local_x.device)
+    if len(set(counts)) != 1 or counts[0] != ybuf.rows:
+        raise ValueError("model_centric_step_fused: even token shares of ybuf.rows required")
+    x = all_gather_rows(local_x, counts, group)
+    a = all_gather_rows(local_assign.t().contiguous(), counts, group).t().contiguous()
+    p = MoeLayerParams(shard.w1, shard.b1, shard.w2, b2 if r == 0 else None, activation)
+    ybuf.view().zero_()
+    ybuf.barrier()  # every owner's rows are zero before any rank reduces
+    stash = layer_forward_tp(x, p, a, ybuf, r == 0, dtype=x.dtype)
+    ybuf.barrier()  # every rank's contributions have landed
+    y = ybuf.view().clone()
+    gy = all_gather_rows(local_gy, counts, group)
+    gxbuf.view().zero_()
+    gxbuf.barrier()
+    g = layer_backward_tp(stash, p, gy, gxbuf)
+    gxbuf.barrier()
+    gx = gxbuf.view().clone()
+    log = ["token_all_gather", "output_fused_reduce_scatter", "grad_all_gather",
+           "input_grad_fused_reduce_scatter"]
+    return DistStepResult(y, MoeGrads(g.gw1, g.gb1, g.gw2, g.gb2 if r == 0 else None, gx), log)
