@@ -263,9 +263,19 @@ def run_ours(args, cfg, rank, ws, local):
         del p, sp
         comp = HD.cuda_compute()
         mc_out = {}
+        fused = not args.no_fused and cfg["dtype"] == "bf16"
+        if fused:
+            # y / g_x reduce-scattered inside the ESMM epilogues over peer
+            # memory (CUDA IPC handles, device barrier) -- no NCCL afterwards
+            ybuf = HD.PeerBuffers(N, D)
+            gxbuf = HD.PeerBuffers(N, D)
 
         def mc_step():
-            res = HD.model_centric_step(x, a, gy, shard, b2, "gelu", comp, reduce="reduce_scatter")
+            if fused:
+                res = HD.model_centric_step_fused(x, a, gy, shard, b2, "gelu", ybuf, gxbuf)
+            else:
+                res = HD.model_centric_step(x, a, gy, shard, b2, "gelu", comp,
+                                            reduce="reduce_scatter")
             mc_out["y"] = res.y
             return res
         mc_step()
@@ -452,7 +462,9 @@ def run_ours(args, cfg, rank, ws, local):
         "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
         "config": {"workload": args.config, "desc": cfg["desc"], "E": E, "k": k, "d": D,
                    "ffn": Hd, "tokens_per_gpu": N, "routing": cfg["dist"],
-                   "parallelism": f"{mode}_tp{ws}" if mode != "single" else "single",
+                   "parallelism": (f"{mode}_tp{ws}" + ("_fused_rs" if mode == "model_centric" and
+                                                         not args.no_fused else ""))
+                   if mode != "single" else "single",
                    "formulation": (f"conventional dispatch/combine, capacity factor "
                                    f"{args.capacity_factor}") if args.capacity_factor > 0
                    else "expert-specific (no padding, no dropping)",
@@ -485,6 +497,8 @@ def main():
     ap.add_argument("--mode", default="auto",
                     choices=["auto", "single", "data_centric", "model_centric"],
                     help="auto: single GPU at N=1, data-centric TP along H at N>1")
+    ap.add_argument("--no-fused", action="store_true",
+                    help="model-centric: NCCL reduce-scatter instead of the fused GEMM epilogues")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the step eagerly instead of replaying its CUDA graph")
     ap.add_argument("--capacity-factor", type=float, default=0.0,
