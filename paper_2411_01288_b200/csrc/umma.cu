@@ -301,11 +301,6 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
                : "memory");
 }
 
-// scalar fp32 reduction that is valid on peer-mapped memory (NVLink / IPC)
-__device__ __forceinline__ void red_add_sys(float* p, float v) {
-  asm volatile("red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
-}
-
 // UMMA shared-memory descriptor (sm100): start>>4 [0,14), LBO>>4 [16,30),
 // SBO>>4 [32,46), version=1 [46,48), layout SWIZZLE_128B=2 [61,64).
 // layout 2 = SWIZZLE_128B, 4 = SWIZZLE_64B.
@@ -963,10 +958,10 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
                   // fused reduce-scatter: the token's owner rank, over peer memory
                   const int owner = static_cast<int>(orr / p.peer_rows);
                   float* o = p.peer[owner] + (orr - owner * p.peer_rows) * N + n + 16 * h2 + cc * 4;
-                  red_add_sys(o, val.x);
-                  red_add_sys(o + 1, val.y);
-                  red_add_sys(o + 2, val.z);
-                  red_add_sys(o + 3, val.w);
+                  // atomicity is provided where the memory lives (the owner's L2);
+                  // ordering against the owner's reads comes from the kernel
+                  // boundary + hxm_peer_barrier (release / acquire, .sys)
+                  red_add_v4(o, val.x, val.y, val.z, val.w);
                   continue;
                 }
                 float* o = p.out_f32 + static_cast<int64_t>(orr) * N + n + 16 * h2 + cc * 4;
