@@ -251,6 +251,18 @@ hxm_status hxm_moe_backward_tp(const hxm_layer_desc* desc, const void* x,
                                float* gw1, float* gb1, float* gw2, float* gb2,
                                const hxm_peer_rows* gx_rows, hxm_stream_t stream);
 
+/* Data-centric TP: the weight gradients reduce-scattered along H inside the
+ * ESTMM epilogues -- gW1 (E x D_i x H) columns h go to rank h / span as its
+ * E x D_i x span shard, gW2 (E x H x D_o) rows h to rank h / span as its
+ * E x span x D_o shard (span = rows_per_rank of the tables; the reference
+ * all-reduces them, dist_sim.cpp:397-398).  gb1, gb2, g_x stay local. */
+hxm_status hxm_moe_backward_dc(const hxm_layer_desc* desc, const void* x,
+                               const void* w1, const void* w2, const void* g_y,
+                               void* workspace, size_t workspace_bytes,
+                               const hxm_peer_rows* gw1_shards, float* gb1,
+                               const hxm_peer_rows* gw2_shards, float* gb2,
+                               float* gx, hxm_stream_t stream);
+
 /* Peer-shareable device memory and its IPC handles (64 bytes). */
 hxm_status hxm_peer_malloc(size_t bytes, void** ptr);
 hxm_status hxm_peer_free(void* ptr);

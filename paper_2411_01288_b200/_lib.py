@@ -93,6 +93,8 @@ SIGNATURES = {
                                      C.POINTER(PeerRows), _p, _sz, _p, _p]),
     "hxm_moe_backward_tp": (C.c_int, [C.POINTER(LayerDesc), _p, _p, _p, _p, _p, _sz, _p, _p, _p,
                                       _p, C.POINTER(PeerRows), _p]),
+    "hxm_moe_backward_dc": (C.c_int, [C.POINTER(LayerDesc), _p, _p, _p, _p, _p, _sz,
+                                      C.POINTER(PeerRows), _p, C.POINTER(PeerRows), _p, _p, _p]),
     "hxm_peer_malloc": (C.c_int, [_sz, C.POINTER(C.c_void_p)]),
     "hxm_peer_free": (C.c_int, [_p]),
     "hxm_ipc_get_handle": (C.c_int, [_p, C.c_char_p]),

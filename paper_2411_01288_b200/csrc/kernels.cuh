@@ -85,6 +85,8 @@ struct EstmmArgs {
   int n_experts;
   float* out;  // E x d1 x d2
   int reverse;      // tcgen05: work items last to first
+  const hxm_peer_rows* peer;  // tcgen05: reduce-scatter to H-shard owners (out unused)
+  int peer_dim;               // 0: d1 (rows) is the split H extent, 1: d2 (columns)
   int skip_zero_split;  // split experts' slices already zeroed by the caller
 };
 

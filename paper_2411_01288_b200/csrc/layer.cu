@@ -292,17 +292,21 @@ hxm_status layer_forward(const hxm_layer_desc* d, const void* x, const void* w1,
 hxm_status layer_backward(const hxm_layer_desc* d, const void* x, const void* w1,
                           const void* w2, const void* g_y, void* ws, size_t ws_bytes,
                           float* gw1, float* gb1, float* gw2, float* gb2, float* gx,
-                          const hxm_peer_rows* gxp, hxm_stream_t stream) {
+                          const hxm_peer_rows* gxp, hxm_stream_t stream,
+                          const hxm_peer_rows* gw1p = nullptr,
+                          const hxm_peer_rows* gw2p = nullptr) {
   HXM_RETURN_IF(check_desc(d));
   const bool tok = d->n_tokens > 0;  // token tensors may be empty (null) when N == 0
-  if ((tok && (!x || !g_y || (!gx && !gxp))) || !w1 || !w2 || !gw1 || !gb1 || !gw2 ||
-      (d->add_b2 && !gb2))
+  if ((tok && (!x || !g_y || (!gx && !gxp))) || !w1 || !w2 || (!gw1 && !gw1p) || !gb1 ||
+      (!gw2 && !gw2p) || (d->add_b2 && !gb2))
     return invalid_arg("moe_backward: null tensor");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   Arena ar(ws, ws_bytes);
   LayerWs w = carve(ar, *d);
   if (ar.overflow) return invalid_arg("moe_backward: workspace too small");
   HXM_RETURN_IF(check_peer(gxp, d, w, "moe_backward_tp"));
+  if ((gw1p || gw2p) && w.rows_a < kUmmaRows)
+    return invalid_arg("moe_backward_dc: the fused reduce-scatter needs the bf16 tcgen05 path");
   const hxm_dtype dt = static_cast<hxm_dtype>(d->dtype);
   const int64_t N = d->n_tokens, E = d->n_experts;
   const int64_t Di = d->d_in, H = d->hidden, Do = d->d_out;
@@ -335,9 +339,9 @@ hxm_status layer_backward(const hxm_layer_desc* d, const void* x, const void* w1
     bp.gx_elems = gxp ? 0 : N * Di;  // peer rows: each owner zeroes its own
     bp.ktiles = w.ktiles;
     bp.n_ktiles = w.n_ktiles;
-    bp.gw2 = gw2;
+    bp.gw2 = gw2p ? nullptr : gw2;  // peer shards are zeroed by their owners
     bp.gw2_slice = H * Do;
-    bp.gw1 = gw1;
+    bp.gw1 = gw1p ? nullptr : gw1;
     bp.gw1_slice = Di * H;
     // algorithmic bytes: g_y read once per routed slot, its sorted copy
     // written, gb2 written, gx zeroed (split-expert zeroing is data-dependent)
@@ -361,6 +365,8 @@ hxm_status layer_backward(const hxm_layer_desc* d, const void* x, const void* w1
   t2.n_experts = static_cast<int>(E);
   t2.out = gw2;
   t2.skip_zero_split = 1;  // done by the backward prologue
+  t2.peer = gw2p;          // data-centric: rows (H) reduce-scattered to the owners
+  t2.peer_dim = 0;
   t2.label = "estmm_gw2";
   t2.work = 2.0 * kn * H * Do;
   // y2 and the sorted g_y read, gW2 (fp32) written
@@ -434,6 +440,8 @@ hxm_status layer_backward(const hxm_layer_desc* d, const void* x, const void* w1
   t1.d2 = H;
   t1.out = gw1;
   t1.reverse = 1;  // g_y1 rows written last by bwd_act are still in L2
+  t1.peer = gw1p;  // data-centric: columns (H) reduce-scattered to the owners
+  t1.peer_dim = 1;
   t1.label = "estmm_gw1";
   t1.work = 2.0 * kn * Di * H;
   t1.bytes = kn * (Di + H) * esz + 4.0 * E * Di * H;
@@ -497,6 +505,16 @@ hxm_status hxm_moe_backward_tp(const hxm_layer_desc* d, const void* x, const voi
   if (!gx_rows) return invalid_arg("moe_backward_tp: null peer rows");
   return layer_backward(d, x, w1, w2, g_y, ws, ws_bytes, gw1, gb1, gw2, gb2, nullptr, gx_rows,
                         stream);
+}
+
+hxm_status hxm_moe_backward_dc(const hxm_layer_desc* d, const void* x, const void* w1,
+                               const void* w2, const void* g_y, void* ws, size_t ws_bytes,
+                               const hxm_peer_rows* gw1_shards, float* gb1,
+                               const hxm_peer_rows* gw2_shards, float* gb2, float* gx,
+                               hxm_stream_t stream) {
+  if (!gw1_shards || !gw2_shards) return invalid_arg("moe_backward_dc: null peer shards");
+  return layer_backward(d, x, w1, w2, g_y, ws, ws_bytes, nullptr, gb1, nullptr, gb2, gx,
+                        nullptr, stream, gw1_shards, gw2_shards);
 }
 
 hxm_status hxm_moe_stash_export(const hxm_layer_desc* d, const void* ws, int64_t choice,

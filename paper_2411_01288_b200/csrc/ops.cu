@@ -28,6 +28,11 @@ hxm_status launch_esmm(hxm_dtype dt, const EsmmArgs& a, cudaStream_t st) {
 
 hxm_status launch_estmm(hxm_dtype dt, const EstmmArgs& a, cudaStream_t st) {
   ProfScope ps(st, a.label ? a.label : "estmm", a.work, WORK_FLOP, a.bytes);
+  if (a.peer) {  // owners zero their shards; every tile reduces
+    if (dt != HXM_BF16 || !umma_supports_estmm(a.d1, a.d2))
+      return invalid_arg("estmm: the fused reduce-scatter needs the tcgen05 path");
+    return umma_estmm(a, st);
+  }
   if (!a.skip_zero_split)
     HXM_RETURN_IF(zero_split_experts(a.tiles, a.n_tiles, a.max_tiles, a.d1 * a.d2, a.out, st));
   if (dt == HXM_BF16 && umma_supports_estmm(a.d1, a.d2)) return umma_estmm(a, st);

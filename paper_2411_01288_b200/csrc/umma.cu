@@ -383,6 +383,7 @@ struct UParams {
   int l2hint;  // MODE 1/2: L2 eviction-priority hints on the stash stores
   int reverse; // walk the work items last to first
   int n_peer;            // EPI_ATOMIC: > 0 -> row t reduces into peer[t / peer_rows]
+  int peer_dim;          // ESTMM: 0 = output rows, 1 = output columns split over peers
   long long peer_rows;
   float* peer[HXM_MAX_PEERS];
   int K, N, M;  // ESMM: K=d1, N=d2 ; ESTMM: M=d1, N=d2
@@ -1031,6 +1032,23 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
               const float4 val =
                   *reinterpret_cast<const float4*>(stg + rr * 64 + ((cc ^ ((rr >> 1) & 3)) * 16));
               if (m0 + rr >= p.M || (kTrace && (p.dbg_noload & 2))) continue;
+              if (p.n_peer > 0) {
+                // fused reduce-scatter of the weight gradient along H to the
+                // shard owners: rows (peer_dim 0, gW2) or columns (1, gW1)
+                const int64_t m = m0 + rr, n = n0 + c0 + 16 * h2 + cc * 4;
+                const int64_t span = p.peer_rows;
+                float* o;
+                if (p.peer_dim == 0) {
+                  const int owner = static_cast<int>(m / span);
+                  o = p.peer[owner] + (t.expert * span + (m - owner * span)) * p.N + n;
+                } else {
+                  const int owner = static_cast<int>(n / span);
+                  o = p.peer[owner] + (t.expert * static_cast<int64_t>(p.M) + m) * span +
+                      (n - owner * span);
+                }
+                if (!empty_seg) red_add_v4(o, val.x, val.y, val.z, val.w);
+                continue;
+              }
               float* o = obase + static_cast<int64_t>(m0 + rr) * p.N + n0 + c0 + 16 * h2 + cc * 4;
               if (split && !empty_seg) red_add_v4(o, val.x, val.y, val.z, val.w);
               else *reinterpret_cast<float4*>(o) = val;
@@ -1401,6 +1419,16 @@ hxm_status umma_estmm(const EstmmArgs& a, cudaStream_t st) {
   prm.est_out = a.out;
   prm.label = a.label;
   prm.reverse = a.reverse && rev_on();
+  if (a.peer) {  // gW reduce-scattered to the owners' H-shards
+    const int64_t span = a.peer->rows_per_rank, ext = a.peer_dim == 0 ? a.d1 : a.d2;
+    if (a.peer->n_ranks < 1 || a.peer->n_ranks > HXM_MAX_PEERS || span < 1 ||
+        span * a.peer->n_ranks != ext || span % 4 != 0)
+      return invalid_arg("estmm: peer shards must split the H extent evenly (multiple of 4)");
+    prm.n_peer = a.peer->n_ranks;
+    prm.peer_rows = span;
+    prm.peer_dim = a.peer_dim;
+    for (int r = 0; r < prm.n_peer; ++r) prm.peer[r] = a.peer->ptrs[r];
+  }
   const int work = a.max_tiles * prm.n_mt * prm.n_nt;
   if (CG == 2) return launch_bn_any<3, 2>(bn, prm, work, st);
   return launch_bn_any<3, 1>(bn, prm, work, st);

@@ -554,16 +554,22 @@ class PeerBuffers:
     exchanged through ``group``).  ``PeerBuffers.local`` builds the same table
     from buffers of one process (single-GPU tests, no IPC)."""
 
-    def __init__(self, rows_per_rank: int, cols: int, group=None):
+    def __init__(self, rows_per_rank: int, cols: int, group=None, shape=None):
+        """rows_per_rank x cols fp32 per rank; or any per-rank ``shape`` with
+        ``rows_per_rank`` the H span each rank owns (weight-gradient shards)."""
         from ._lib import PeerFlags, PeerRows, check, lib
         L = lib()
         self.rows, self.cols = rows_per_rank, cols
+        self.shape = tuple(shape) if shape is not None else (rows_per_rank, cols)
         self.P, self.rank = _ws(group), _rank(group)
         if self.P > 8:
             raise ValueError("PeerBuffers: at most 8 ranks (HXM_MAX_PEERS)")
         self._own = []
         buf, flg = C.c_void_p(), C.c_void_p()
-        check(L.hxm_peer_malloc(rows_per_rank * cols * 4, C.byref(buf)), "peer_malloc")
+        nelem = 1
+        for v in self.shape:
+            nelem *= v
+        check(L.hxm_peer_malloc(nelem * 4, C.byref(buf)), "peer_malloc")
         check(L.hxm_peer_malloc(8 * 4, C.byref(flg)), "peer_malloc")
         self._own = [buf.value, flg.value]
         hb, hf = C.create_string_buffer(64), C.create_string_buffer(64)
@@ -587,11 +593,14 @@ class PeerBuffers:
         self._tables(bufs, flags, PeerRows, PeerFlags)
 
     @classmethod
-    def local(cls, tensors: Sequence[torch.Tensor], rank: int = 0):
-        """Table over same-process fp32 buffers (simulated ranks on one GPU)."""
+    def local(cls, tensors: Sequence[torch.Tensor], rank: int = 0, span: Optional[int] = None):
+        """Table over same-process fp32 buffers (simulated ranks on one GPU);
+        ``span``: the H extent each buffer owns (default: its row count)."""
         from ._lib import PeerFlags, PeerRows
         self = cls.__new__(cls)
-        self.rows, self.cols = tensors[0].shape
+        self.shape = tuple(tensors[0].shape)
+        self.rows = span if span is not None else tensors[0].shape[0]
+        self.cols = tensors[0].shape[-1]
         self.P, self.rank = len(tensors), rank
         self._own, self._opened = [], []
         self._keep = list(tensors)
@@ -614,7 +623,7 @@ class PeerBuffers:
     def view(self, rank: Optional[int] = None) -> torch.Tensor:
         """torch view of rank's buffer (default: this rank's own rows)."""
         r = self.rank if rank is None else rank
-        return torch.as_tensor(_CudaArray(self.bufs[r], (self.rows, self.cols)), device="cuda")
+        return torch.as_tensor(_CudaArray(self.bufs[r], self.shape), device="cuda")
 
     def barrier(self, stream=None) -> None:
         from ._lib import check, lib
@@ -706,3 +715,57 @@ def model_centric_step_fused(local_x, local_assign, local_gy, shard: ParamShard,
     log = ["token_all_gather", "output_fused_reduce_scatter", "grad_all_gather",
            "input_grad_fused_reduce_scatter"]
     return DistStepResult(y, MoeGrads(g.gw1, g.gb1, g.gw2, g.gb2 if r == 0 else None, gx), log)
+
+
+def layer_backward_dc(stash, params, g_y, gw1_shards: "PeerBuffers", gw2_shards: "PeerBuffers"):
+    """Data-centric backward with the weight gradients reduce-scattered along
+    H inside the ESTMM epilogues (hxm_moe_backward_dc): gW1 columns / gW2 rows
+    land, summed over ranks, in their owner's E x D_i x span / E x span x D_o
+    shard.  Returns this rank's full gb1, gb2 and g_x (reduced by the caller)."""
+    from ._lib import check, lib
+    p, d = params, stash.desc
+    f = dict(dtype=torch.float32, device=g_y.device)
+    gb1 = torch.empty(p.experts(), p.hidden(), **f)
+    gb2 = torch.empty(p.experts(), p.d_out(), **f) if d.add_b2 else None
+    gx = torch.empty(g_y.shape[0], p.d_in(), **f)
+    check(lib().hxm_moe_backward_dc(C.byref(d), stash.x.data_ptr(), p.w1.data_ptr(),
+                                    p.w2.data_ptr(), g_y.contiguous().data_ptr(),
+                                    stash.workspace.data_ptr(), stash.workspace.numel(),
+                                    C.byref(gw1_shards.rows_struct), gb1.data_ptr(),
+                                    C.byref(gw2_shards.rows_struct),
+                                    None if gb2 is None else gb2.data_ptr(), gx.data_ptr(),
+                                    torch.cuda.current_stream().cuda_stream), "moe_backward_dc")
+    return gb1, gb2, gx
+
+
+def data_centric_step_fused(local_x, local_assign, local_gy, shard: ParamShard, b2, hidden_sizes,
+                            activation: str, gw1_shards: "PeerBuffers", gw2_shards: "PeerBuffers",
+                            group=None, side_stream: Optional[torch.cuda.Stream] = None):
+    """dist_sim.cpp:352-452 with the weight-gradient reduce-scatter fused into
+    the ESTMM epilogues: parameters all-gathered (NCCL) into the cache, the
+    full layer run on this rank's tokens, gW1 / gW2 reduced straight into the
+    shard owners' buffers over peer memory; the small gb1 / gb2 are reduced
+    with NCCL.  Even hidden shares; returns this rank's shards (as
+    data_centric_step(grad_reduce="reduce_scatter"))."""
+    from .moe_layer import MoeGrads
+    from .moe_layer import moe_forward
+    if len(set(hidden_sizes)) != 1:
+        raise ValueError("data_centric_step_fused: even hidden shares required")
+    r, h = _rank(group), hidden_sizes[0]
+    full = gather_params(shard, b2, hidden_sizes, activation, group, side_stream)
+    if side_stream is not None:
+        torch.cuda.current_stream().wait_stream(side_stream)
+    fw = moe_forward(local_x, full, local_assign, validate=False)
+    gw1_shards.view().zero_()
+    gw2_shards.view().zero_()
+    gw1_shards.barrier()  # every owner's shards are zero before any rank reduces
+    gw2_shards.barrier()
+    gb1, gb2, gx = layer_backward_dc(fw.stash, full, local_gy, gw1_shards, gw2_shards)
+    gw1_shards.barrier()  # all contributions landed
+    gw2_shards.barrier()
+    dist.all_reduce(gb1, group=group)
+    dist.reduce(gb2, dst=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    off = shard.hidden_offset
+    return DistStepResult(fw.y, MoeGrads(gw1_shards.view().clone(), gb1[:, off:off + h].contiguous(),
+                                         gw2_shards.view().clone(), gb2 if r == 0 else None, gx),
+                          ["param_all_gather", "grad_fused_reduce_scatter", "bias_grad_reduce"])

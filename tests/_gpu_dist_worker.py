@@ -66,6 +66,25 @@ def main():
     errs["mc_gw2"] = scaled(res.grads.gw2, gref.gw2[:, off:off + h, :])
     if r == 0:
         errs["mc_gb2"] = scaled(res.grads.gb2, gref.gb2)
+    # fused collectives over peer memory (CUDA IPC tables built over NCCL)
+    yb, gxb = D.PeerBuffers(n_local, Dm), D.PeerBuffers(n_local, Dm)
+    res = D.model_centric_step_fused(lx, la, lgy, sh, sp.b2, "gelu", yb, gxb)
+    errs["mcf_y"] = scaled(res.y, ref.y[lo:hi])
+    errs["mcf_gx"] = scaled(res.grads.gx, gref.gx[lo:hi])
+    errs["mcf_gw1"] = scaled(res.grads.gw1, gref.gw1[:, :, off:off + h])
+    E_ = p.experts()
+    w1b = D.PeerBuffers(h, Dm, shape=(E_, Dm, h))
+    w2b = D.PeerBuffers(h, Dm, shape=(E_, h, Dm))
+    res = D.data_centric_step_fused(lx, la, lgy, sh, sp.b2 if r == 0 else None, sp.hidden_sizes,
+                                    "gelu", w1b, w2b)
+    errs["dcf_y"] = scaled(res.y, ref.y[lo:hi])
+    errs["dcf_gw1"] = scaled(res.grads.gw1, gref.gw1[:, :, off:off + h])
+    errs["dcf_gw2"] = scaled(res.grads.gw2, gref.gw2[:, off:off + h, :])
+    errs["dcf_gb1"] = scaled(res.grads.gb1, gref.gb1[:, off:off + h])
+    torch.cuda.synchronize()
+    dist.barrier()
+    for b in (yb, gxb, w1b, w2b):
+        b.close()
     # multi-layer pipeline (two-slot cache, NCCL gathers on a side stream)
     # vs the single-GPU sequential stack of the same layers
     L = 3

@@ -110,3 +110,39 @@ def test_fused_reduce_scatter_two_processes_ipc():
     for rank, errs in out.items():
         bad = {k: v for k, v in errs.items() if not v <= 1e-3}
         assert not bad, (rank, bad)
+
+
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="no CUDA device")
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_fused_grad_reduce_scatter_simulated_ranks(P):
+    """Data-centric: each simulated rank runs the full layer on its own tokens
+    and reduces gW1 / gW2 into the H-shard owners' buffers; the shards must
+    equal the H-slices of the summed single-GPU gradients."""
+    import paper_2411_01288_b200 as H
+    from paper_2411_01288_b200 import dist as D
+    E, k, Dm, Hd, n = 8, 2, 128, 256 * P, 256
+    p, _ = H.make_random_params(E, Dm, Hd, Dm, "gelu", seed=9, n_tokens=0)
+    span = Hd // P
+    gw1s = [torch.zeros(E, Dm, span, device="cuda") for _ in range(P)]
+    gw2s = [torch.zeros(E, span, Dm, device="cuda") for _ in range(P)]
+    b1 = D.PeerBuffers.local(gw1s, span=span)
+    b2 = D.PeerBuffers.local(gw2s, span=span)
+    tot_w1 = torch.zeros(E, Dm, Hd, device="cuda")
+    tot_w2 = torch.zeros(E, Hd, Dm, device="cuda")
+    for rr in range(P):
+        _, x = H.make_random_params(E, Dm, Hd, Dm, "gelu", seed=100 + rr, n_tokens=n)
+        r = H.synthesize_routing(n, E, k, "uniform", 200 + rr)
+        gy = torch.randn(n, Dm, generator=torch.Generator().manual_seed(rr)).to("cuda",
+                                                                             torch.bfloat16)
+        fw = H.moe_forward(x, p, r)
+        g = H.moe_backward(fw.stash, p, gy)
+        tot_w1 += g.gw1
+        tot_w2 += g.gw2
+        fw2 = H.moe_forward(x, p, r)
+        gb1, gb2, gx = D.layer_backward_dc(fw2.stash, p, gy, b1, b2)
+        assert scaled(gb1, g.gb1) <= 1e-5 and scaled(gx, g.gx) <= 1e-5
+    torch.cuda.synchronize()
+    for rr in range(P):
+        sl = slice(rr * span, (rr + 1) * span)
+        assert scaled(gw1s[rr], tot_w1[:, :, sl]) <= 1e-4, rr
+        assert scaled(gw2s[rr], tot_w2[:, sl, :]) <= 1e-4, rr
