@@ -35,7 +35,7 @@ constexpr int UK = 16;   // UMMA K for kind::f16
 // F' multiply, column sums, TMA stores) is the bottleneck at K = 384 and needs
 // more warps to hide its latencies.  Threads = producer + MMA + epilogue.
 __host__ __device__ constexpr int epi_warps(int bn, int mode) {
-  return (mode == 1 || mode == 2) && bn == 256 ? 16 : 8;
+  return (mode == 1 || mode == 2 || mode == 3) && bn == 256 ? 16 : 8;
 }
 __host__ __device__ constexpr int kthreads(int bn, int mode) { return 64 + 32 * epi_warps(bn, mode); }
 constexpr uint32_t kTmemCols = 512;
@@ -1223,8 +1223,13 @@ hxm_status launch_bn(const UParams& prm, int max_work, cudaStream_t st) {
   // D = 384); at long K the MMA bounds it and 8 warps keep more ring stages
   if constexpr (epi_warps(BN, MODE) == 16) {
     const int m = epi16_mode();
-    if (m == 2 || (m == 1 && prm.K <= 512))
+    if constexpr (MODE == 3) {
+      // ESTMM: the store-heavy epilogue (a full fp32 gW tile per item) bounds
+      // items with few tokens (skewed routing); neutral for the others
+      if (m != 0) return launch_bn_ew<BN, MODE, CG, ACT, 16>(prm, max_work, st);
+    } else if (m == 2 || (m == 1 && prm.K <= 512)) {
       return launch_bn_ew<BN, MODE, CG, ACT, 16>(prm, max_work, st);
+    }
   }
   return launch_bn_ew<BN, MODE, CG, ACT, 8>(prm, max_work, st);
 }
