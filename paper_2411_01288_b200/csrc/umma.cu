@@ -769,13 +769,13 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
             tma_2d(ybox(dchunk + j), &p.tmY, ybar(dchunk + j), n0 + 32 * j, qbase);
           }
         }
-        // bias of this warp's HB columns: lane l holds columns 4l..4l+3,
-        // broadcast by shuffles (loaded before the wait)
-        float4 bl = make_float4(0.f, 0.f, 0.f, 0.f);
+        // bias of this warp's HB columns: every lane reads the same 32 floats
+        // per chunk (uniform-address LDG.128, one broadcast transaction each,
+        // L1-resident) and adds them in f32x2
         const bool has_bias = p.bias && !bwd;
-        if (has_bias && lane * 4 < HB)
-          bl = __ldg(reinterpret_cast<const float4*>(p.bias + static_cast<int64_t>(t.expert) * N +
-                                                     n0) + lane);
+        const float4* bias4 =
+            has_bias ? reinterpret_cast<const float4*>(p.bias + static_cast<int64_t>(t.expert) * N + n0)
+                     : nullptr;
         if (warp == 2 && lane == 0) TRACE(ep_it, 3);
         if constexpr (CG == 2) mbar_wait_cl(&tfull[acc], aph);
         else mbar_wait(&tfull[acc], aph);
@@ -805,11 +805,10 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
           if (has_bias) {
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
-              const int src = (c0 + i) / 4;
-              v[i] += __shfl_sync(0xffffffffu, bl.x, src);
-              v[i + 1] += __shfl_sync(0xffffffffu, bl.y, src);
-              v[i + 2] += __shfl_sync(0xffffffffu, bl.z, src);
-              v[i + 3] += __shfl_sync(0xffffffffu, bl.w, src);
+              const float4 b = __ldg(bias4 + (c0 + i) / 4);
+              const float2 lo = f2_fma(make_float2(v[i], v[i + 1]), f2(1.f), make_float2(b.x, b.y));
+              const float2 hi = f2_fma(make_float2(v[i + 2], v[i + 3]), f2(1.f), make_float2(b.z, b.w));
+              v[i] = lo.x; v[i + 1] = lo.y; v[i + 2] = hi.x; v[i + 3] = hi.y;
             }
           }
           if (dense_out) {
