@@ -337,6 +337,35 @@ def test_layer_c2_full_size_properties():
     assert torch.isfinite(g.gw1).all() and torch.isfinite(g.gx).all()
 
 
+def test_layer_c4_full_size_properties():
+    """BASELINE.json c4 at its full 131072 tokens on one GPU (64 experts
+    top-2, d 1024, ffn 4096): size-independent exact properties instead of
+    the CPU oracle (hours at this size).  gb2 counts the routed slots exactly
+    for g_y = ones; the backward is linear in g_y and scaling by 2 is exact in
+    floating point, so every gradient of 2 g_y is bitwise twice that of g_y
+    (deterministic reductions: k = 2 reductions commute); a 64-token
+    subsample of the batch matches the oracle."""
+    H = hx()
+    E, k, D, Hd, N = 64, 2, 1024, 4096, 131072
+    p, x = H.make_random_params(E, D, Hd, D, "gelu", seed=4, n_tokens=N)
+    r = H.synthesize_routing(N, E, k, "uniform", 4)
+    ones = torch.ones(N, D, dtype=torch.bfloat16, device="cuda")
+    fw = H.moe_forward(x, p, r)
+    g1 = H.moe_backward(fw.stash, p, ones)
+    counts = np.bincount(r.assignments.ravel(), minlength=E).astype(np.float64)
+    assert np.array_equal(host(g1.gb2), np.repeat(counts[:, None], D, axis=1))
+    g2 = H.moe_backward(fw.stash, p, 2 * ones)
+    for key in ("gw1", "gb1", "gw2", "gb2", "gx"):
+        assert torch.equal(getattr(g2, key), 2 * getattr(g1, key)), key
+    del g2
+    # token subsample against the oracle (the rows of y depend only on
+    # their own token)
+    sub = np.arange(0, N, N // 64)
+    y_ref, _, _ = O.moe_forward(host(x)[sub], host(p.w1), host(p.b1), host(p.w2), host(p.b2),
+                                r.assignments[:, sub], 8, "gelu")
+    assert O.scaled_err(host(fw.y)[sub], y_ref) <= RTOL_BF16
+
+
 @pytest.mark.parametrize("E,k,D,Hd,N,dtype", [
     (1, 1, 64, 128, 1, torch.bfloat16),     # one token, one expert
     (3, 3, 64, 128, 5, torch.bfloat16),     # k == E
