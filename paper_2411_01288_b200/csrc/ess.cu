@@ -402,15 +402,6 @@ __global__ void __launch_bounds__(NT) gather_relayout(const T* __restrict__ x1, 
 
 }  // namespace
 
-hxm_status launch_gather_rows(hxm_dtype dt, const void* src, RowMap map, int64_t d,
-                              const int32_t* idx, int n_experts, int64_t bound, void* dst,
-                              cudaStream_t st, double work_bytes) {
-  ProfScope ps(st, "gather_rows", work_bytes, WORK_BYTES);
-  return dt == HXM_BF16
-             ? gather_typed<__nv_bfloat16, int32_t>(src, map, d, idx, n_experts, bound, dst, st)
-             : gather_typed<float, int32_t>(src, map, d, idx, n_experts, bound, dst, st);
-}
-
 hxm_status launch_estmm_relayout(const void* x1, int64_t d1, const void* x2, int64_t d2,
                                   const int64_t* v, const int64_t* idx, int E, int64_t bound,
                                   int32_t* idx64, void* o1, void* o2, cudaStream_t st) {

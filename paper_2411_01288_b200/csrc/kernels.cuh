@@ -108,18 +108,17 @@ struct EssArgs {
 };
 
 // dst[p] = src[map(p)] for p < idx[E] (padding slots -> zero rows): the
-// expert-sorted copy of a token-order tensor, bandwidth-bound.
-hxm_status launch_gather_rows(hxm_dtype dt, const void* src, RowMap map, int64_t d,
-                              const int32_t* idx, int n_experts, int64_t bound, void* dst,
-                              cudaStream_t st, double work_bytes = 0.0);
+// expert-sorted copy of a token-order tensor, bandwidth-bound (operator ESMM).
+hxm_status launch_gather_rows64(hxm_dtype dt, const void* src, RowMap map, int64_t d,
+                                const int64_t* idx, int n_experts, int64_t bound, void* dst,
+                                cudaStream_t st);
+
 // ESTMM operator (bf16): segments re-laid to 64-position multiples (idx64,
 // E+1 int32) and both operands gathered into that layout (o1, o2: bound rows)
 hxm_status launch_estmm_relayout(const void* x1, int64_t d1, const void* x2, int64_t d2,
                                   const int64_t* v, const int64_t* idx, int E, int64_t bound,
                                   int32_t* idx64, void* o1, void* o2, cudaStream_t st);
-hxm_status launch_gather_rows64(hxm_dtype dt, const void* src, RowMap map, int64_t d,
-                                const int64_t* idx, int n_experts, int64_t bound, void* dst,
-                                cudaStream_t st);
+
 
 // out[e] = sum over e's tiles t (tile_off[e]..tile_off[e+1]) and the
 // `parts` partial rows of each tile of partial[(t * parts + r) x d]: the

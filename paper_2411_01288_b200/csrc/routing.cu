@@ -501,19 +501,6 @@ __global__ void __launch_bounds__(kThreads) fwd_prologue(FwdPrologue a) {
 
 }  // namespace
 
-template <class IdxT>
-hxm_status launch_tiles3(const IdxT* idx, int64_t E, const TileSpec* specs, int count,
-                         cudaStream_t st) {
-  if (count < 1 || count > 3) return invalid_arg("launch_tiles3: 1..3 specs");
-  build_tiles<IdxT><<<1, 1024, 0, st>>>(idx, static_cast<int>(E), specs[0],
-                                        specs[count > 1 ? 1 : 0], specs[count > 2 ? 2 : 0],
-                                        count);
-  HXM_CHECK_LAUNCH();
-  return HXM_OK;
-}
-template hxm_status launch_tiles3<int32_t>(const int32_t*, int64_t, const TileSpec*, int,
-                                           cudaStream_t);
-
 size_t reindex_ws_bytes(int64_t n, int64_t E) {
   const int chunk = pick_chunk(n);
   const int64_t nchunks = ceil_div(n, chunk);
@@ -524,11 +511,6 @@ size_t reindex_ws_bytes(int64_t n, int64_t E) {
   return ar.used;
 }
 
-hxm_status build_reindex_slots(const int32_t* a, int64_t n_slots, int64_t E,
-                               int64_t blk, int32_t* v, int32_t* idx, void* ws,
-                               size_t ws_bytes, int32_t* status, cudaStream_t st) {
-  return build_impl<int32_t, int32_t>(a, n_slots, E, blk, v, idx, ws, ws_bytes, status, st);
-}
 
 template <class IdxT>
 hxm_status launch_tiles(const IdxT* idx, int64_t E, int rows, bool min_one,

@@ -6,21 +6,13 @@ namespace hxm {
 
 size_t reindex_ws_bytes(int64_t n, int64_t E);
 
-// Combined k-choice index: `a` is the k x N assignment matrix viewed as k*N
-// slots; v receives slot ids grouped by expert (choice-major, token-ascending
-// inside a segment), segments padded with -1 to a multiple of blk.
-hxm_status build_reindex_slots(const int32_t* a, int64_t n_slots, int64_t E,
-                               int64_t blk, int32_t* v, int32_t* idx, void* ws,
-                               size_t ws_bytes, int32_t* status, cudaStream_t st);
-
 // Cut every expert segment [idx[e], idx[e+1]) into tiles of <= rows positions.
 template <class IdxT>
 hxm_status launch_tiles(const IdxT* idx, int64_t E, int rows, bool min_one,
                         SegTile* tiles, int32_t* tile_off, int32_t* n_tiles,
                         cudaStream_t st, int split_rows = 0);
 
-// Up to three tilings of the same index in one launch (the layer builds its
-// ESMM, ESTMM-chunk and ESS tables together).
+// One tiling of a segment index (rows per tile, see tile_pass).
 struct TileSpec {
   int rows;
   int min_one;
@@ -31,10 +23,6 @@ struct TileSpec {
                        // split_rows-position tiles instead (ESTMM chunks: one
                        // chunk per expert unless it is heavily skewed)
 };
-template <class IdxT>
-hxm_status launch_tiles3(const IdxT* idx, int64_t E, const TileSpec* specs, int count,
-                         cudaStream_t st);
-
 int64_t max_tiles(int64_t n_padded_bound, int64_t E, int rows);
 
 // The layer forward's prologue in one cooperative launch: k-choice slot index
