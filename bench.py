@@ -303,6 +303,8 @@ def run_ours(args, cfg, rank, ws, local):
         sp = HD.shard_params(p, HD.even_split(Hd, ws))
         dc = HD.DataCentricRunner(sp.shards[rank], sp.b2 if rank == 0 else None,
                                   sp.hidden_sizes, "gelu", N, k, None, dtype)
+        if not args.no_fused and cfg["dtype"] == "bf16":
+            dc.enable_fused_grads()  # gW reduce-scatter inside the ESTMM epilogues
         del p, sp
         run = dc.runner
         y_out = run.y
@@ -462,8 +464,7 @@ def run_ours(args, cfg, rank, ws, local):
         "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
         "config": {"workload": args.config, "desc": cfg["desc"], "E": E, "k": k, "d": D,
                    "ffn": Hd, "tokens_per_gpu": N, "routing": cfg["dist"],
-                   "parallelism": (f"{mode}_tp{ws}" + ("_fused_rs" if mode == "model_centric" and
-                                                         not args.no_fused else ""))
+                   "parallelism": (f"{mode}_tp{ws}" + ("_fused_rs" if not args.no_fused else ""))
                    if mode != "single" else "single",
                    "formulation": (f"conventional dispatch/combine, capacity factor "
                                    f"{args.capacity_factor}") if args.capacity_factor > 0

@@ -355,6 +355,9 @@ class DataCentricRunner:
         self.cache = PipelineSharedCache(full.param_elements())
         self.cache.fill(0, full)
         self.runner = LayerRunner(full, n_tokens, k, dev, dtype)
+        if P == 1:  # one rank: the gather lands directly in the cache layout
+            self.w1g, self.w2g = full.w1, full.w2
+            self.b1g = self.runner.b1
         self.side = torch.cuda.Stream(device=dev)
         self.gw1 = torch.empty((E, Di, h), dtype=torch.float32, device=dev)
         self.gb1 = torch.empty((E, h), dtype=torch.float32, device=dev)
@@ -370,15 +373,28 @@ class DataCentricRunner:
             dist.all_gather_into_tensor(self.b1g, self.shard.b1.contiguous(), group=self.group)
             dist.broadcast(self.b2, src=dist.get_global_rank(self.group, 0)
                            if self.group is not None else 0, group=self.group)
-            p = self.cache.params()
-            Di, h, Do = self.w1g.shape[1], self.h, self.w2g.shape[2]
-            p.w1.view(E, Di, P, h).copy_(self.w1g.view(P, E, Di, h).permute(1, 2, 0, 3))
-            p.w2.view(E, P, h, Do).copy_(self.w2g.view(P, E, h, Do).permute(1, 0, 2, 3))
-            self.runner.b1.view(E, P, h).copy_(self.b1g.view(P, E, h).permute(1, 0, 2))
+            if P > 1:  # rank-major gather buffers -> the cache's reference layout
+                p = self.cache.params()
+                Di, h, Do = self.w1g.shape[1], self.h, self.w2g.shape[2]
+                p.w1.view(E, Di, P, h).copy_(self.w1g.view(P, E, Di, h).permute(1, 2, 0, 3))
+                p.w2.view(E, P, h, Do).copy_(self.w2g.view(P, E, h, Do).permute(1, 0, 2, 3))
+                self.runner.b1.view(E, P, h).copy_(self.b1g.view(P, E, h).permute(1, 0, 2))
         torch.cuda.current_stream().wait_stream(self.side)
+
+    def enable_fused_grads(self) -> None:
+        """Reduce-scatter gW1 / gW2 inside the ESTMM epilogues into the shard
+        owners' peer-mapped buffers (hxm_moe_backward_dc) instead of NCCL
+        reduce-scatters of permuted copies; gb1 / gb2 stay NCCL (tiny)."""
+        E, Di, h = self.shard.w1.shape
+        Do = self.shard.w2.shape[2]
+        self._w1b = PeerBuffers(h, Di, self.group, shape=(E, Di, h))
+        self._w2b = PeerBuffers(h, Do, self.group, shape=(E, h, Do))
+        self.gw1, self.gw2 = self._w1b.view(), self._w2b.view()
 
     def step(self, x, assignments, g_y):
         self.gather()
+        if getattr(self, "_w1b", None) is not None:
+            return self._step_fused(x, assignments, g_y)
         self.runner.step(x, assignments, g_y)
         g = self.runner.grads
         E = g.gw1.shape[0]
@@ -513,6 +529,28 @@ def _reduce_param_grads(g, shard: ParamShard, hidden_sizes, group, how: str):
     dist.reduce(g.gb2, dst=dist.get_global_rank(group, 0) if group is not None else 0,
                 group=group)
     return MoeGrads(outs[0], outs[1], outs[2], g.gb2 if r == 0 else None, g.gx)
+
+
+def _dc_step_fused(self, x, assignments, g_y):
+    run = self.runner
+    run.forward(x, assignments)
+    self._w1b.view().zero_()
+    self._w2b.view().zero_()
+    self._w1b.barrier()  # every owner's shards are zero before any rank reduces
+    self._w2b.barrier()
+    gb1, gb2 = run.grads.gb1, run.grads.gb2
+    run.backward_dc(x, g_y, self._w1b, self._w2b)
+    self._w1b.barrier()  # all contributions landed
+    self._w2b.barrier()
+    E, P, h = gb1.shape[0], self.P, self.h
+    b1 = gb1.view(E, P, h).permute(1, 0, 2).contiguous()
+    dist.reduce_scatter_tensor(self.gb1, b1, group=self.group)
+    if gb2 is not None:
+        dist.all_reduce(gb2, group=self.group)
+    return run.y
+
+
+DataCentricRunner._step_fused = _dc_step_fused
 
 
 def _reduce_rows(t: torch.Tensor, counts: Sequence[int], group, how: str) -> torch.Tensor:

@@ -56,6 +56,20 @@ class LayerRunner:
             "moe_backward")
         return g
 
+    def backward_dc(self, x: torch.Tensor, g_y: torch.Tensor, gw1_shards, gw2_shards, stream=None):
+        """Data-centric backward: gW1 / gW2 reduce-scattered along H into the
+        shard owners' peer buffers (dist.PeerBuffers) inside the ESTMM
+        epilogues; gb1, gb2, gx land in this runner's grads."""
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        g = self.grads
+        check(self._L.hxm_moe_backward_dc(
+            self._pd, x.data_ptr(), self.p.w1.data_ptr(), self.p.w2.data_ptr(), g_y.data_ptr(),
+            self.ws.data_ptr(), self.ws.numel(), C.byref(gw1_shards.rows_struct),
+            g.gb1.data_ptr(), C.byref(gw2_shards.rows_struct),
+            None if g.gb2 is None else g.gb2.data_ptr(), g.gx.data_ptr(), st),
+            "moe_backward_dc")
+        return g
+
     def step(self, x, assignments, g_y, stream=None):
         self.forward(x, assignments, stream)
         return self.backward(x, g_y, stream)

@@ -55,6 +55,15 @@ def main():
     runner = D.DataCentricRunner(sh, sp.b2 if r == 0 else None, sp.hidden_sizes, "gelu", n_local,
                                  k)
     y = runner.step(lx, la, lgy)
+    frun = D.DataCentricRunner(sh, sp.b2 if r == 0 else None, sp.hidden_sizes, "gelu", n_local, k)
+    frun.enable_fused_grads()
+    for _ in range(2):
+        yf = frun.step(lx, la, lgy)
+    torch.cuda.synchronize()
+    errs["dcrf_y"] = scaled(yf, ref.y[lo:hi])
+    errs["dcrf_gw1"] = scaled(frun.gw1, gref.gw1[:, :, off:off + h])
+    errs["dcrf_gb1"] = scaled(frun.gb1, gref.gb1[:, off:off + h])
+    errs["dcrf_gw2"] = scaled(frun.gw2, gref.gw2[:, off:off + h, :])
     errs["dcr_y"] = scaled(y, ref.y[lo:hi])
     errs["dcr_gw1"] = scaled(runner.gw1, gref.gw1[:, :, off:off + h])
     errs["dcr_gb1"] = scaled(runner.gb1, gref.gb1[:, off:off + h])
