@@ -113,6 +113,81 @@ __device__ __forceinline__ void ess_item(const EssArgs& a, int ti, int slab) {
   }
 }
 
+// Whole-row variant: one item is a full segment tile (every column), the
+// lanes loop over GPL column groups, so a bf16 row of up to 32*GPL*VEC
+// columns is one item (no half-empty column slabs, one round of items).
+template <class T, int VEC, int GPL>
+__device__ __forceinline__ void ess_item_rows(const EssArgs& a, int ti) {
+  const SegTile tile = a.tiles[ti];
+  const T* X = static_cast<const T*>(a.x);
+  const int64_t D = a.d;
+  const int col_groups = static_cast<int>(D / VEC);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  constexpr int W = NT / 32;
+  __shared__ int rows[kEssRows];
+  __shared__ float red[W][32 * VEC * GPL];
+  __syncthreads();
+  for (int i = threadIdx.x; i < kEssRows; i += NT) {
+    const int64_t p = tile.begin + i;
+    rows[i] = p < tile.end ? a.map(p) : -1;
+  }
+  __syncthreads();
+  const int nrows = tile.end - tile.begin;
+  float acc[GPL][VEC];
+#pragma unroll
+  for (int g = 0; g < GPL; ++g)
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) acc[g][i] = 0.f;
+  constexpr int U = 2;  // rows in flight per warp (x GPL groups per lane)
+  for (int r0 = warp; r0 < nrows; r0 += W * U) {
+    float v[U][GPL][VEC];
+    int rr[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int r = r0 + u * W;
+      rr[u] = r < nrows ? rows[r] : -2;
+#pragma unroll
+      for (int g = 0; g < GPL; ++g) {
+        const int cg = lane + 32 * g;
+        if (rr[u] >= 0 && cg < col_groups)
+          load_vec<T, VEC>(X + static_cast<int64_t>(rr[u]) * D + static_cast<int64_t>(cg) * VEC,
+                           v[u][g]);
+        else
+#pragma unroll
+          for (int i = 0; i < VEC; ++i) v[u][g][i] = 0.f;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (rr[u] == -2) continue;
+#pragma unroll
+      for (int g = 0; g < GPL; ++g) {
+        const int cg = lane + 32 * g;
+        if (cg >= col_groups) continue;
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) acc[g][i] += v[u][g][i];
+        if (a.copy_out)  // padding slots copy as zero rows
+          store_vec<T, VEC>(static_cast<T*>(a.copy_out) +
+                                (static_cast<int64_t>(tile.begin) + r0 + u * W) * D +
+                                static_cast<int64_t>(cg) * VEC,
+                            v[u][g]);
+      }
+    }
+  }
+  if (!a.partial) return;
+#pragma unroll
+  for (int g = 0; g < GPL; ++g)
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) red[warp][(lane + 32 * g) * VEC + i] = acc[g][i];
+  __syncthreads();
+  for (int c = threadIdx.x; c < D; c += NT) {  // fixed warp order: deterministic
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < W; ++w) s += red[w][c];
+    a.partial[static_cast<int64_t>(ti) * D + c] = s;
+  }
+}
+
 template <class T, int VEC>
 __global__ void __launch_bounds__(NT) ess_partial(EssArgs a) {
   // grid: x = segment tile (<= 128 positions), y = column slab of 32 vector
@@ -314,9 +389,15 @@ __global__ void __launch_bounds__(NT) bwd_prologue(BwdPrologue b) {
   }
   const EssArgs& a = b.es;
   const int col_groups = static_cast<int>((a.d + VEC - 1) / VEC);
-  const int slabs = static_cast<int>(ceil_div(col_groups, 32));
-  const int items = *a.n_tiles * slabs;
-  for (int it = blockIdx.x; it < items; it += gridDim.x) ess_item<T, VEC>(a, it / slabs, it % slabs);
+  if (VEC > 1 && col_groups <= 32 * 2 && a.d % VEC == 0) {
+    // whole rows per item (D <= 64 * VEC): one round of items, no half slabs
+    for (int ti = blockIdx.x; ti < *a.n_tiles; ti += gridDim.x) ess_item_rows<T, VEC, 2>(a, ti);
+  } else {
+    const int slabs = static_cast<int>(ceil_div(col_groups, 32));
+    const int items = *a.n_tiles * slabs;
+    for (int it = blockIdx.x; it < items; it += gridDim.x)
+      ess_item<T, VEC>(a, it / slabs, it % slabs);
+  }
   if (!a.out) return;
   cgp::this_grid().sync();
   const int chunks = static_cast<int>(ceil_div(a.d, 128));
