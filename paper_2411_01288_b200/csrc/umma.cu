@@ -421,9 +421,12 @@ struct Cfg {
   // 227 KB opt-in smem = stages + epilogue staging + 1 KB alignment slack +
   // barriers.  Staging: 2 KB per epilogue warp (MODE 0 / 3).
   static constexpr int kStaging = kGroups * kGroupBytes;
-  static constexpr int kBudget = 232448 - 1024 - 256 - kStaging;
+  // MODE 1: the item's bias columns (BN floats), shared by a column group's warps
+  static constexpr int kBias = MODE == 1 ? BN * 4 : 0;
+  static constexpr int kBudget = 232448 - 1024 - 256 - kStaging - kBias;
   static constexpr int kStages = kBudget / kStage > 8 ? 8 : kBudget / kStage;
-  static constexpr int kSmem = kStages * kStage + kStaging + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kSmem =
+      kStages * kStage + kStaging + kBias + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 // MODE: 0 = ESMM, fp32 write / accumulate / reduce epilogue; 1 = ESMM with
@@ -449,7 +452,8 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
   // staging accesses compile to LDS/STS rather than generic LD/ST
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* staging = smem + C::kStages * C::kStage;
-  uint64_t* full = reinterpret_cast<uint64_t*>(staging + C::kStaging);
+  float* bias_s = reinterpret_cast<float*>(staging + C::kStaging);  // MODE 1
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + C::kStaging + C::kBias);
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + 2;
@@ -740,14 +744,31 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
     int ep_it = 0;
     SegTile t_cur = ESTMM || cluster >= total ? SegTile{0, 0, 0, 0} : tile_at(wmap(cluster));
     int orow_cur = ESTMM ? -1 : orow_of(t_cur);
+    // MODE 1 bias: the column group's HB bias floats of the current item sit
+    // in smem; lane l < HB / 4 of lane-group warp lg owns entry lg * HB / 4 + l,
+    // loads the next item's value during this item (latency hidden) and
+    // writes it once the group is past this item's last read (the chunk
+    // barriers order writes and reads)
+    constexpr int kBq = HB / 4;
+    float* gbias = bias_s + half * HB;
+    const bool bias_smem = MODE == 1 && p.bias != nullptr;
+    auto bias_at = [&](const SegTile& tt, int ww) {
+      return __ldg(p.bias + static_cast<int64_t>(tt.expert) * p.N + (ww % per_item) * BN + half * HB +
+                   lg * kBq + lane);
+    };
+    if (bias_smem && lane < kBq && cluster < total) gbias[lg * kBq + lane] = bias_at(t_cur, wmap(cluster));
+    int y_iss = 0;  // MODE 2 (elected thread): global F'(y1) chunks issued so far
     for (int wl = cluster; wl < total; wl += n_clusters) {
       const int w = wmap(wl);
       const SegTile t = ESTMM ? p.tiles[w / per_item] : t_cur;
       const int rem = w % per_item;
       if (!ESTMM) {
         const bool has_nx = wl + n_clusters < total;
-        const SegTile t_nx = has_nx ? tile_at(wmap(wl + n_clusters)) : SegTile{0, 0, 0, 0};  // prefetch
+        const int w_nx = has_nx ? wmap(wl + n_clusters) : 0;
+        const SegTile t_nx = has_nx ? tile_at(w_nx) : SegTile{0, 0, 0, 0};  // prefetch
         int orow_nx = -1;
+        float bias_nx = 0.f;
+        if (bias_smem && has_nx && lane < kBq) bias_nx = bias_at(t_nx, w_nx);
         const int n0 = rem * BN + half * HB;
         const int orow = orow_cur;
         const int N = p.N;
@@ -762,17 +783,27 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
           return hstage + C::kOutBufs * C::kOutBox + (gchunk % kYRing) * 8192;
         };
         auto ybar = [&](int gchunk) { return &dbar[half * kYRing + gchunk % kYRing]; };
-        if (bwd && elect) {  // F'(y1) boxes of the first chunks, overlapping the MMA
-#pragma unroll
-          for (int j = 0; j < (kNch < kYRing - 1 ? kNch : kYRing - 1); ++j) {
-            mbar_arrive_tx(ybar(dchunk + j), 8192);
-            tma_2d(ybox(dchunk + j), &p.tmY, ybar(dchunk + j), n0 + 32 * j, qbase);
+        // F'(y1) boxes stream kYRing - 1 chunks ahead of the math, across the
+        // item boundary (the next item's first boxes load during this item's
+        // last chunk); a box goes into the slot of the chunk before the one
+        // being computed, which every thread has left at that chunk's barrier
+        const int chunk0 = dchunk;  // this item's first global chunk
+        auto y_issue_to = [&](int limit) {
+          if (limit > chunk0 + (has_nx ? 2 : 1) * kNch) limit = chunk0 + (has_nx ? 2 : 1) * kNch;
+          for (; y_iss < limit; ++y_iss) {
+            const int c = y_iss - chunk0;
+            const bool nx = c >= kNch;
+            const int col = (nx ? (w_nx % per_item) * BN + half * HB : n0) + 32 * (nx ? c - kNch : c);
+            const int row = (nx ? t_nx.begin : t.begin) + static_cast<int>(rank) * BM;
+            mbar_arrive_tx(ybar(y_iss), 8192);
+            tma_2d(ybox(y_iss), &p.tmY, ybar(y_iss), col, row);
           }
-        }
-        // bias of this warp's HB columns: every lane reads the same 32 floats
-        // per chunk (uniform-address LDG.128, one broadcast transaction each,
-        // L1-resident) and adds them in f32x2
-        const bool has_bias = p.bias && !bwd;
+        };
+        if (bwd && elect) y_issue_to(chunk0 + (kNch < kYRing - 1 ? kNch : kYRing - 1));
+        // MODE 0 bias of this warp's HB columns: every lane reads the same 32
+        // floats per chunk (uniform-address LDG.128, one broadcast transaction
+        // each, L1-resident) and adds them in f32x2 (MODE 1: from smem, below)
+        const bool has_bias = p.bias && !bwd && !dense_out;
         const float4* bias4 =
             has_bias ? reinterpret_cast<const float4*>(p.bias + static_cast<int64_t>(t.expert) * N + n0)
                      : nullptr;
@@ -825,11 +856,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             }
             named_bar_sync(1 + half, 128);
-            if (bwd && elect && c0 + 32 * (kYRing - 1) < HB) {  // F'(y1) kYRing-1 chunks ahead
-              const int ga = dchunk + kYRing - 1;
-              mbar_arrive_tx(ybar(ga), 8192);
-              tma_2d(ybox(ga), &p.tmY, ybar(ga), n + 32 * (kYRing - 1), qbase);
-            }
+            if (bwd && elect) y_issue_to(dchunk + kYRing);  // F'(y1) kYRing-1 chunks ahead
             uint4 dv[4];
             if (bwd) {  // this row's F'(y1) chunk from the staged box
               mbar_wait(ybar(dchunk), (dchunk / kYRing) & 1);
@@ -845,9 +872,13 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
                 // stash = (F'(y1), F(y1)): everything the backward needs
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                  float2 f, df;
+                  float2 f, df, x = make_float2(v[8 * j + 2 * i], v[8 * j + 2 * i + 1]);
+                  if (bias_smem) {  // uniform-address LDS: broadcast
+                    const float2 b = *reinterpret_cast<const float2*>(gbias + c0 + 8 * j + 2 * i);
+                    x = f2_fma(x, f2(1.f), b);
+                  }
                   // activation fixed at compile time (MODE 1 instantiations)
-                  act_pair<ACT>(make_float2(v[8 * j + 2 * i], v[8 * j + 2 * i + 1]), f, df);
+                  act_pair<ACT>(x, f, df);
                   a1[i] = pad ? 0u : pack_bf16(df.x, df.y);
                   a2[i] = pad ? 0u : pack_bf16(f.x, f.y);
                 }
@@ -871,7 +902,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
             //     32-row slice at a segment end), one bulk group per chunk
             fence_async_smem();
             named_bar_sync(1 + half, 128);
-            if (elect) {
+            if (elect && !(kTrace && (p.dbg_noload & 2))) {
               if (rows_here >= BM) {
                 // L2 policy: what the NEXT kernel reads stays (MODE 1: F(y1)
                 // for ESMM fwd2; MODE 2: g_y1 for ESTMM gW1 / ESMM gx), what
@@ -986,6 +1017,9 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
             }
           }
         }
+        // every warp of the group is past this item's last bias read (the
+        // last chunk's barrier): stage the next item's bias
+        if (bias_smem && has_nx && lane < kBq) gbias[lg * kBq + lane] = bias_nx;
         t_cur = t_nx;
         orow_cur = orow_nx;
         if (warp == 2 && lane == 0) TRACE(ep_it, 5);
