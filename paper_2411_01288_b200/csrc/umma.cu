@@ -55,6 +55,13 @@ constexpr bool kTrace = true;
 #else
 constexpr bool kTrace = false;
 #endif
+// HXM_DEBUG_NOLOAD knobs (operand loads / stores / MMAs skipped) without the
+// timeline: -DHXM_DBG_BUILD (python tools/trace_build.py --dbg)
+#if defined(HXM_DBG_BUILD) || defined(HXM_TRACE_BUILD)
+constexpr bool kDbg = true;
+#else
+constexpr bool kDbg = false;
+#endif
 #define TRACE(item, slot)                                                              \
   do {                                                                                 \
     if (kTrace && p.trace && (item) < 64)                                              \
@@ -79,6 +86,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "r"(a), "r"(parity)
       : "memory");
   if (done) return;
+#ifdef HXM_SIMPLE_WAIT
+  while (!done)
+    asm volatile(
+        "{\n.reg .pred P;\nmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P;\n}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  return;
+#endif
   const long long t0 = clock64();
   while (true) {
     asm volatile(
@@ -136,16 +153,6 @@ __device__ __forceinline__ void tc_fence_before() {
 }
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db,
-                                          uint32_t idesc, uint32_t accum) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(idesc), "r"(accum));
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile(
@@ -259,16 +266,6 @@ __device__ __forceinline__ void tma_4d_cg2(void* dst, const CUtensorMap* map, ui
       "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
-__device__ __forceinline__ void umma_bf16_cg2(uint32_t tmem_d, uint64_t da, uint64_t db,
-                                              uint32_t idesc, uint32_t accum) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(idesc), "r"(accum));
-}
 // arrive on the barrier at this smem offset in BOTH CTAs of the pair
 __device__ __forceinline__ void umma_commit_cg2(uint64_t* bar) {
   asm volatile(
@@ -276,6 +273,95 @@ __device__ __forceinline__ void umma_commit_cg2(uint64_t* bar) {
       " [%0], %1;" ::"r"(smem_u32(bar)),
       "h"(static_cast<uint16_t>(3))
       : "memory");
+}
+
+// One 64-deep k-block: four K=16 UMMAs (descriptors advanced in their low
+// words, which hold the start address) and the commit that frees the stage,
+// in one asm statement so the issuing thread converts its operands to
+// uniform registers once per k-block.  first = 1: the item's first k-block
+// (overwrite the accumulator).  skip = 1 (debug): commit only.
+template <int CG>
+__device__ __forceinline__ void umma_kblock(uint32_t tmem_d, uint32_t a_lo, uint32_t a_hi,
+                                            uint32_t a_step, uint32_t b_lo, uint32_t b_hi,
+                                            uint32_t b_step, uint32_t idesc, uint32_t first,
+                                            uint64_t* bar, uint32_t skip = 0) {
+  if constexpr (CG == 2) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p0, p1, sk;\n"
+        ".reg .b64 da, db;\n"
+        ".reg .b32 al, bl;\n"
+        "setp.ne.b32 p0, %8, 0;\n"
+        "setp.eq.b32 p1, %8, %8;\n"
+        "setp.ne.b32 sk, %10, 0;\n"
+        "@sk bra.uni DONE%=;\n"
+        "mov.b64 da, {%1, %2};\n"
+        "mov.b64 db, {%4, %5};\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %7, p0;\n"
+        "add.u32 al, %1, %3;\n"
+        "add.u32 bl, %4, %6;\n"
+        "mov.b64 da, {al, %2};\n"
+        "mov.b64 db, {bl, %5};\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %7, p1;\n"
+        "add.u32 al, al, %3;\n"
+        "add.u32 bl, bl, %6;\n"
+        "mov.b64 da, {al, %2};\n"
+        "mov.b64 db, {bl, %5};\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %7, p1;\n"
+        "add.u32 al, al, %3;\n"
+        "add.u32 bl, bl, %6;\n"
+        "mov.b64 da, {al, %2};\n"
+        "mov.b64 db, {bl, %5};\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %7, p1;\n"
+        "DONE%=:\n"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%9], %11;\n"
+        "}\n" ::"r"(tmem_d),
+        "r"(a_lo), "r"(a_hi), "r"(a_step), "r"(b_lo), "r"(b_hi), "r"(b_step), "r"(idesc),
+        "r"(first ? 0u : 1u), "r"(smem_u32(bar)), "r"(skip), "h"(static_cast<uint16_t>(3))
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n"
+        ".reg .pred p0, p1, sk;\n"
+        ".reg .b64 da, db;\n"
+        ".reg .b32 al, bl;\n"
+        "setp.ne.b32 p0, %8, 0;\n"
+        "setp.eq.b32 p1, %8, %8;\n"
+        "setp.ne.b32 sk, %10, 0;\n"
+        "@sk bra.uni DONE%=;\n"
+        "mov.b64 da, {%1, %2};\n"
+        "mov.b64 db, {%4, %5};\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %7, p0;\n"
+        "add.u32 al, %1, %3;\n"
+        "add.u32 bl, %4, %6;\n"
+        "mov.b64 da, {al, %2};\n"
+        "mov.b64 db, {bl, %5};\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %7, p1;\n"
+        "add.u32 al, al, %3;\n"
+        "add.u32 bl, bl, %6;\n"
+        "mov.b64 da, {al, %2};\n"
+        "mov.b64 db, {bl, %5};\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %7, p1;\n"
+        "add.u32 al, al, %3;\n"
+        "add.u32 bl, bl, %6;\n"
+        "mov.b64 da, {al, %2};\n"
+        "mov.b64 db, {bl, %5};\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %7, p1;\n"
+        "DONE%=:\n"
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%9];\n"
+        "}\n" ::"r"(tmem_d),
+        "r"(a_lo), "r"(a_hi), "r"(a_step), "r"(b_lo), "r"(b_hi), "r"(b_step), "r"(idesc),
+        "r"(first ? 0u : 1u), "r"(smem_u32(bar)), "r"(skip)
+        : "memory");
+  }
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n"
+      : "=r"(pred));
+  return pred != 0;
 }
 
 // same load without the completion wait (pair with tmem_wait)
@@ -528,18 +614,28 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
         }
         unsigned long long pw = 0;
         for (int kb = 0; kb < nk; ++kb) {
-          const unsigned long long tp0 = (kTrace && p.trace) ? gtime() : 0;
+          const long long tp0 = (kTrace && p.trace) ? clock64() : 0;
           mbar_wait(&empty[s], ph ^ 1);
-          if (kTrace && p.trace) pw += gtime() - tp0;
+          if (kTrace && p.trace) pw += clock64() - tp0;
           if (kTrace && p.trace && lane == 0 && kb == nk - 1 && pit_ < 64) p.trace[(static_cast<size_t>(blockIdx.x) * 64 + pit_) * 8 + 7] = pw;
           uint8_t* sa = smem + s * C::kStage;
           uint8_t* sb = sa + kABytes;
           if constexpr (CG == 2) {
             // dense only: this CTA's 128 rows of A and BN/2 columns of B,
             // completion counted on the leader's full barrier
-            if (lane == 0) {
+            if (elect_one()) {
               const uint32_t fb = full_lead + 8u * s;
-              if (kTrace && (p.dbg_noload & 1)) { mbar_arrive_cl(fb); __syncwarp(); if (++s == C::kStages) { s = 0; ph ^= 1; } continue; }
+              if (kDbg && (p.dbg_noload & 1)) { mbar_arrive_cl(fb); __syncwarp(); if (++s == C::kStages) { s = 0; ph ^= 1; } continue; }
+              if (kDbg && (p.dbg_noload & 24)) {  // debug: A only (8) / B only (16)
+                mbar_arrive_tx_cl(fb, (p.dbg_noload & 8) ? kABytes : C::kBBytes);
+                const int nb = n0 + static_cast<int>(rank) * (BN / 2);
+                if (p.dbg_noload & 8) tma_2d_cg2(sa, &p.tmA, fb, kb * BK, t.begin + static_cast<int>(rank) * BM);
+                else if (p.b_kmajor) tma_3d_cg2(sb, &p.tmB, fb, kb * BK, nb, t.expert);
+                else tma_4d_cg2(sb, &p.tmB, fb, 0, kb * BK, nb / (p.b_sw64 ? 32 : 64), t.expert);
+                __syncwarp();
+                if (++s == C::kStages) { s = 0; ph ^= 1; }
+                continue;
+              }
               mbar_arrive_tx_cl(fb, C::kStage);
               tma_2d_cg2(sa, &p.tmA, fb, kb * BK, t.begin + static_cast<int>(rank) * BM);
               const int nb = n0 + static_cast<int>(rank) * (BN / 2);
@@ -551,15 +647,16 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
               }
             }
           } else {
-            if (lane == 0) mbar_arrive_tx(&full[s], C::kStage);
+            const bool el = elect_one();
+            if (el) mbar_arrive_tx(&full[s], C::kStage);
             __syncwarp();
             if (p.a_gather) {
               tma_gather4(sa + lane * 512, &p.tmA, &full[s], kb * BK, rows[0], rows[1], rows[2],
                           rows[3]);
-            } else if (lane == 0) {
+            } else if (el) {
               tma_2d(sa, &p.tmA, &full[s], kb * BK, t.begin);
             }
-            if (lane == 0) {
+            if (el) {
               if (p.b_kmajor) {
                 tma_3d(sb, &p.tmB, &full[s], kb * BK, n0, t.expert);
               } else {
@@ -581,9 +678,9 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
           uint8_t* sa = smem + s * C::kStage;
           uint8_t* sb = sa + kABytes;
           if constexpr (CG == 2) {  // dense only (host guarantees)
-            if (lane == 0) {
+            if (elect_one()) {
               const uint32_t fb = full_lead + 8u * s;
-              if (kTrace && (p.dbg_noload & 1)) { mbar_arrive_cl(fb); __syncwarp(); if (++s == C::kStages) { s = 0; ph ^= 1; } continue; }
+              if (kDbg && (p.dbg_noload & 1)) { mbar_arrive_cl(fb); __syncwarp(); if (++s == C::kStages) { s = 0; ph ^= 1; } continue; }
               mbar_arrive_tx_cl(fb, C::kStage);
               // both 64-column chunks of A, all chunks of B: one 3D box each
               tma_3d_cg2(sa, &p.tmA, fb, 0, p0, m0 / 64);
@@ -593,7 +690,8 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
             if (++s == C::kStages) { s = 0; ph ^= 1; }
             continue;
           }
-          if (lane == 0) mbar_arrive_tx(&full[s], C::kStage);
+          const bool el = elect_one();
+          if (el) mbar_arrive_tx(&full[s], C::kStage);
           __syncwarp();
           // A = X1^T: two 64-column chunks of the 64 k-rows
           if (p.a_gather) {
@@ -606,7 +704,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
             }
             tma_gather4(sa + ch * 8192 + rg * 512, &p.tmA, &full[s], m0 + 64 * ch, r[0], r[1],
                         r[2], r[3]);
-          } else if (lane == 0) {
+          } else if (el) {
             tma_3d(sa, &p.tmA, &full[s], 0, p0, m0 / 64);
           }
           // B = X2: BN/64 chunks of the 64 k-rows
@@ -622,7 +720,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
               tma_gather4(sb + ch * 8192 + rg * 512, &p.tmB, &full[s], n0 + 64 * ch, r[0], r[1],
                           r[2], r[3]);
             }
-          } else if (lane == 0) {
+          } else if (el) {
             tma_3d(sb, &p.tmB, &full[s], 0, p0, n0 / 64);
           }
           __syncwarp();
@@ -640,7 +738,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
     // instructions (the tensor pipe needs a new UMMA every 64-128 cycles).
     // CG = 2: only the leader CTA issues; its descriptors address the same
     // smem offsets in both CTAs.
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {  // the whole warp walks the loop (uniform); one elected lane issues
       const uint32_t idesc = ESTMM ? kIdescEst : (p.b_kmajor ? kIdescEsmmK : kIdescEsmmMN);
       // per UMMA_K (16) step, in 16-byte descriptor units: K-major = 32 B
       // inside the swizzle atom; MN-major = 16 k-rows = 2 x 1024 B
@@ -653,44 +751,45 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
       const uint64_t db0 = !b_mn ? sdesc(base + kABytes, 16, 1024)
                            : sw64 ? sdesc(base + kABytes, 4096, 512, 4)
                                   : sdesc(base + kABytes, 8192, 1024);
+      const uint32_t a_lo = static_cast<uint32_t>(da0), a_hi = static_cast<uint32_t>(da0 >> 32);
+      const uint32_t b_lo = static_cast<uint32_t>(db0), b_hi = static_cast<uint32_t>(db0 >> 32);
       constexpr uint32_t kStageUnits = C::kStage >> 4;
+      static_assert(BK / UK == 4, "umma_kblock issues four K=16 UMMAs per k-block");
+      const uint32_t skip = kDbg && (p.dbg_noload & 4) ? 1u : 0u;
       int s = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
       int it_ = 0;
       for (int wl = cluster; wl < total; wl += n_clusters, ++it_) {
         const int w = wmap(wl);
-        const SegTile t = p.tiles[w / per_item];
-        const int nk = ESTMM ? (t.end - t.begin + BK - 1) / BK : p.K / BK;
-        TRACE(it_, 0);
+        const int nk = ESTMM ? (p.tiles[w / per_item].end - p.tiles[w / per_item].begin + BK - 1) / BK
+                             : p.K / BK;
+        if (lane == 0) TRACE(it_, 0);
         if constexpr (CG == 2) mbar_wait_cl(&tempty[acc], aph ^ 1);
         else mbar_wait(&tempty[acc], aph ^ 1);
-        TRACE(it_, 1);
+        if (lane == 0) TRACE(it_, 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
         unsigned long long wsum = 0;
         for (int kb = 0; kb < nk; ++kb) {
-          const unsigned long long tw0 = (kTrace && p.trace) ? gtime() : 0;
+          const long long tw0 = (kTrace && p.trace) ? clock64() : 0;
           if constexpr (CG == 2) mbar_wait_cl(&full[s], ph);
           else mbar_wait(&full[s], ph);
-          if (kTrace && p.trace) wsum += gtime() - tw0;
+          if (kTrace && p.trace) wsum += clock64() - tw0;
           tc_fence_after();
-          const uint64_t da = da0 + s * kStageUnits, db = db0 + s * kStageUnits;
-#pragma unroll
-          for (int kk = 0; kk < BK / UK; ++kk) {
-            if (kTrace && (p.dbg_noload & 4)) break;
-            if constexpr (CG == 2)
-              umma_bf16_cg2(d, da + kk * a_step, db + kk * b_step, idesc, (kb | kk) != 0);
-            else
-              umma_bf16(d, da + kk * a_step, db + kk * b_step, idesc, (kb | kk) != 0);
-          }
-          if constexpr (CG == 2) umma_commit_cg2(&empty[s]);
-          else umma_commit(&empty[s]);
+          const uint32_t so = static_cast<uint32_t>(s) * kStageUnits;
+          if (elect_one())
+            umma_kblock<CG>(d, a_lo + so, a_hi, a_step, b_lo + so, b_hi, b_step, idesc, kb == 0,
+                            &empty[s], skip);
+          __syncwarp();
           if (++s == C::kStages) { s = 0; ph ^= 1; }
         }
-        if constexpr (CG == 2) umma_commit_cg2(&tfull[acc]);
-        else umma_commit(&tfull[acc]);
-        TRACE(it_, 2);
-        if (kTrace && p.trace && it_ < 64) p.trace[(static_cast<size_t>(blockIdx.x) * 64 + it_) * 8 + 6] = wsum;
+        if (elect_one()) {
+          if constexpr (CG == 2) umma_commit_cg2(&tfull[acc]);
+          else umma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (lane == 0) TRACE(it_, 2);
+        if (kTrace && p.trace && lane == 0 && it_ < 64) p.trace[(static_cast<size_t>(blockIdx.x) * 64 + it_) * 8 + 6] = wsum;
         if (++acc == 2) { acc = 0; aph ^= 1; }
       }
     }
@@ -812,6 +911,15 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
         else mbar_wait(&tfull[acc], aph);
         if (warp == 2 && lane == 0) TRACE(ep_it, 4);
         tc_fence_after();
+        if (kDbg && !dense_out && (p.dbg_noload & 32)) {  // debug: no epilogue work
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) release_acc(acc);
+          t_cur = t_nx;
+          orow_cur = has_nx ? orow_of(t_nx) : -1;
+          if (++acc == 2) { acc = 0; aph ^= 1; }
+          continue;
+        }
         const uint32_t taddr =
             tmem + (static_cast<uint32_t>(lg * 32) << 16) + acc * BN + half * HB;
         uint32_t rbuf[2][32];
@@ -902,7 +1010,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
             //     32-row slice at a segment end), one bulk group per chunk
             fence_async_smem();
             named_bar_sync(1 + half, 128);
-            if (elect && !(kTrace && (p.dbg_noload & 2))) {
+            if (elect && !(kDbg && (p.dbg_noload & 2))) {
               if (rows_here >= BM) {
                 // L2 policy: what the NEXT kernel reads stays (MODE 1: F(y1)
                 // for ESMM fwd2; MODE 2: g_y1 for ESTMM gW1 / ESMM gx), what
@@ -984,7 +1092,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
                 const int orr = __shfl_sync(0xffffffffu, orow, rr);
                 const float4 val =
                     *reinterpret_cast<const float4*>(stg + rr * 64 + ((cc ^ ((rr >> 1) & 3)) * 16));
-                if (orr < 0 || (kTrace && (p.dbg_noload & 2))) continue;
+                if (orr < 0 || (kDbg && (p.dbg_noload & 2))) continue;
                 if (p.n_peer > 0) {
                   // fused reduce-scatter: the token's owner rank, over peer memory
                   const int owner = static_cast<int>(orr / p.peer_rows);
@@ -1064,7 +1172,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
               const int rr = i * 8 + lane / 4, cc = lane % 4;
               const float4 val =
                   *reinterpret_cast<const float4*>(stg + rr * 64 + ((cc ^ ((rr >> 1) & 3)) * 16));
-              if (m0 + rr >= p.M || (kTrace && (p.dbg_noload & 2))) continue;
+              if (m0 + rr >= p.M || (kDbg && (p.dbg_noload & 2))) continue;
               if (p.n_peer > 0) {
                 // fused reduce-scatter of the weight gradient along H to the
                 // shard owners: rows (peer_dim 0, gW2) or columns (1, gW1)
@@ -1189,7 +1297,7 @@ hxm_status launch_bn_ew(const UParams& prm_in, int max_work, cudaStream_t st) {
   }
   // debug decomposition (HXM_DEBUG_NOLOAD bits: 1 = no operand loads, 2 = no
   // epilogue stores, 4 = no MMAs); results are garbage, timing only
-  if (kTrace) { const char* e = std::getenv("HXM_DEBUG_NOLOAD"); prm.dbg_noload = e ? std::atoi(e) : 0; }
+  if (kDbg) { const char* e = std::getenv("HXM_DEBUG_NOLOAD"); prm.dbg_noload = e ? std::atoi(e) : 0; }
   using C = Cfg<BN, CG, MODE, EW>;
   auto kern = umma_kernel<BN, MODE, CG, ACT, EW>;
   constexpr int kThreads = 64 + 32 * EW;

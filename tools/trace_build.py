@@ -6,4 +6,4 @@ sys.path.insert(0, os.getcwd())
 from paper_2411_01288_b200.build import CSRC, build  # noqa: E402
 
 os.utime(os.path.join(CSRC, "umma.cu"))
-build(extra=[] if "--off" in sys.argv else ["-DHXM_TRACE_BUILD"])
+build(extra=[] if "--off" in sys.argv else ["-DHXM_DBG_BUILD"] if "--dbg" in sys.argv else ["-DHXM_TRACE_BUILD"])

@@ -37,4 +37,4 @@ for cta in (0, 2, 74):
             break
         f = lambda v: (v - t0) / 1e3 if v else float("nan")  # noqa: E731
         print(f"  {i:2d}  mma {f(r[0]):7.2f} {f(r[1]):7.2f} {f(r[2]):7.2f}   epi {f(r[3]):7.2f} {f(r[4]):7.2f} {f(r[5]):7.2f}"
-              f"   mma-waits-full {r[6] / 1e3:6.2f}  producer-waits-empty {r[7] / 1e3:6.2f}")
+              f"   mma-waits-full {r[6] / 1965:6.2f}  producer-waits-empty {r[7] / 1965:6.2f}")
