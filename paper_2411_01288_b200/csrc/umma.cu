@@ -73,9 +73,10 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
-// Blocking phase wait.  A pipeline bug must not hang the GPU: after ~2^34
-// cycles (several seconds) without progress the kernel traps, which surfaces
-// as a CUDA error on the host instead of a wedged device.
+// Blocking phase wait.  A pipeline bug must not hang the GPU: after 2^28
+// failed polls (seconds) without progress the kernel traps, which surfaces as
+// a CUDA error on the host instead of a wedged device.  (A clock64 deadline
+// in the poll loop measurably slowed the pipeline hand-offs.)
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   uint32_t done;
@@ -86,17 +87,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "r"(a), "r"(parity)
       : "memory");
   if (done) return;
-#ifdef HXM_SIMPLE_WAIT
-  while (!done)
-    asm volatile(
-        "{\n.reg .pred P;\nmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n"
-        "selp.u32 %0, 1, 0, P;\n}\n"
-        : "=r"(done)
-        : "r"(a), "r"(parity)
-        : "memory");
-  return;
-#endif
+#ifdef HXM_CLOCK_WAIT
   const long long t0 = clock64();
+#else
+  uint32_t n = 0;
+#endif
   while (true) {
     asm volatile(
         "{\n.reg .pred P;\nmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n"
@@ -105,7 +100,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "r"(a), "r"(parity)
         : "memory");
     if (done) return;
+#ifdef HXM_CLOCK_WAIT
     if (clock64() - t0 > (1ll << 34)) __trap();
+#else
+    // every failed try_wait suspends the thread for up to a hardware time
+    // limit first, so 2^28 of them are many seconds
+    if (++n == (1u << 28)) __trap();
+#endif
   }
 }
 __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
