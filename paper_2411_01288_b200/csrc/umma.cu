@@ -626,25 +626,24 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
             // completion counted on the leader's full barrier
             if (elect_one()) {
               const uint32_t fb = full_lead + 8u * s;
-              if (kDbg && (p.dbg_noload & 1)) { mbar_arrive_cl(fb); __syncwarp(); if (++s == C::kStages) { s = 0; ph ^= 1; } continue; }
-              if (kDbg && (p.dbg_noload & 24)) {  // debug: A only (8) / B only (16)
+              if (kDbg && (p.dbg_noload & 1)) {  // debug: no operand loads
+                mbar_arrive_cl(fb);
+              } else if (kDbg && (p.dbg_noload & 24)) {  // debug: A only (8) / B only (16)
                 mbar_arrive_tx_cl(fb, (p.dbg_noload & 8) ? kABytes : C::kBBytes);
                 const int nb = n0 + static_cast<int>(rank) * (BN / 2);
                 if (p.dbg_noload & 8) tma_2d_cg2(sa, &p.tmA, fb, kb * BK, t.begin + static_cast<int>(rank) * BM);
                 else if (p.b_kmajor) tma_3d_cg2(sb, &p.tmB, fb, kb * BK, nb, t.expert);
                 else tma_4d_cg2(sb, &p.tmB, fb, 0, kb * BK, nb / (p.b_sw64 ? 32 : 64), t.expert);
-                __syncwarp();
-                if (++s == C::kStages) { s = 0; ph ^= 1; }
-                continue;
-              }
-              mbar_arrive_tx_cl(fb, C::kStage);
-              tma_2d_cg2(sa, &p.tmA, fb, kb * BK, t.begin + static_cast<int>(rank) * BM);
-              const int nb = n0 + static_cast<int>(rank) * (BN / 2);
-              if (p.b_kmajor) {
-                tma_3d_cg2(sb, &p.tmB, fb, kb * BK, nb, t.expert);
               } else {
-                // all of this CTA's swizzle-atom column chunks in one 4D box
-                tma_4d_cg2(sb, &p.tmB, fb, 0, kb * BK, nb / (p.b_sw64 ? 32 : 64), t.expert);
+                mbar_arrive_tx_cl(fb, C::kStage);
+                tma_2d_cg2(sa, &p.tmA, fb, kb * BK, t.begin + static_cast<int>(rank) * BM);
+                const int nb = n0 + static_cast<int>(rank) * (BN / 2);
+                if (p.b_kmajor) {
+                  tma_3d_cg2(sb, &p.tmB, fb, kb * BK, nb, t.expert);
+                } else {
+                  // all of this CTA's swizzle-atom column chunks in one 4D box
+                  tma_4d_cg2(sb, &p.tmB, fb, 0, kb * BK, nb / (p.b_sw64 ? 32 : 64), t.expert);
+                }
               }
             }
           } else {
@@ -681,11 +680,14 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
           if constexpr (CG == 2) {  // dense only (host guarantees)
             if (elect_one()) {
               const uint32_t fb = full_lead + 8u * s;
-              if (kDbg && (p.dbg_noload & 1)) { mbar_arrive_cl(fb); __syncwarp(); if (++s == C::kStages) { s = 0; ph ^= 1; } continue; }
-              mbar_arrive_tx_cl(fb, C::kStage);
-              // both 64-column chunks of A, all chunks of B: one 3D box each
-              tma_3d_cg2(sa, &p.tmA, fb, 0, p0, m0 / 64);
-              tma_3d_cg2(sb, &p.tmB, fb, 0, p0, n0 / (p.b_sw64 ? 32 : 64));
+              if (kDbg && (p.dbg_noload & 1)) {  // debug: no operand loads
+                mbar_arrive_cl(fb);
+              } else {
+                mbar_arrive_tx_cl(fb, C::kStage);
+                // both 64-column chunks of A, all chunks of B: one 3D box each
+                tma_3d_cg2(sa, &p.tmA, fb, 0, p0, m0 / 64);
+                tma_3d_cg2(sb, &p.tmB, fb, 0, p0, n0 / (p.b_sw64 ? 32 : 64));
+              }
             }
             __syncwarp();
             if (++s == C::kStages) { s = 0; ph ^= 1; }
