@@ -869,8 +869,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
         const int w_nx = has_nx ? wmap(wl + n_clusters) : 0;
         const SegTile t_nx = has_nx ? tile_at(w_nx) : SegTile{0, 0, 0, 0};  // prefetch
         int orow_nx = -1;
-        float bias_nx = 0.f;
-        if (bias_smem && has_nx && lane < kBq) bias_nx = bias_at(t_nx, w_nx);
+        float bias_nx = 0.f;  // loaded during the last chunk (short register lifetime)
         const int n0 = rem * BN + half * HB;
         const int orow = orow_cur;
         const int N = p.N;
@@ -925,7 +924,11 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
         }
         const uint32_t taddr =
             tmem + (static_cast<uint32_t>(lg * 32) << 16) + acc * BN + half * HB;
-        uint32_t rbuf[2][32];
+        // 8 epilogue warps double-buffer the TMEM loads (the next chunk's
+        // load overlaps this chunk's math); 16 warps hide the latency with
+        // each other and keep the 32 registers (their budget is 112)
+        constexpr bool kTmemDB = EW == 8;
+        uint32_t rbuf[kTmemDB ? 2 : 1][32];
         tmem_ld32_async(taddr, rbuf[0]);
         tmem_wait();
         if (HB == 32) {
@@ -935,11 +938,22 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
         }
 #pragma unroll
         for (int c0 = 0; c0 < HB; c0 += 32) {
-          uint32_t (&r)[32] = rbuf[(c0 / 32) & 1];
-          // next chunk's TMEM load overlaps this chunk's math
-          if (c0 + 32 < HB) tmem_ld32_async(taddr + c0 + 32, rbuf[((c0 / 32) + 1) & 1]);
+          uint32_t (&r)[32] = rbuf[kTmemDB ? (c0 / 32) & 1 : 0];
+          if constexpr (kTmemDB) {
+            // next chunk's TMEM load overlaps this chunk's math
+            if (c0 + 32 < HB) tmem_ld32_async(taddr + c0 + 32, rbuf[((c0 / 32) + 1) & 1]);
+          } else if (c0 > 0) {
+            tmem_ld32_async(taddr + c0, rbuf[0]);
+            tmem_wait();
+            if (c0 + 32 >= HB) {  // last TMEM load landed: free the accumulator
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) release_acc(acc);
+            }
+          }
           // the next item's output row (its tile was loaded at this item's start)
           if (c0 == 0 && has_nx) orow_nx = orow_of(t_nx);
+          if (c0 + 32 >= HB && bias_smem && has_nx && lane < kBq) bias_nx = bias_at(t_nx, w_nx);
           const int n = n0 + c0;
           float v[32];
 #pragma unroll
@@ -1119,7 +1133,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
               }
             }
           }
-          if (c0 + 32 < HB) {
+          if (kTmemDB && c0 + 32 < HB) {
             tmem_wait();
             if (c0 + 64 >= HB) {  // last TMEM load landed: free the accumulator
               tc_fence_before();
