@@ -908,6 +908,9 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
         const float4* bias4 =
             has_bias ? reinterpret_cast<const float4*>(p.bias + static_cast<int64_t>(t.expert) * N + n0)
                      : nullptr;
+        // the group's bias entries for this item (written by all four
+        // warps at the previous item's end / before the loop) are complete
+        if (bias_smem) named_bar_sync(1 + half, 128);
         if (warp == 2 && lane == 0) TRACE(ep_it, 3);
         if constexpr (CG == 2) mbar_wait_cl(&tfull[acc], aph);
         else mbar_wait(&tfull[acc], aph);
@@ -972,6 +975,23 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
             const int hrow = lg * 32 + lane;  // this thread's row in the 128-row box
             const int swz = (hrow >> 1) & 3;  // TMA 64B swizzle: chunk ^= (row >> 1) & 3
             uint8_t* obox = hstage + (dchunk % C::kOutBufs) * C::kOutBox;
+            // MODE 1: the chunk's math (bias + F, F' packed to bf16) before
+            // the box barrier, overlapping the previous store's smem read
+            uint32_t o1[16], o2[16];
+            if (!bwd) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                float2 f, df, x = make_float2(v[2 * i], v[2 * i + 1]);
+                if (bias_smem) {  // uniform-address LDS: broadcast
+                  const float2 b = *reinterpret_cast<const float2*>(gbias + c0 + 2 * i);
+                  x = f2_fma(x, f2(1.f), b);
+                }
+                // activation fixed at compile time (MODE 1 instantiations)
+                act_pair<ACT>(x, f, df);
+                o1[i] = pad ? 0u : pack_bf16(df.x, df.y);
+                o2[i] = pad ? 0u : pack_bf16(f.x, f.y);
+              }
+            }
             // (1) the store that last used this box has read its smem, and
             //     every thread is past the previous chunk's F'(y1) reads
             if (elect) {
@@ -992,23 +1012,15 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
             }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              uint32_t a1[4], a2[4];
               if (!bwd) {
                 // stash = (F'(y1), F(y1)): everything the backward needs
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  float2 f, df, x = make_float2(v[8 * j + 2 * i], v[8 * j + 2 * i + 1]);
-                  if (bias_smem) {  // uniform-address LDS: broadcast
-                    const float2 b = *reinterpret_cast<const float2*>(gbias + c0 + 8 * j + 2 * i);
-                    x = f2_fma(x, f2(1.f), b);
-                  }
-                  // activation fixed at compile time (MODE 1 instantiations)
-                  act_pair<ACT>(x, f, df);
-                  a1[i] = pad ? 0u : pack_bf16(df.x, df.y);
-                  a2[i] = pad ? 0u : pack_bf16(f.x, f.y);
-                }
+                *reinterpret_cast<uint4*>(obox + hrow * 64 + ((j ^ swz) * 16)) =
+                    make_uint4(o1[4 * j], o1[4 * j + 1], o1[4 * j + 2], o1[4 * j + 3]);
+                *reinterpret_cast<uint4*>(obox + 8192 + hrow * 64 + ((j ^ swz) * 16)) =
+                    make_uint4(o2[4 * j], o2[4 * j + 1], o2[4 * j + 2], o2[4 * j + 3]);
               } else {
                 // g_y1 = g_y2 * F'(y1)
+                uint32_t a1[4];
                 const __nv_bfloat16* yb = reinterpret_cast<const __nv_bfloat16*>(&dv[j]);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
@@ -1016,12 +1028,9 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
                                           __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(yb)[i]));
                   a1[i] = pad ? 0u : pack_bf16(g.x, g.y);
                 }
+                *reinterpret_cast<uint4*>(obox + hrow * 64 + ((j ^ swz) * 16)) =
+                    make_uint4(a1[0], a1[1], a1[2], a1[3]);
               }
-              *reinterpret_cast<uint4*>(obox + hrow * 64 + ((j ^ swz) * 16)) =
-                  make_uint4(a1[0], a1[1], a1[2], a1[3]);
-              if (!bwd)
-                *reinterpret_cast<uint4*>(obox + 8192 + hrow * 64 + ((j ^ swz) * 16)) =
-                    make_uint4(a2[0], a2[1], a2[2], a2[3]);
             }
             // (2) box complete -> one TMA store per output (or per valid
             //     32-row slice at a segment end), one bulk group per chunk
