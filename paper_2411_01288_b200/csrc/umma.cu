@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(&full[s], CG);  // CG = 2: both CTAs' producers arrive on the leader's
+      mbar_init(&full[s], 1);  // CG = 2: the leader's producer expects both CTAs' bytes
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -627,15 +627,17 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
             if (elect_one()) {
               const uint32_t fb = full_lead + 8u * s;
               if (kDbg && (p.dbg_noload & 1)) {  // debug: no operand loads
-                mbar_arrive_cl(fb);
+                if (rank == 0) mbar_arrive(&full[s]);
               } else if (kDbg && (p.dbg_noload & 24)) {  // debug: A only (8) / B only (16)
-                mbar_arrive_tx_cl(fb, (p.dbg_noload & 8) ? kABytes : C::kBBytes);
+                if (rank == 0) mbar_arrive_tx(&full[s], 2 * ((p.dbg_noload & 8) ? kABytes : C::kBBytes));
                 const int nb = n0 + static_cast<int>(rank) * (BN / 2);
                 if (p.dbg_noload & 8) tma_2d_cg2(sa, &p.tmA, fb, kb * BK, t.begin + static_cast<int>(rank) * BM);
                 else if (p.b_kmajor) tma_3d_cg2(sb, &p.tmB, fb, kb * BK, nb, t.expert);
                 else tma_4d_cg2(sb, &p.tmB, fb, 0, kb * BK, nb / (p.b_sw64 ? 32 : 64), t.expert);
               } else {
-                mbar_arrive_tx_cl(fb, C::kStage);
+                // the leader expects both CTAs' bytes; the peer's loads
+                // only complete_tx on it (no second remote arrive)
+                if (rank == 0) mbar_arrive_tx(&full[s], 2 * C::kStage);
                 tma_2d_cg2(sa, &p.tmA, fb, kb * BK, t.begin + static_cast<int>(rank) * BM);
                 const int nb = n0 + static_cast<int>(rank) * (BN / 2);
                 if (p.b_kmajor) {
@@ -681,9 +683,9 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
             if (elect_one()) {
               const uint32_t fb = full_lead + 8u * s;
               if (kDbg && (p.dbg_noload & 1)) {  // debug: no operand loads
-                mbar_arrive_cl(fb);
+                if (rank == 0) mbar_arrive(&full[s]);
               } else {
-                mbar_arrive_tx_cl(fb, C::kStage);
+                if (rank == 0) mbar_arrive_tx(&full[s], 2 * C::kStage);
                 // both 64-column chunks of A, all chunks of B: one 3D box each
                 tma_3d_cg2(sa, &p.tmA, fb, 0, p0, m0 / 64);
                 tma_3d_cg2(sb, &p.tmB, fb, 0, p0, n0 / (p.b_sw64 ? 32 : 64));
