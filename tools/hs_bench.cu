@@ -5,6 +5,8 @@
 //   mode 0: MMA thread releases stages with tcgen05.commit (multicast to both CTAs)
 //   mode 1: plain remote mbarrier arrives instead of tcgen05.commit
 //   mode 2: like 0, the producer's lane 0 alone (no __syncwarp)
+//   mode 3: like 0, only the leader's producer arrives (local), count 1
+//   mode 4: everything CTA-local (leader only; plain local arrives)
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -43,7 +45,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) { init(&full[s], 2); init(&empty[s], 1); }
+    for (int s = 0; s < S; ++s) { init(&full[s], mode >= 3 ? 1 : 2); init(&empty[s], 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1)
@@ -56,8 +58,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
     int s = 0; uint32_t ph = 0;
     for (int kb = 0; kb < nk; ++kb) {
       if (mode == 2 && lane != 0) break;
+      if (mode >= 3 && rank != 0) break;
       wait(&empty[s], ph ^ 1);
-      if (lane == 0) arrive_cl(mapa(su32(&full[s]), 0));
+      if (lane == 0) {
+        if (mode >= 3)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&full[s])) : "memory");
+        else
+          arrive_cl(mapa(su32(&full[s]), 0));
+      }
       if (mode != 2) __syncwarp();
       if (++s == S) { s = 0; ph ^= 1; }
     }
@@ -66,7 +74,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
     for (int kb = 0; kb < nk; ++kb) {
       wait(&full[s], ph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (mode == 1) {
+      if (mode == 4) {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[s])) : "memory");
+      } else if (mode == 1) {
         arrive_cl(mapa(su32(&empty[s]), 0));
         arrive_cl(mapa(su32(&empty[s]), 1));
       } else {
@@ -91,8 +101,8 @@ int main() {
   long long* d;
   cudaMalloc(&d, 148 * sizeof(long long));
   const int nk = 24 * 100;
-  for (int mode = 0; mode < 3; ++mode) {
-    for (int grid : {1, 2, 7, 14}) {
+  for (int mode = 0; mode < 5; ++mode) {
+    for (int grid : {1, 7}) {
       cudaMemset(d, 0, 148 * sizeof(long long));
       auto k = grid == 1 ? hs<1> : grid == 2 ? hs<2> : grid == 7 ? hs<7> : hs<14>;
       k<<<148, 128>>>(nk, mode, d);
