@@ -421,14 +421,19 @@ __global__ void __launch_bounds__(kThreads) fwd_prologue(FwdPrologue a) {
         __syncwarp();
       }
     }
-    if (blockIdx.x == gridDim.x - 1) {
+    // the three tilings on three different blocks (the last ones), so no
+    // block carries all of them into the grid barrier
+    const int tb = static_cast<int>(gridDim.x) - 1 - static_cast<int>(blockIdx.x);
+    const bool one = gridDim.x < 3;  // (tiny grids: the last block does all three)
+    if (tb == 0)
       tile_pass<int32_t, kThreads>(sidx, E, a.s0.rows, a.s0.min_one, a.s0.tiles, a.s0.tile_off,
                                    a.s0.n_tiles, a.total, a.s0.split_rows);
+    if (one ? tb == 0 : tb == 1)
       tile_pass<int32_t, kThreads>(sidx, E, a.s1.rows, a.s1.min_one, a.s1.tiles, a.s1.tile_off,
                                    a.s1.n_tiles, a.total, a.s1.split_rows);
+    if (one ? tb == 0 : tb == 2)
       tile_pass<int32_t, kThreads>(sidx, E, a.s2.rows, a.s2.min_one, a.s2.tiles, a.s2.tile_off,
                                    a.s2.n_tiles, a.total, a.s2.split_rows);
-    }
   }
   pro_ts(5);
   if (!a.x) return;
