@@ -431,7 +431,9 @@ __device__ __forceinline__ float tanh_approx(float u) {
   return t;
 }
 // F and F' of two values at once (tensor.cpp:39-53, 62-72); GELU-tanh with
-// one tanh.approx per value shared by F and F', the rest in f32x2 ops.
+// one tanh.approx per value shared by F and F', the rest in f32x2 ops:
+// with s = (1 + tanh u) / 2,  F = x s  and  F' = s + 2 u'(x) F (1 - s)
+// (1 - tanh^2 u = 4 s (1 - s)): 9 packed ops per pair.
 template <int ACT>
 __device__ __forceinline__ void act_pair(float2 x, float2& f, float2& df) {
   if constexpr (ACT == HXM_ACT_GELU) {
@@ -439,11 +441,11 @@ __device__ __forceinline__ void act_pair(float2 x, float2& f, float2& df) {
     const float2 x2 = f2_mul(x, x);
     const float2 u = f2_mul(x, f2_fma(f2(k1), x2, f2(k0)));
     const float2 t = make_float2(tanh_approx(u.x), tanh_approx(u.y));
-    const float2 hx = f2_mul(x, f2(0.5f));
-    f = f2_fma(hx, t, hx);
-    const float2 du = f2_fma(f2(3.f * k1), x2, f2(k0));
-    const float2 omt = f2_fma(make_float2(-t.x, -t.y), t, f2(1.f));
-    df = f2_fma(f2_mul(hx, omt), du, f2_fma(t, f2(0.5f), f2(0.5f)));
+    const float2 s = f2_fma(t, f2(0.5f), f2(0.5f));
+    f = f2_mul(x, s);
+    const float2 du2 = f2_fma(f2(6.f * k1), x2, f2(2.f * k0));  // 2 u'(x)
+    const float2 oms = f2_fma(s, f2(-1.f), f2(1.f));
+    df = f2_fma(du2, f2_mul(f, oms), s);
   } else if constexpr (ACT == HXM_ACT_RELU) {
     f = make_float2(x.x > 0.f ? x.x : 0.f, x.y > 0.f ? x.y : 0.f);
     df = make_float2(x.x > 0.f ? 1.f : 0.f, x.y > 0.f ? 1.f : 0.f);
@@ -973,7 +975,12 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
             }
           }
           if (dense_out) {
-            const bool pad = orow < 0;  // padding slot -> zero row
+            // MODE 1 stores its padding slots' rows unmasked: their x_s rows
+            // are zero (prologue), so y1 = b1 gives finite F, F' that fwd2
+            // drops and that meet zero g_y_s rows in the backward.  MODE 2
+            // masks them: the fused gb1 column sums read the whole staged box,
+            // including rows past the segment end
+            const bool pad = orow < 0;
             const int hrow = lg * 32 + lane;  // this thread's row in the 128-row box
             const int swz = (hrow >> 1) & 3;  // TMA 64B swizzle: chunk ^= (row >> 1) & 3
             uint8_t* obox = hstage + (dchunk % C::kOutBufs) * C::kOutBox;
@@ -990,8 +997,8 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
                 }
                 // activation fixed at compile time (MODE 1 instantiations)
                 act_pair<ACT>(x, f, df);
-                o1[i] = pad ? 0u : pack_bf16(df.x, df.y);
-                o2[i] = pad ? 0u : pack_bf16(f.x, f.y);
+                o1[i] = pack_bf16(df.x, df.y);
+                o2[i] = pack_bf16(f.x, f.y);
               }
             }
             // (1) the store that last used this box has read its smem, and
