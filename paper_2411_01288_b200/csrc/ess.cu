@@ -200,7 +200,9 @@ __global__ void __launch_bounds__(NT) ess_partial(EssArgs a) {
 // the block's W warps split the rows (4 rows in flight per warp, each lane
 // 4 columns), then fixed-order smem combine -> deterministic, and a long
 // reduction (a skewed expert's hundreds of tiles) is W-way parallel.
-template <int W>
+// kFresh: the partial rows were written by other blocks of the running
+// kernel -- read them through L2 (ld.global.cg), not the read-only path
+template <int W, bool kFresh = false>
 __device__ __forceinline__ void combine_block(const float* __restrict__ partial, int64_t r0,
                                               int64_t r1, int64_t d, int64_t c0,
                                               float* __restrict__ out_row) {
@@ -216,11 +218,13 @@ __device__ __forceinline__ void combine_block(const float* __restrict__ partial,
       const int64_t rr = r + u * W;
       const float* row = partial + rr * d;
       if (rr < r1 && vec) {
-        const float4 q = __ldg(reinterpret_cast<const float4*>(row + c));
+        const float4 q = kFresh ? __ldcg(reinterpret_cast<const float4*>(row + c))
+                                : __ldg(reinterpret_cast<const float4*>(row + c));
         v[u][0] = q.x; v[u][1] = q.y; v[u][2] = q.z; v[u][3] = q.w;
       } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) v[u][j] = (rr < r1 && c + j < d) ? __ldg(row + c + j) : 0.f;
+        for (int j = 0; j < 4; ++j)
+          v[u][j] = (rr < r1 && c + j < d) ? (kFresh ? __ldcg(row + c + j) : __ldg(row + c + j)) : 0.f;
       }
     }
 #pragma unroll
@@ -348,13 +352,13 @@ hxm_status gather_typed(const void* src, RowMap map, int64_t d, const IdxT* idx,
 }
 
 // ------------------------------------------------ fused backward prologue --
-// One cooperative launch before the backward GEMMs: g_x = 0, zeroed gW
-// slices of the experts whose ESTMM is split over chunks (they accumulate
-// with red.add), gb2 partials of g_y fused with its expert-sorted copy
-// (ESS, es_ops.cpp:86-102) | grid barrier | per-expert gb2 combine.
+// One launch before the backward GEMMs: g_x = 0, zeroed gW slices of the
+// experts whose ESTMM is split over chunks (they accumulate with red.add),
+// gb2 partials of g_y fused with its expert-sorted copy (ESS,
+// es_ops.cpp:86-102), and each expert's gb2 combine by the block that
+// finishes its last ESS item.
 template <class T, int VEC>
 __global__ void __launch_bounds__(NT) bwd_prologue(BwdPrologue b) {
-  namespace cgp = cooperative_groups;
   const int64_t gtid = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x;
   const int64_t gthreads = static_cast<int64_t>(gridDim.x) * NT;
   {
@@ -389,23 +393,50 @@ __global__ void __launch_bounds__(NT) bwd_prologue(BwdPrologue b) {
   }
   const EssArgs& a = b.es;
   const int col_groups = static_cast<int>((a.d + VEC - 1) / VEC);
-  if (VEC > 1 && col_groups <= 32 * 2 && a.d % VEC == 0) {
-    // whole rows per item (D <= 64 * VEC): one round of items, no half slabs
-    for (int ti = blockIdx.x; ti < *a.n_tiles; ti += gridDim.x) ess_item_rows<T, VEC, 2>(a, ti);
-  } else {
-    const int slabs = static_cast<int>(ceil_div(col_groups, 32));
-    const int items = *a.n_tiles * slabs;
-    for (int it = blockIdx.x; it < items; it += gridDim.x)
-      ess_item<T, VEC>(a, it / slabs, it % slabs);
-  }
-  if (!a.out) return;
-  cgp::this_grid().sync();
+  const bool rows = VEC > 1 && col_groups <= 32 * 2 && a.d % VEC == 0;
+  const int slabs = rows ? 1 : static_cast<int>(ceil_div(col_groups, 32));
   const int chunks = static_cast<int>(ceil_div(a.d, 128));
-  for (int it = blockIdx.x; it < a.n_experts * chunks; it += gridDim.x) {
-    const int e = it / chunks;
-    combine_block<NT / 32>(a.partial, a.tile_off[e], a.tile_off[e + 1], a.d,
-                           static_cast<int64_t>(it % chunks) * 128,
-                           a.out + static_cast<int64_t>(e) * a.d);
+  // gb2 of an expert without positions is zero
+  if (a.out)
+    for (int e = blockIdx.x; e < a.n_experts; e += gridDim.x)
+      if (a.tile_off[e + 1] == a.tile_off[e])
+        for (int64_t c = threadIdx.x; c < a.d; c += NT) a.out[static_cast<int64_t>(e) * a.d + c] = 0.f;
+  // after an item: the block that brings an expert's item count to its total
+  // combines that expert's partial rows (fixed order: deterministic) -- no
+  // grid-wide barrier; the counter is left at zero for the next call
+  __shared__ int last;
+  auto arrive = [&](int ti) {
+    if (!a.out) return;
+    const int e = a.tiles[ti].expert;
+    __syncthreads();  // every thread's partial stores of this item are issued
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const int total = (a.tile_off[e + 1] - a.tile_off[e]) * slabs;
+      last = atomicAdd(&b.done[e], 1) == total - 1;
+      if (last) {
+        b.done[e] = 0;
+        __threadfence();
+      }
+    }
+    __syncthreads();
+    if (last)
+      for (int c = 0; c < chunks; ++c)
+        combine_block<NT / 32, true>(a.partial, a.tile_off[e], a.tile_off[e + 1], a.d,
+                                     static_cast<int64_t>(c) * 128,
+                                     a.out + static_cast<int64_t>(e) * a.d);
+  };
+  if (rows) {
+    // whole rows per item (D <= 64 * VEC): one round of items, no half slabs
+    for (int ti = blockIdx.x; ti < *a.n_tiles; ti += gridDim.x) {
+      ess_item_rows<T, VEC, 2>(a, ti);
+      arrive(ti);
+    }
+  } else {
+    const int items = *a.n_tiles * slabs;
+    for (int it = blockIdx.x; it < items; it += gridDim.x) {
+      ess_item<T, VEC>(a, it / slabs, it % slabs);
+      arrive(it / slabs);
+    }
   }
 }
 
@@ -422,7 +453,7 @@ hxm_status bwd_prologue_typed(BwdPrologue& b, cudaStream_t st) {
   if (occ < 1) return invalid_arg("backward prologue: cannot be resident");
   const int grid = sm_count() * std::min(occ, 4);
   void* args[] = {&b};
-  HXM_TRY_CUDA(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(NT), args, 0, st));
+  HXM_TRY_CUDA(cudaLaunchKernel(kern, dim3(grid), dim3(NT), args, 0, st));
   HXM_CHECK_LAUNCH();
   return HXM_OK;
 }

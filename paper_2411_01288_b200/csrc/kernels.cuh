@@ -142,6 +142,8 @@ struct BwdPrologue {
   int64_t gw2_slice;
   float* gw1;
   int64_t gw1_slice;
+  int32_t* done;  // E ESS arrival counters (zero on entry, left zero): the block
+                  // that finishes an expert's last ESS item combines its gb2
 };
 hxm_status launch_bwd_prologue(hxm_dtype dt, BwdPrologue b, cudaStream_t st);
 

@@ -45,6 +45,7 @@ struct LayerWs {
   int32_t* etiles_off;
   int32_t* n_etiles;
   float* partial;
+  int32_t* done;  // bwd prologue: per-expert ESS arrival counters
   void* xs;   // x in expert-sorted slot order (forward stash)
   void* gys;  // g_y in expert-sorted slot order (backward scratch)
   void* y1s;
@@ -97,6 +98,7 @@ LayerWs carve(Arena& ar, const hxm_layer_desc& d) {
   w.etiles = ar.take<SegTile>(w.max_etiles);
   w.etiles_off = ar.take<int32_t>(d.n_experts + 1);
   w.n_etiles = ar.take<int32_t>(1);
+  w.done = ar.take<int32_t>(d.n_experts);
   w.partial = ar.take<float>(static_cast<size_t>(w.max_etiles) * std::max(d.hidden, d.d_out));
   const size_t stash = static_cast<size_t>(w.bound) * d.hidden * esize(d.dtype);
   w.xs = ar.take<char>(static_cast<size_t>(w.bound) * d.d_in * esize(d.dtype));
@@ -227,6 +229,8 @@ hxm_status layer_forward(const hxm_layer_desc* d, const void* x, const void* w1,
     pro.y = y;
     pro.y_elems = yp ? 0 : N * d->d_out;  // peer rows: each owner zeroes its own
     pro.status = status;
+    pro.zero_i32 = w.done;
+    pro.zero_n = static_cast<int>(E);
     pro.ws = w.rws;
     pro.ws_bytes = w.rws_bytes;
     // algorithmic bytes: assignments read twice, v written, every routed
@@ -330,7 +334,7 @@ hxm_status layer_backward(const hxm_layer_desc* d, const void* x, const void* w1
   es.label = "ess_gb2";
   es.work = kn * Do * esz + static_cast<double>(E) * Do * 4.0;
   {
-    // one cooperative launch: gx = 0, split experts' gW slices = 0, and the
+    // one launch: gx = 0, split experts' gW slices = 0, and the
     // gb2 ESS fused with the expert-sorted copy of g_y
     BwdPrologue bp{};
     bp.label = "bwd_prologue";
@@ -343,6 +347,7 @@ hxm_status layer_backward(const hxm_layer_desc* d, const void* x, const void* w1
     bp.gw2_slice = H * Do;
     bp.gw1 = gw1p ? nullptr : gw1;
     bp.gw1_slice = Di * H;
+    bp.done = w.done;
     // algorithmic bytes: g_y read once per routed slot, its sorted copy
     // written, gb2 written, gx zeroed (split-expert zeroing is data-dependent)
     bp.work = 2.0 * kn * Do * esz + static_cast<double>(E) * Do * 4.0 + 4.0 * N * Di;

@@ -318,6 +318,8 @@ __global__ void __launch_bounds__(kThreads) fwd_prologue(FwdPrologue a) {
   const int64_t gtid = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
   const int64_t gthreads = static_cast<int64_t>(gridDim.x) * kThreads;
   // ---- 1: validation, per-chunk histograms --------------------------------
+  if (a.zero_i32 && blockIdx.x == 0)
+    for (int i = threadIdx.x; i < a.zero_n; i += kThreads) a.zero_i32[i] = 0;
   {
     int32_t* h = reinterpret_cast<int32_t*>(smem_raw) + warp * E;
     for (int c = gwarp; c < a.nchunks; c += nwarps) {

@@ -44,6 +44,8 @@ struct FwdPrologue {
   float* y;
   int64_t y_elems;
   int32_t* status;
+  int32_t* zero_i32;  // optional: zeroed in phase 1 (the backward prologue's
+  int zero_n;         // per-expert ESS arrival counters)
   void* ws;  // reindex scratch (reindex_ws_bytes)
   size_t ws_bytes;
   // filled by the launcher
