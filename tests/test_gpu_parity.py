@@ -337,6 +337,32 @@ def test_layer_c2_full_size_properties():
     assert torch.isfinite(g.gw1).all() and torch.isfinite(g.gx).all()
 
 
+def test_layer_backward_repeatable_gb2_combine():
+    """The backward prologue combines gb2 per expert in the block that brings
+    the expert's ESS items to completion (per-expert arrival counters that
+    reset themselves): repeated backward passes on one stash give
+    bit-identical bias gradients, an expert without tokens gets gb2 = 0, and
+    with g_y = ones gb2[e] is the exact slot count."""
+    H = hx()
+    E, k, D, Hd, N = 16, 2, 128, 256, 3000
+    p, x = H.make_random_params(E, D, Hd, D, "gelu", seed=11, n_tokens=N)
+    r = H.synthesize_routing(N, E, k, "uniform", 12)
+    a = r.assignments.copy()
+    a[:, :] = np.where(a == 15, 14, a)  # expert 15 empty
+    bad = a[0] == a[1]
+    a[1, bad] = (a[0, bad] + 1) % 15
+    r = H.RoutingChoice(N, E, k, a)
+    ones = torch.ones(N, D, dtype=torch.bfloat16, device="cuda")
+    fw = H.moe_forward(x, p, r)
+    runs = [H.moe_backward(fw.stash, p, ones) for _ in range(3)]
+    counts = np.bincount(a.ravel(), minlength=E).astype(np.float64)
+    assert counts[15] == 0
+    for g in runs:
+        assert np.array_equal(host(g.gb2), np.repeat(counts[:, None], D, axis=1))
+        assert torch.equal(g.gb1, runs[0].gb1)
+        assert torch.equal(g.gx, runs[0].gx)
+
+
 def test_layer_c4_full_size_properties():
     """BASELINE.json c4 at its full 131072 tokens on one GPU (64 experts
     top-2, d 1024, ffn 4096): size-independent exact properties instead of
