@@ -37,7 +37,6 @@ constexpr int UK = 16;   // UMMA K for kind::f16
 __host__ __device__ constexpr int epi_warps(int bn, int mode) {
   return (mode == 1 || mode == 2 || mode == 3) && bn == 256 ? 16 : 8;
 }
-__host__ __device__ constexpr int kthreads(int bn, int mode) { return 64 + 32 * epi_warps(bn, mode); }
 constexpr uint32_t kTmemCols = 512;
 constexpr int kABytes = BM * BK * 2;  // 16 KB
 
@@ -227,14 +226,10 @@ __device__ __forceinline__ uint32_t mapa0(uint32_t local) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(local));
   return r;
 }
-// Arrivals on the leader's barriers.  Default (cta-scope) semantics, as in
-// CUTLASS's ClusterBarrier: what they order is TMA / TMEM traffic, which the
-// tcgen05 fences cover; a .cluster-scope release/acquire would make ptxas
-// emit MEMBAR / CCTL.IVALL (L1 invalidation) on every spin.
-__device__ __forceinline__ void mbar_arrive_tx_cl(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cluster.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-               : "memory");
-}
+// Arrival on the leader's barrier (the epilogues' accumulator release).
+// Default (cta-scope) semantics, as in CUTLASS's ClusterBarrier: what it
+// orders is TMEM traffic, which the tcgen05 fences cover; a .cluster-scope
+// release/acquire would make ptxas emit MEMBAR / CCTL.IVALL on every spin.
 __device__ __forceinline__ void mbar_arrive_cl(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
 }
