@@ -90,6 +90,20 @@ struct Arena {
 };
 
 // --------------------------------------------------------------- device --
+// out[0:n] = 0 by a grid-stride loop (thread t0 of `stride`): 256-bit stores
+// (STG.256) when out is 32-byte aligned, a scalar tail
+__device__ __forceinline__ void zero_f32(float* out, int64_t n, int64_t t0, int64_t stride) {
+  int64_t done = 0;
+  if ((reinterpret_cast<uintptr_t>(out) & 31) == 0) {
+    const int64_t n8 = n / 8;
+    const float z = 0.f;
+    for (int64_t i = t0; i < n8; i += stride)
+      asm volatile("st.global.v8.f32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1};" ::"l"(out + 8 * i), "f"(z)
+                   : "memory");
+    done = n8 * 8;
+  }
+  for (int64_t i = done + t0; i < n; i += stride) out[i] = 0.f;
+}
 __device__ __forceinline__ float to_f32(float v) { return v; }
 __device__ __forceinline__ float to_f32(__nv_bfloat16 v) {
   return __bfloat162float(v);

@@ -361,12 +361,7 @@ template <class T, int VEC>
 __global__ void __launch_bounds__(NT) bwd_prologue(BwdPrologue b) {
   const int64_t gtid = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x;
   const int64_t gthreads = static_cast<int64_t>(gridDim.x) * NT;
-  {
-    float4* g4 = reinterpret_cast<float4*>(b.gx);
-    const int64_t n4 = b.gx_elems / 4;
-    for (int64_t i = gtid; i < n4; i += gthreads) g4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int64_t i = n4 * 4 + gtid; i < b.gx_elems; i += gthreads) b.gx[i] = 0.f;
-  }
+  zero_f32(b.gx, b.gx_elems, gtid, gthreads);
   // split experts: 16 block-sized parts of each first chunk's slices
   constexpr int kParts = 64;
   const int nk = *b.n_ktiles;

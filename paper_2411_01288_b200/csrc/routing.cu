@@ -377,12 +377,7 @@ __global__ void __launch_bounds__(kThreads) fwd_prologue(FwdPrologue a) {
     const int zb0 = gridDim.x > static_cast<unsigned>(E) ? E : 0;
     const int64_t zt = static_cast<int64_t>(blockIdx.x - zb0) * kThreads + threadIdx.x;
     const int64_t zn = static_cast<int64_t>(gridDim.x - zb0) * kThreads;
-    if (static_cast<int>(blockIdx.x) >= zb0) {
-      float4* y4 = reinterpret_cast<float4*>(a.y);
-      const int64_t n4 = a.y_elems / 4;
-      for (int64_t i = zt; i < n4; i += zn) y4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int64_t i = n4 * 4 + zt; i < a.y_elems; i += zn) a.y[i] = 0.f;
-    }
+    if (static_cast<int>(blockIdx.x) >= zb0) zero_f32(a.y, a.y_elems, zt, zn);
   }
   pro_ts(3);
   grid.sync();
