@@ -86,11 +86,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "r"(a), "r"(parity)
       : "memory");
   if (done) return;
-#ifdef HXM_CLOCK_WAIT
-  const long long t0 = clock64();
-#else
   uint32_t n = 0;
-#endif
   while (true) {
     asm volatile(
         "{\n.reg .pred P;\nmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n"
@@ -99,13 +95,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "r"(a), "r"(parity)
         : "memory");
     if (done) return;
-#ifdef HXM_CLOCK_WAIT
-    if (clock64() - t0 > (1ll << 34)) __trap();
-#else
     // every failed try_wait suspends the thread for up to a hardware time
     // limit first, so 2^28 of them are many seconds
     if (++n == (1u << 28)) __trap();
-#endif
   }
 }
 __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
