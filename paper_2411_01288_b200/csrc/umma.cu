@@ -486,14 +486,16 @@ struct Cfg {
   static constexpr int kStage = kABytes + kBBytes;
   static constexpr int kEW = EW;
   static constexpr int kGroups = kEW / 4;  // column groups of 4 warps (one per lane group)
-  // MODE 1 / 2 staging per column group: kOutBufs output boxes (MODE 1: two
-  // 8 KB boxes F', F; MODE 2: one 8 KB g_y1 box) + a kYRing-deep F'(y1) ring
-  // (MODE 2); 16 epilogue warps trade depth for the extra groups.
+  // MODE 1 / 2 staging per column group: MODE 1: kOutBufs output boxes (two
+  // 8 KB boxes F', F each); MODE 2: a kYRing-deep ring of 8 KB F'(y1) boxes,
+  // each overwritten in place by its chunk's g_y1 (a thread reads its own
+  // row of F' before writing that row of g_y1) and TMA-stored from there;
+  // 16 epilogue warps trade depth for the extra groups.
   static constexpr int kOutBufs = kEW == 16 ? 1 : 2;
   static constexpr int kYRing = kEW == 16 ? 2 : 3;
   static constexpr int kOutBox = MODE == 1 ? 16384 : 8192;
   static constexpr int kGroupBytes =
-      MODE == 1 ? kOutBufs * kOutBox : MODE == 2 ? kOutBufs * kOutBox + kYRing * 8192 : 4 * 2048;
+      MODE == 1 ? kOutBufs * kOutBox : MODE == 2 ? kYRing * 8192 : 4 * 2048;
   // 227 KB opt-in smem = stages + epilogue staging + 1 KB alignment slack +
   // barriers.  Staging: 2 KB per epilogue warp (MODE 0 / 3).
   static constexpr int kStaging = kGroups * kGroupBytes;
@@ -871,9 +873,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
         // every 32-row warp slice is entirely valid or entirely past the end.
         const int qbase = t.begin + static_cast<int>(rank) * BM;  // row 0 of the box
         const int rows_here = t.end - qbase;
-        auto ybox = [&](int gchunk) {
-          return hstage + C::kOutBufs * C::kOutBox + (gchunk % kYRing) * 8192;
-        };
+        auto ybox = [&](int gchunk) { return hstage + (gchunk % kYRing) * 8192; };
         auto ybar = [&](int gchunk) { return &dbar[half * kYRing + gchunk % kYRing]; };
         // F'(y1) boxes stream kYRing - 1 chunks ahead of the math, across the
         // item boundary (the next item's first boxes load during this item's
@@ -970,7 +970,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
             const bool pad = orow < 0;
             const int hrow = lg * 32 + lane;  // this thread's row in the 128-row box
             const int swz = (hrow >> 1) & 3;  // TMA 64B swizzle: chunk ^= (row >> 1) & 3
-            uint8_t* obox = hstage + (dchunk % C::kOutBufs) * C::kOutBox;
+            uint8_t* obox = bwd ? ybox(dchunk) : hstage + (dchunk % C::kOutBufs) * C::kOutBox;
             // MODE 1: the chunk's math (bias + F, F' packed to bf16) before
             // the box barrier, overlapping the previous store's smem read
             uint32_t o1[16], o2[16];
@@ -990,8 +990,10 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
             }
             // (1) the store that last used this box has read its smem, and
             //     every thread is past the previous chunk's F'(y1) reads
+            //     (MODE 2: the previous chunk's box is the slot the next F'
+            //     load refills, so its store must have read it)
             if (elect) {
-              if constexpr (C::kOutBufs == 2)
+              if constexpr (C::kOutBufs == 2 && !bwd)
                 asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
               else
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
