@@ -11,9 +11,10 @@ g_y = ones as in tools/commands.cpp:220-221).
 value   : whole-job tokens/s with inputs resident in HBM, each step timed with
           CUDA events on the launch stream, L2 flushed (256 MiB write) between
           steps outside the timed events, max over ranks.
-e2e     : the same metric through the public API (paper_2411_01288_b200.LayerRunner)
-          with x, g_y and the routing in pinned HOST memory: H2D copies, fwd+bwd
-          and the D2H read of y are inside the timed region every step.
+e2e     : the same metric through the public API (paper_2411_01288_b200.HostPipeline /
+          LayerRunner) with x, g_y and the routing in pinned HOST memory: H2D
+          copies, fwd+bwd and the D2H reads of y and g_x are inside the timed
+          region every step (e2e_full_grads: plus gW1, gb1, gW2, gb2 D2H).
 roofline: the dominant kernel's algorithmic FLOP (or bytes) per launch over its
           live CUDA-event duration inside the timed region, against
           MEASURED_PEAKS.json.
@@ -156,29 +157,67 @@ def barrier(ws):
     torch.cuda.synchronize()
 
 
-def cpu_baseline(cfg, max_seconds=25.0):
-    """Reference CPU path (oracle/_ref) on a bounded token sample, all host threads."""
+def cpu_model():
+    """lscpu's model name of this host."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def _ref_rate(O, cfg, n, threads):
+    E, k, D, H = cfg["E"], cfg["k"], cfg["D"], cfg["H"]
+    return n / O.ref_time_layer(E, k, D, H, D, n, 8, threads, 1)
+
+
+def ref_sample_tokens(O, cfg, threads, seconds):
+    """Tokens per reference step: >= REF_MIN_PER_THREAD tokens per thread (so
+    the per-call fixed costs -- transpose_experts of the whole weight set,
+    moe_layer.cpp:91-92 -- are amortised as in one full-batch call), grown to
+    about `seconds` of work, never above N.  Independent of --steps."""
+    probe = min(cfg["N"], threads * 64)
+    rate = _ref_rate(O, cfg, probe, threads)
+    n = max(threads * REF_MIN_PER_THREAD, int(rate * seconds))
+    n = min(cfg["N"], n, max(probe, int(rate * seconds * 4)))  # large dims: bounded
+    return max(threads, n // threads * threads)
+
+
+REF_MIN_PER_THREAD = 512
+
+
+def cpu_baseline(cfg, max_seconds=20.0):
+    """Reference CPU path (oracle/_ref) on a bounded token sample: all host
+    threads on disjoint token shards, plus a 1-core figure (the reference is
+    single-threaded)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
     if not O.ref_available():
         return None
     threads = max(1, min(os.cpu_count() or 1, 64))
+    n = ref_sample_tokens(O, cfg, threads, max_seconds)
     E, k, D, H = cfg["E"], cfg["k"], cfg["D"], cfg["H"]
-    # probe the rate, then size the sample to ~max_seconds (never above N)
-    probe = max(threads * 8, 16)
-    t = O.ref_time_layer(E, k, D, H, D, probe, 8, threads, 1)
-    rate = probe / max(t, 1e-6)
-    n = int(min(cfg["N"], max(probe, rate * max_seconds * 0.8)))
-    n = max(threads, n // threads * threads)
     t = O.ref_time_layer(E, k, D, H, D, n, 8, threads, 1)
+    # one core: a single moe_forward + moe_backward call of ~10 s of work
+    n1 = max(64, min(cfg["N"], int(n / t / threads * 10.0)))
+    t1 = O.ref_time_layer(E, k, D, H, D, n1, 8, 1, 1)
     return {"value": n / t, "unit": "tokens/s", "cores": threads, "kind": "reference",
             "sample": f"{n} of {cfg['N']} tokens, fwd+bwd via moekit::moe_forward/"
-                      f"moe_backward, {threads} threads on disjoint token shards",
-            "seconds": t}
+                      f"moe_backward, {threads} threads on disjoint token shards "
+                      f"({n // threads} tokens each)",
+            "seconds": t, "cpu_model": cpu_model(),
+            "single_core": {"value": n1 / t1, "unit": "tokens/s", "cores": 1,
+                            "sample": f"{n1} tokens, one call", "seconds": t1}}
 
 
 def run_reference(args, cfg, rank, ws):
-    """--impl reference: the reference's CPU implementation of the same path."""
+    """--impl reference: the reference's CPU implementation of the same path
+    (oracle/_ref = the unmodified moekit sources), all host threads on
+    disjoint token shards; each step a fixed sample (>= 512 tokens per thread,
+    about 8 s of work, independent of --steps)."""
     if rank != 0:
         return
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -188,18 +227,17 @@ def run_reference(args, cfg, rank, ws):
         return
     threads = max(1, min(os.cpu_count() or 1, 64))
     E, k, D, H = cfg["E"], cfg["k"], cfg["D"], cfg["H"]
-    budget = 150.0 / max(1, args.steps + args.warmup)  # whole run within minutes
-    probe = max(threads * 8, 16)
-    tp = O.ref_time_layer(E, k, D, H, D, probe, 8, threads, 1)
-    rate = probe / max(tp, 1e-6)
-    n = int(min(cfg["N"], max(probe, rate * budget * 0.8)))
-    n = max(threads, n // threads * threads)
+    n = ref_sample_tokens(O, cfg, threads, 8.0)
+    # warm-up: caches / page faults only, on a small sample (a CPU path has
+    # no JIT or autotuning to warm)
+    nw = max(threads, min(n, threads * 32))
     for _ in range(args.warmup):
-        O.ref_time_layer(E, k, D, H, D, n, 8, threads, 1)
+        O.ref_time_layer(E, k, D, H, D, nw, 8, threads, 1)
     times = [O.ref_time_layer(E, k, D, H, D, n, 8, threads, 1) for _ in range(args.steps)]
     total = sum(times)
     val = n * args.steps / total
-    sample = f"{n} of {cfg['N']} tokens per step, {threads} threads"
+    sample = (f"{n} of {cfg['N']} tokens per step ({n // threads} per thread), {threads} "
+              f"threads on disjoint token shards; warm-up steps {nw} tokens")
     out = {
         "impl": "reference", "metric": "MoE layer fwd+bwd tokens/sec", "value": val,
         "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -208,7 +246,7 @@ def run_reference(args, cfg, rank, ws):
         "config": {"workload": args.config, "desc": cfg["desc"], "E": E, "k": k, "d": D,
                    "ffn": H, "tokens": cfg["N"]},
         "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": threads,
-                         "kind": "reference", "sample": sample},
+                         "kind": "reference", "sample": sample, "cpu_model": cpu_model()},
         "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -369,47 +407,73 @@ def run_ours(args, cfg, rank, ws, local):
     value = N * ws * args.steps / (total_ms / 1000.0)
 
     # ---- end-to-end through the public API with host buffers --------------
+    # every step: x, g_y and the routing copied in from pinned host memory,
+    # fwd+bwd, and the per-token outputs y AND g_x read back (what a layer
+    # inside a network hands its neighbours); a second variant also reads
+    # back the parameter gradients gW1, gb1, gW2, gb2 -- everything the
+    # reference's moe_backward returns in host memory (moe_layer.hpp:70-73)
     xh = x.cpu().pin_memory()
     gyh = gy.cpu().pin_memory()
     ah = a.cpu().pin_memory()
     yh = torch.empty(N, D, dtype=torch.float32).pin_memory()
+    gxh = torch.empty(N, D, dtype=torch.float32).pin_memory()
     e2e_steps = max(3, args.steps, 40)  # amortise the 3-stage pipeline fill / drain
 
-    if use_graph:
-        # public API HostPipeline: H2D of step i, compute of step i-1 and
-        # D2H of step i-2 overlap on three streams (double-buffered)
-        from paper_2411_01288_b200.runner import HostPipeline
-        pipe = HostPipeline(run.p, N, k, D, D, dev, dtype)
+    def run_e2e(full_grads):
+        if use_graph:
+            # public API HostPipeline: H2D of step i, compute of step i-1 and
+            # D2H of step i-2 overlap on three streams (double-buffered)
+            from paper_2411_01288_b200.moe_layer import MoeGrads
+            from paper_2411_01288_b200.runner import HostPipeline
+            pipe = HostPipeline(run.p, N, k, D, D, dev, dtype)
+            gh = None
+            if full_grads:
+                g0 = run.grads
+                gh = MoeGrads(*(None if t is None else torch.empty_like(t, device="cpu")
+                                .pin_memory() for t in (g0.gw1, g0.gb1, g0.gw2, g0.gb2, g0.gx)))
 
-        def e2e_step():
-            pipe.push(xh, ah, gyh, yh)
-    else:
-        def e2e_step():
-            # the step's static inputs are x / a / gy: refill them from the host
-            x.copy_(xh, non_blocking=True)
-            a.copy_(ah, non_blocking=True)
-            gy.copy_(gyh, non_blocking=True)
-            step_fn()
-            yh.copy_(mc_out["y"] if mode == "model_centric" else y_out, non_blocking=True)
+            def e2e_step():
+                pipe.push(xh, ah, gyh, yh, gxh, gh)
+            drain = pipe.drain
+        else:
+            gsrc = None if mode == "model_centric" else run.grads
 
-    for _ in range(2):
-        e2e_step()
-    if use_graph:
-        pipe.drain()
-    barrier(ws)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(e2e_steps):
-        e2e_step()
-    if use_graph:
-        pipe.drain()  # the last D2H lands before e1
-    e1.record(stream)
-    barrier(ws)
-    e2e_ms = max_over_ranks(e0.elapsed_time(e1), ws)
-    e2e_val = N * ws * e2e_steps / (e2e_ms / 1000.0)
+            def e2e_step():
+                # the step's static inputs are x / a / gy: refill them from the host
+                x.copy_(xh, non_blocking=True)
+                a.copy_(ah, non_blocking=True)
+                gy.copy_(gyh, non_blocking=True)
+                res = step_fn()
+                yh.copy_(mc_out["y"] if mode == "model_centric" else y_out, non_blocking=True)
+                gxs = res.grads.gx if mode == "model_centric" else gsrc.gx
+                gxh[:gxs.shape[0]].copy_(gxs, non_blocking=True)
+            drain = None
+        for _ in range(2):
+            e2e_step()
+        if drain:
+            drain()
+        barrier(ws)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            e2e_step()
+        if drain:
+            drain()  # the last D2H lands before e1
+        e1.record(stream)
+        barrier(ws)
+        ms = max_over_ranks(e0.elapsed_time(e1), ws)
+        return N * ws * e2e_steps / (ms / 1000.0)
+
+    e2e_val = run_e2e(False)
     h2d = xh.numel() * xh.element_size() + gyh.numel() * gyh.element_size() + \
         ah.numel() * ah.element_size()
-    d2h = yh.numel() * yh.element_size()
+    d2h = yh.numel() * yh.element_size() + gxh.numel() * gxh.element_size()
+    e2e_full = None
+    if use_graph:
+        e2e_full = run_e2e(True)
+        g0 = run.grads
+        d2h_full = d2h + sum(t.numel() * 4 for t in (g0.gw1, g0.gb1, g0.gw2, g0.gb2)
+                             if t is not None)
 
     if rank != 0:
         return
@@ -479,12 +543,37 @@ def run_ours(args, cfg, rank, ws, local):
         "roofline": roof, "kernels": kernels,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "steps": e2e_steps},
+                "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+                "copies": "H2D x, g_y, routing; D2H y and g_x (fp32), every step"},
+        "e2e_full_grads": None if e2e_full is None else {
+            "value": e2e_full, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h_full, "steps": e2e_steps,
+            "copies": "as e2e plus gW1, gb1, gW2, gb2 (fp32) D2H every step"},
         "gpu_launches": int(launches),
         "redundancy": _redundancy(args, r, D, Hd) if args.capacity_factor > 0 else None,
         "clocks": clocks.summary(),
     }
     print(json.dumps(out))
+
+
+def relaunch(args):
+    """--gpus N without a torchrun environment: re-exec this command as N
+    ranks (one process per GPU, NCCL over NVLink) -- or fail loudly when the
+    box has fewer GPUs, never silently measure one."""
+    import subprocess
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} requested but only {have} CUDA device(s) visible")
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.run(cmd).returncode)
 
 
 def main():
@@ -518,6 +607,16 @@ def main():
         rank = int(os.environ.get("RANK", "0"))
         run_reference(args, cfg, rank, int(os.environ.get("WORLD_SIZE", "1")))
         return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        relaunch(args)  # does not return
+    env_ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if env_ws != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_ws}: launch one rank per GPU "
+                 f"(python -m torch.distributed.run --nproc-per-node {args.gpus} bench.py ...)")
+    if args.gpus > 1:
+        # communicator init lines (rank counts) on stderr for the driver
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     rank, ws, local = dist_init(args)
     try:
         run_ours(args, cfg, rank, ws, local)

@@ -2,13 +2,21 @@
 with a capacity factor (reference core/src/gemm_oracle.cpp), as the GPU
 baseline the expert-specific path is measured against.
 
-Semantics (count_redundancy, gemm_oracle.cpp:251-285): all k*N (token,
-choice) slots compete for E per-expert buffers of
+Semantics follow count_redundancy (gemm_oracle.cpp:251-285, whose comment
+at :269 says "all k*N (token, choice) pairs compete for the same per-expert
+buffers"): the k*N slots compete for E per-expert buffers of
 C = ceil(capacity_factor * k * N / E) rows; the lowest slot ids are kept
-(gemm_oracle.cpp:91-94's keep-lowest policy over the combined slot order
-choice-major, token-ascending), overflow slots are dropped (zero
-contribution to y and to every gradient), and shortfall rows are zero
-padding that the GEMMs really compute.
+(dispatch()'s keep-lowest policy, gemm_oracle.cpp:88-95, applied to the
+combined slot order choice-major, token-ascending), overflow slots are
+dropped (zero contribution to y and to every gradient), and shortfall rows
+are zero padding that the GEMMs really compute.
+
+Deliberate divergence: the reference's oracle_forward calls dispatch() once
+per choice (gemm_oracle.cpp:154-156), so there each choice has its own
+capacity-C buffer and for k > 1 fewer slots are dropped.  The device baseline
+follows count_redundancy's combined competition -- the accounting the bench
+columns (padded_rows, dropped_tokens, macs_oracle) report -- so its drops and
+its MAC count agree with those columns; for k = 1 the two coincide.
 
 On the device the baseline is the same layer with a fixed-capacity index
 (hxm_layer_desc.capacity): the dispatch is the expert-sorted gather, the

@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(NT) bwd_prologue(BwdPrologue b) {
   const int64_t gtid = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x;
   const int64_t gthreads = static_cast<int64_t>(gridDim.x) * NT;
   zero_f32(b.gx, b.gx_elems, gtid, gthreads);
-  // split experts: 16 block-sized parts of each first chunk's slices
+  // split experts: kParts (64) block-sized parts of each first chunk's slices
   constexpr int kParts = 64;
   const int nk = *b.n_ktiles;
   for (int it = blockIdx.x; it < nk * kParts; it += gridDim.x) {
@@ -398,14 +398,24 @@ __global__ void __launch_bounds__(NT) bwd_prologue(BwdPrologue b) {
         for (int64_t c = threadIdx.x; c < a.d; c += NT) a.out[static_cast<int64_t>(e) * a.d + c] = 0.f;
   // after an item: the block that brings an expert's item count to its total
   // combines that expert's partial rows (fixed order: deterministic) -- no
-  // grid-wide barrier; the counter is left at zero for the next call
+  // grid-wide barrier; the counter is left at zero for the next call.
+  // Arrival-counter protocol (a classic threadfence reduction):
+  //   release (every arriving block): bar.sync -- all of this block's
+  //     partial-row stores precede thread 0's next step in block order;
+  //     thread 0 __threadfence() (fence.sc.gpu, cumulative over those
+  //     stores); then the counter atomicAdd.
+  //   acquire (the last arriver): its atomicAdd observes every other
+  //     block's increment, hence (fence cumulativity) their partial rows;
+  //     thread 0 __threadfence(); bar.sync publishes `last` to the block;
+  //     combine_block then reads the partials with ld.global.cg (L2, never
+  //     a stale L1 line).
   __shared__ int last;
   auto arrive = [&](int ti) {
     if (!a.out) return;
     const int e = a.tiles[ti].expert;
-    __syncthreads();  // every thread's partial stores of this item are issued
+    __syncthreads();  // release, step 1: the block's partial stores are issued
     if (threadIdx.x == 0) {
-      __threadfence();
+      __threadfence();  // release, step 2 (cumulative over the block's stores)
       const int total = (a.tile_off[e + 1] - a.tile_off[e]) * slabs;
       last = atomicAdd(&b.done[e], 1) == total - 1;
       if (last) {

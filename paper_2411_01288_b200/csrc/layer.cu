@@ -185,6 +185,23 @@ hxm_status check_peer(const hxm_peer_rows* pr, const hxm_layer_desc* d, const La
     return invalid_arg(std::string(what) + ": the fused reduce-scatter needs the bf16 tcgen05 path");
   return HXM_OK;
 }
+// data-centric gW shard tables: H split evenly over 1..8 ranks in spans of a
+// multiple of 4 columns, every rank's shard mapped -- checked before the
+// first launch so a bad table leaves no partial results behind
+hxm_status check_shards(const hxm_peer_rows* pr, const hxm_layer_desc* d, const LayerWs& w,
+                        const char* what) {
+  if (!pr) return HXM_OK;
+  const int64_t span = pr->rows_per_rank;
+  if (pr->n_ranks < 1 || pr->n_ranks > HXM_MAX_PEERS || span < 1 ||
+      span * pr->n_ranks != d->hidden || span % 4 != 0)
+    return invalid_arg(std::string(what) +
+                       ": peer shards must split H evenly over 1..8 ranks (span % 4 == 0)");
+  for (int r = 0; r < pr->n_ranks; ++r)
+    if (!pr->ptrs[r]) return invalid_arg(std::string(what) + ": null peer shard");
+  if (w.rows_a < kUmmaRows)
+    return invalid_arg(std::string(what) + ": the fused reduce-scatter needs the bf16 tcgen05 path");
+  return HXM_OK;
+}
 }  // namespace
 
 // y (or, with `yp`, the owners' peer rows) = the layer forward
@@ -309,8 +326,8 @@ hxm_status layer_backward(const hxm_layer_desc* d, const void* x, const void* w1
   LayerWs w = carve(ar, *d);
   if (ar.overflow) return invalid_arg("moe_backward: workspace too small");
   HXM_RETURN_IF(check_peer(gxp, d, w, "moe_backward_tp"));
-  if ((gw1p || gw2p) && w.rows_a < kUmmaRows)
-    return invalid_arg("moe_backward_dc: the fused reduce-scatter needs the bf16 tcgen05 path");
+  HXM_RETURN_IF(check_shards(gw1p, d, w, "moe_backward_dc gW1"));
+  HXM_RETURN_IF(check_shards(gw2p, d, w, "moe_backward_dc gW2"));
   const hxm_dtype dt = static_cast<hxm_dtype>(d->dtype);
   const int64_t N = d->n_tokens, E = d->n_experts;
   const int64_t Di = d->d_in, H = d->hidden, Do = d->d_out;

@@ -374,6 +374,14 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
                "f"(d)
                : "memory");
 }
+// Reductions into ANOTHER GPU's memory (fused reduce-scatter over NVLink):
+// several GPUs add into the same owner row, so the atomics must be morally
+// strong across devices -- system scope, not the default .gpu scope.
+__device__ __forceinline__ void red_add_v4_sys(float* p, float a, float b, float c, float d) {
+  asm volatile("red.relaxed.sys.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a),
+               "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
 
 // UMMA shared-memory descriptor (sm100): start>>4 [0,14), LBO>>4 [16,30),
 // SBO>>4 [32,46), version=1 [46,48), layout SWIZZLE_128B=2 [61,64).
@@ -1117,14 +1125,14 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
                 const float4 val =
                     *reinterpret_cast<const float4*>(stg + rr * 64 + ((cc ^ ((rr >> 1) & 3)) * 16));
                 if (orr < 0 || (kDbg && (p.dbg_noload & 2))) continue;
-                if (p.n_peer > 0) {
+                if (MODE == 0 && p.n_peer > 0) {
                   // fused reduce-scatter: the token's owner rank, over peer memory
                   const int owner = static_cast<int>(orr / p.peer_rows);
                   float* o = p.peer[owner] + (orr - owner * p.peer_rows) * N + n + 16 * h2 + cc * 4;
-                  // atomicity is provided where the memory lives (the owner's L2);
-                  // ordering against the owner's reads comes from the kernel
-                  // boundary + hxm_peer_barrier (release / acquire, .sys)
-                  red_add_v4(o, val.x, val.y, val.z, val.w);
+                  // system-scope atomics (several GPUs add into one owner row);
+                  // ordering against the owner's reads: the epilogue's closing
+                  // fence.sc.sys + hxm_peer_barrier (release / acquire, .sys)
+                  red_add_v4_sys(o, val.x, val.y, val.z, val.w);
                   continue;
                 }
                 float* o = p.out_f32 + static_cast<int64_t>(orr) * N + n + 16 * h2 + cc * 4;
@@ -1211,7 +1219,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
                   o = p.peer[owner] + (t.expert * static_cast<int64_t>(p.M) + m) * span +
                       (n - owner * span);
                 }
-                if (!empty_seg) red_add_v4(o, val.x, val.y, val.z, val.w);
+                if (!empty_seg) red_add_v4_sys(o, val.x, val.y, val.z, val.w);
                 continue;
               }
               float* o = obase + static_cast<int64_t>(m0 + rr) * p.N + n0 + c0 + 16 * h2 + cc * 4;
@@ -1228,6 +1236,12 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
   }
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();  // pair done with TMEM
+  if constexpr (MODE == 0 || MODE == 3) {
+    // peer reductions (ordered before this point by the barrier above) made
+    // visible system-wide before the kernel ends; hxm_peer_barrier's .sys
+    // release / acquire then orders them before the owners' reads
+    if (threadIdx.x == 0 && p.n_peer > 0) asm volatile("fence.sc.sys;" ::: "memory");
+  }
   if (warp == 1) {
     tc_fence_after();
     if constexpr (CG == 1)

@@ -100,7 +100,11 @@ class HostPipeline:
     y run concurrently on three streams, double-buffered (two LayerRunners
     sharing the parameters, each replaying its own CUDA graph).
 
-    push(x_h, a_h, gy_h, y_h): enqueue one step; y_h (pinned) receives y.
+    push(x_h, a_h, gy_h, y_h, gx_h=None, grads_h=None): enqueue one step;
+    y_h (pinned) receives y, gx_h (optional, pinned N x D_i fp32) g_x, and
+    grads_h (optional: a MoeGrads of pinned host tensors) the parameter
+    gradients -- what a caller of the reference's moe_backward receives in
+    host memory (moe_layer.hpp:70-73).
     drain(): wait for everything enqueued."""
 
     def __init__(self, p: MoeLayerParams, n_tokens: int, k: int, d_in: int, d_out: int,
@@ -130,7 +134,7 @@ class HostPipeline:
             self.ev_out[b].record(self.s_comp)
         self.captured = True
 
-    def push(self, x_h, a_h, gy_h, y_h):
+    def push(self, x_h, a_h, gy_h, y_h, gx_h=None, grads_h=None):
         if not self.captured:
             self._capture(a_h.to(self.a[0].device))
         b = self.i % 2
@@ -148,6 +152,14 @@ class HostPipeline:
         with torch.cuda.stream(self.s_out):
             self.s_out.wait_event(self.ev_comp[b])
             y_h.copy_(self.runners[b].y, non_blocking=True)
+            g = self.runners[b].grads
+            if gx_h is not None:
+                gx_h.copy_(g.gx, non_blocking=True)
+            if grads_h is not None:
+                for key in ("gw1", "gb1", "gw2", "gb2"):
+                    dst = getattr(grads_h, key)
+                    if dst is not None and getattr(g, key) is not None:
+                        dst.copy_(getattr(g, key), non_blocking=True)
             self.ev_out[b].record(self.s_out)
 
     def drain(self):
