@@ -201,6 +201,10 @@ def cpu_baseline(cfg, max_seconds=20.0):
     n = ref_sample_tokens(O, cfg, threads, max_seconds)
     E, k, D, H = cfg["E"], cfg["k"], cfg["D"], cfg["H"]
     t = O.ref_time_layer(E, k, D, H, D, n, 8, threads, 1)
+    if t < 0.5 * max_seconds and n < cfg["N"]:  # the probe underestimated the rate
+        n = min(cfg["N"], int(n * max_seconds * 0.8 / max(t, 1e-3)))
+        n = max(threads, n // threads * threads)
+        t = O.ref_time_layer(E, k, D, H, D, n, 8, threads, 1)
     # one core: a single moe_forward + moe_backward call of ~10 s of work
     n1 = max(64, min(cfg["N"], int(n / t / threads * 10.0)))
     t1 = O.ref_time_layer(E, k, D, H, D, n1, 8, 1, 1)

@@ -84,6 +84,19 @@ hxm_status hxm_build_reindex(const int32_t* assignment, int64_t n_tokens,
                              size_t workspace_bytes, int32_t* status_dev,
                              hxm_stream_t stream);
 
+/* build_reindex_all (routing.hpp:46, routing.cpp:72-80): one ReIndex per
+ * routing choice, all k built in the same three launches.  assignments:
+ * device int32 k x n (RoutingChoice::assignments); choice i's v at
+ * v + i * v_stride (v_stride >= hxm_reindex_bound), its idx at
+ * idx + i * (E + 1).  Same checks and status word as hxm_build_reindex. */
+size_t hxm_reindex_all_workspace_bytes(int64_t n_tokens, int64_t n_experts, int64_t k);
+hxm_status hxm_build_reindex_all(const int32_t* assignments, int64_t k,
+                                 int64_t n_tokens, int64_t n_experts,
+                                 int64_t blk, int64_t* v, int64_t v_stride,
+                                 int64_t* idx, void* workspace,
+                                 size_t workspace_bytes, int32_t* status_dev,
+                                 hxm_stream_t stream);
+
 /* ------------------------------------------------------------------------
  * Operators -- replace moekit::esmm / ess / estmm / esfk (es_ops.hpp:37-65).
  * v/idx are a ReIndex built by hxm_build_reindex (or copied from the
@@ -131,6 +144,27 @@ hxm_status hxm_esfk(hxm_dtype dtype, const void* x, const void* g,
                     int64_t n_padded_bound, float* grad_x, float* grad_b,
                     float* grad_w, void* workspace, size_t workspace_bytes,
                     hxm_stream_t stream);
+
+/* OpStats / per-operator work counters (es_ops.hpp:17-24), incremented the
+ * way the reference's tiles do (es_ops.cpp:53-56, 80, 97-101, 124-127):
+ * real slots count MACs (esmm, estmm: real * d1 * d2) or adds (ess:
+ * real * d1), -1 pad slots count padding_slots once per operator pass; esfk
+ * (x N x d1, g N x d2) is esmm + ess + estmm.  For a valid ReIndex real_slots
+ * = n_tokens and padding_slots = idx[E] - n_tokens.  Host-side: the counters
+ * depend only on the index, so no device work or sync is needed. */
+typedef struct hxm_op_stats {
+  uint64_t macs;
+  uint64_t adds;
+  uint64_t padding_slots;
+} hxm_op_stats;
+typedef enum hxm_op_kind {
+  HXM_OP_ESMM = 0,
+  HXM_OP_ESS = 1,
+  HXM_OP_ESTMM = 2,
+  HXM_OP_ESFK = 3
+} hxm_op_kind;
+void hxm_op_stats_add(hxm_op_kind op, int64_t real_slots, int64_t padding_slots,
+                      int64_t d1, int64_t d2, hxm_op_stats* stats);
 
 /* ------------------------------------------------------------------------
  * MoE layer -- replaces moekit::moe_forward / moe_backward
@@ -197,6 +231,11 @@ hxm_status hxm_moe_stash_export(const hxm_layer_desc* desc,
  * conventional baseline = E*capacity*(D_i*H + H*D_o), padding included
  * (count_redundancy's token_macs_oracle, gemm_oracle.cpp:281-282). */
 uint64_t hxm_layer_forward_macs(const hxm_layer_desc* desc);
+
+/* Which kernels the layer runs for this descriptor: 2 = bf16 tcgen05 GEMMs
+ * on CTA pairs (cta_group::2, 256-row tiles), 1 = bf16 tcgen05 on single
+ * CTAs, 0 = the fp32 SIMT path, -1 = invalid descriptor. */
+int hxm_layer_path(const hxm_layer_desc* desc);
 
 /* ------------------------------------------------------------------------
  * Input generators (the reference's own seeded streams, random.hpp:13-54,

@@ -5,7 +5,7 @@ moe_layer, /root/reference/proj/core/include/moekit/) with every kernel a
 hand-written sm_100a CUDA kernel behind the C ABI in include/hexamoe.h.
 """
 from ._lib import CacheError, HexaMoeCudaError, ShapeError, lib  # noqa: F401
-from .es_ops import ACCUMULATE, WRITE, EsfkResult, esfk, esmm, ess, estmm  # noqa: F401
+from .es_ops import ACCUMULATE, WRITE, EsfkResult, OpStats, esfk, esmm, ess, estmm  # noqa: F401
 from .moe_layer import (ForwardStash, MoeForwardResult, MoeGrads, MoeLayerParams,  # noqa: F401
                         estimate_activation_memory, layer_workspace, make_desc,
                         make_random_params, moe_backward, moe_forward)

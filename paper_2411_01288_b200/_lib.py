@@ -66,6 +66,9 @@ SIGNATURES = {
     "hxm_reindex_bound": (_sz, [_i64, _i64, _i64]),
     "hxm_reindex_workspace_bytes": (_sz, [_i64, _i64]),
     "hxm_build_reindex": (C.c_int, [_p, _i64, _i64, _i64, _p, _p, _p, _sz, _p, _p]),
+    "hxm_reindex_all_workspace_bytes": (_sz, [_i64, _i64, _i64]),
+    "hxm_build_reindex_all": (C.c_int, [_p, _i64, _i64, _i64, _i64, _p, _i64, _p, _p, _sz, _p,
+                                        _p]),
     "hxm_op_workspace_bytes": (_sz, [_i64, _i64, _i64, _i64, _i64]),
     "hxm_esmm": (C.c_int, [C.c_int, _p, _i64, _i64, _p, _i64, _i64, C.c_int, _p, _p, _p, _i64,
                            C.c_int, _p, _p, _sz, _p]),
@@ -81,6 +84,8 @@ SIGNATURES = {
                                    _p, _p]),
     "hxm_moe_stash_export": (C.c_int, [C.POINTER(LayerDesc), _p, _i64, _p, _p, _p]),
     "hxm_layer_forward_macs": (C.c_uint64, [C.POINTER(LayerDesc)]),
+    "hxm_layer_path": (C.c_int, [C.POINTER(LayerDesc)]),
+    "hxm_op_stats_add": (None, [C.c_int, _i64, _i64, _i64, _i64, _p]),
     "hxm_synthesize_routing": (C.c_int, [_i64, _i64, _i64, C.c_char_p, C.c_uint64, _p]),
     "hxm_make_layer_inputs": (None, [C.c_uint64, _i64, _i64, _i64, _i64, _i64, C.c_double, _p,
                                      _p, _p, _p, _p]),

@@ -160,3 +160,31 @@ void hxm_make_layer_inputs(uint64_t seed, int64_t E, int64_t din, int64_t hid, i
 }
 
 }  // extern "C"
+
+// OpStats (es_ops.hpp:17-24) as the reference increments them: every tile
+// visits its blk slots, counting real tokens into macs / adds and -1 pads
+// into padding_slots (es_ops.cpp:53-56, 80, 97-101, 124-127); esfk runs the
+// three tile lists (es_ops.cpp:226-245).
+extern "C" void hxm_op_stats_add(hxm_op_kind op, int64_t real_slots, int64_t padding_slots,
+                                 int64_t d1, int64_t d2, hxm_op_stats* s) {
+  if (!s || real_slots < 0 || padding_slots < 0 || d1 < 0 || d2 < 0) return;
+  const uint64_t r = static_cast<uint64_t>(real_slots), pad = static_cast<uint64_t>(padding_slots);
+  const uint64_t a = static_cast<uint64_t>(d1), b = static_cast<uint64_t>(d2);
+  switch (op) {
+    case HXM_OP_ESMM:
+    case HXM_OP_ESTMM:
+      s->macs += r * a * b;
+      s->padding_slots += pad;
+      break;
+    case HXM_OP_ESS:  // d1 = row width
+      s->adds += r * a;
+      s->padding_slots += pad;
+      break;
+    case HXM_OP_ESFK:  // x: N x d1, g: N x d2 -> esmm(g, w_t) + ess(g) + estmm(x, g)
+      s->macs += 2 * r * a * b;
+      s->adds += r * b;
+      s->padding_slots += 3 * pad;
+      break;
+  }
+}
+

@@ -161,6 +161,13 @@ size_t hxm_layer_workspace_bytes(const hxm_layer_desc* d) {
   return ar.used;
 }
 
+int hxm_layer_path(const hxm_layer_desc* d) {
+  if (check_desc(d) != HXM_OK) return -1;
+  Arena ar(nullptr, 0);
+  const LayerWs w = carve(ar, *d);
+  return w.rows_a == kUmma2Rows ? 2 : (w.rows_a == kUmmaRows ? 1 : 0);
+}
+
 uint64_t hxm_layer_forward_macs(const hxm_layer_desc* d) {
   // rows the GEMMs compute per weight: every routed slot (expert-specific)
   // or E x capacity (conventional baseline, padding included)

@@ -28,10 +28,14 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
+// blockIdx.y = routing choice (build_reindex_all: k independent indices in
+// one launch; every per-choice array is offset by the choice's stride)
 __global__ void count_chunks(const int32_t* __restrict__ a, int64_t n, int E,
                              int chunk, int nchunks, int32_t* __restrict__ cnt,
                              int32_t* status) {
   extern __shared__ int32_t hist[];  // [kWarps][E]
+  a += static_cast<int64_t>(blockIdx.y) * n;
+  cnt += static_cast<int64_t>(blockIdx.y) * (static_cast<int64_t>(nchunks) * E + 1);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   int32_t* h = hist + warp * E;
   for (int e = lane; e < E; e += 32) h[e] = 0;
@@ -60,6 +64,10 @@ __global__ void scan_experts(const int32_t* __restrict__ cnt, int E, int nchunks
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int32_t carry;
   const int e = blockIdx.x;
+  const int64_t cstride = static_cast<int64_t>(nchunks) * E + 1;
+  cnt += blockIdx.y * cstride;
+  base += blockIdx.y * cstride;
+  total += static_cast<int64_t>(blockIdx.y) * (E + 1);
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   for (int c0 = 0; c0 < nchunks; c0 += kThreads) {
@@ -109,8 +117,16 @@ __global__ void scatter(const int32_t* __restrict__ a, int64_t n, int E,
                         int64_t blk, int chunk, int nchunks,
                         const int32_t* __restrict__ base,
                         const int32_t* __restrict__ total, VT* __restrict__ v,
-                        IdxT* __restrict__ idx_out) {
+                        IdxT* __restrict__ idx_out, int64_t v_stride) {
   extern __shared__ unsigned char smem_raw[];
+  {
+    const int64_t cstride = static_cast<int64_t>(nchunks) * E + 1;
+    a += static_cast<int64_t>(blockIdx.y) * n;
+    base += blockIdx.y * cstride;
+    total += static_cast<int64_t>(blockIdx.y) * (E + 1);
+    v += blockIdx.y * v_stride;
+    idx_out += static_cast<int64_t>(blockIdx.y) * (E + 1);
+  }
   IdxT* sidx = reinterpret_cast<IdxT*>(smem_raw);                     // E+1
   int64_t* cursor = reinterpret_cast<int64_t*>(
       smem_raw + align_up((E + 1) * sizeof(IdxT), 16));             // [kWarps][E]
@@ -158,26 +174,30 @@ int pick_chunk(int64_t n) {
   return static_cast<int>(c);
 }
 
+// k independent indices (k = 1: build_reindex; k > 1: build_reindex_all,
+// routing.cpp:72-80) in three launches, choice = blockIdx.y: v of choice i
+// at v + i * v_stride, idx at idx + i * (E + 1)
 template <class IdxT, class VT>
 hxm_status build_impl(const int32_t* a, int64_t n, int64_t E, int64_t blk,
                       VT* v, IdxT* idx, void* ws, size_t ws_bytes,
-                      int32_t* status, cudaStream_t st) {
+                      int32_t* status, cudaStream_t st, int k = 1, int64_t v_stride = 0) {
   const int chunk = pick_chunk(n);
   const int nchunks = static_cast<int>(ceil_div(n, chunk));
   Arena ar(ws, ws_bytes);
-  int32_t* cnt = ar.take<int32_t>(static_cast<size_t>(nchunks) * E + 1);
-  int32_t* base = ar.take<int32_t>(static_cast<size_t>(nchunks) * E + 1);
-  int32_t* total = ar.take<int32_t>(E + 1);
+  int32_t* cnt = ar.take<int32_t>((static_cast<size_t>(nchunks) * E + 1) * k);
+  int32_t* base = ar.take<int32_t>((static_cast<size_t>(nchunks) * E + 1) * k);
+  int32_t* total = ar.take<int32_t>((E + 1) * k);
   if (ar.overflow) return invalid_arg("build_reindex: workspace too small");
+  if (k > 65535) return invalid_arg("build_reindex_all: too many choices");
   const int blocks = static_cast<int>(std::max<int64_t>(1, ceil_div(nchunks, kWarps)));
   const size_t hist_smem = static_cast<size_t>(kWarps) * E * sizeof(int32_t);
   if (nchunks > 0) {
-    count_chunks<<<blocks, kThreads, hist_smem, st>>>(a, n, static_cast<int>(E), chunk,
-                                                      nchunks, cnt, status);
+    count_chunks<<<dim3(blocks, k), kThreads, hist_smem, st>>>(a, n, static_cast<int>(E), chunk,
+                                                               nchunks, cnt, status);
     HXM_CHECK_LAUNCH();
   }
-  scan_experts<<<static_cast<int>(E), kThreads, 0, st>>>(cnt, static_cast<int>(E),
-                                                         nchunks, base, total);
+  scan_experts<<<dim3(static_cast<int>(E), k), kThreads, 0, st>>>(cnt, static_cast<int>(E),
+                                                                  nchunks, base, total);
   HXM_CHECK_LAUNCH();
   const size_t sc_smem = align_up((E + 1) * sizeof(IdxT), 16) +
                          static_cast<size_t>(kWarps) * E * sizeof(int64_t);
@@ -186,9 +206,8 @@ hxm_status build_impl(const int32_t* a, int64_t n, int64_t E, int64_t blk,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(sc_smem)));
   }
-  scatter<IdxT, VT><<<blocks, kThreads, sc_smem, st>>>(a, n, static_cast<int>(E), blk,
-                                                        chunk, nchunks, base, total,
-                                                        v, idx);
+  scatter<IdxT, VT><<<dim3(blocks, k), kThreads, sc_smem, st>>>(
+      a, n, static_cast<int>(E), blk, chunk, nchunks, base, total, v, idx, v_stride);
   HXM_CHECK_LAUNCH();
   return HXM_OK;
 }
@@ -503,13 +522,13 @@ __global__ void __launch_bounds__(kThreads) fwd_prologue(FwdPrologue a) {
 
 }  // namespace
 
-size_t reindex_ws_bytes(int64_t n, int64_t E) {
+size_t reindex_ws_bytes(int64_t n, int64_t E, int64_t k) {
   const int chunk = pick_chunk(n);
   const int64_t nchunks = ceil_div(n, chunk);
   Arena ar(nullptr, 0);
-  ar.take<int32_t>(static_cast<size_t>(nchunks) * E + 1);
-  ar.take<int32_t>(static_cast<size_t>(nchunks) * E + 1);
-  ar.take<int32_t>(E + 1);
+  ar.take<int32_t>((static_cast<size_t>(nchunks) * E + 1) * k);
+  ar.take<int32_t>((static_cast<size_t>(nchunks) * E + 1) * k);
+  ar.take<int32_t>((E + 1) * k);
   return ar.used;
 }
 
@@ -584,7 +603,26 @@ size_t hxm_reindex_bound(int64_t n, int64_t E, int64_t blk) {
 }
 
 size_t hxm_reindex_workspace_bytes(int64_t n, int64_t E) {
-  return hxm::reindex_ws_bytes(n, E);
+  return hxm::reindex_ws_bytes(n, E, 1);
+}
+
+size_t hxm_reindex_all_workspace_bytes(int64_t n, int64_t E, int64_t k) {
+  return k < 1 ? 0 : hxm::reindex_ws_bytes(n, E, k);
+}
+
+hxm_status hxm_build_reindex_all(const int32_t* assignments, int64_t k, int64_t n, int64_t E,
+                                 int64_t blk, int64_t* v, int64_t v_stride, int64_t* idx,
+                                 void* ws, size_t ws_bytes, int32_t* status,
+                                 hxm_stream_t stream) {
+  // routing.cpp:72-80: one build_reindex per choice, same checks first
+  if (blk <= 0) return hxm::invalid_arg("build_reindex: blk must be >= 1");
+  if (n < 0 || E <= 0 || k < 1) return hxm::invalid_arg("build_reindex_all: need n >= 0, E >= 1, k >= 1");
+  if (n > 0x7fffffffLL) return hxm::invalid_arg("build_reindex: n exceeds int32 range");
+  if (v_stride < static_cast<int64_t>(hxm_reindex_bound(n, E, blk)))
+    return hxm::invalid_arg("build_reindex_all: v_stride below hxm_reindex_bound");
+  return hxm::build_impl<int64_t, int64_t>(assignments, n, E, blk, v, idx, ws, ws_bytes, status,
+                                           reinterpret_cast<cudaStream_t>(stream),
+                                           static_cast<int>(k), v_stride);
 }
 
 hxm_status hxm_build_reindex(const int32_t* a, int64_t n, int64_t E, int64_t blk,

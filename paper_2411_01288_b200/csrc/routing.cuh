@@ -4,7 +4,7 @@
 
 namespace hxm {
 
-size_t reindex_ws_bytes(int64_t n, int64_t E);
+size_t reindex_ws_bytes(int64_t n, int64_t E, int64_t k = 1);
 
 // Cut every expert segment [idx[e], idx[e+1]) into tiles of <= rows positions.
 template <class IdxT>

@@ -9,6 +9,7 @@ fp32 accumulation, fp32 inputs on fp32 FMA.  Outputs are fp32.
 """
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass
 
 import torch
@@ -18,6 +19,38 @@ from ._lib import HXM_ACCUMULATE, HXM_WRITE, ShapeError, check, lib
 from .routing import ReIndex, _require_cuda, _stream
 
 WRITE, ACCUMULATE = "write", "accumulate"  # moekit::EsOutputMode (es_ops.hpp:13)
+
+HXM_OP_ESMM, HXM_OP_ESS, HXM_OP_ESTMM, HXM_OP_ESFK = range(4)
+
+
+class _CStats(C.Structure):
+    _fields_ = [("macs", C.c_uint64), ("adds", C.c_uint64), ("padding_slots", C.c_uint64)]
+
+
+@dataclass
+class OpStats:
+    """moekit::OpStats (es_ops.hpp:17-24): token-granular work counters.
+    Padding slots contribute nothing, so ``macs`` counts real-token MACs only.
+    Pass one as ``stats=`` to an operator to accumulate its counts (the
+    counters follow the index, computed by hxm_op_stats_add)."""
+    macs: int = 0
+    adds: int = 0
+    padding_slots: int = 0
+
+    def total_ops(self) -> int:
+        return self.macs + self.adds
+
+    def reset(self) -> None:
+        self.macs = self.adds = self.padding_slots = 0
+
+
+def _count(stats, op: int, rx: ReIndex, d1: int, d2: int) -> None:
+    if stats is None:
+        return
+    c = _CStats(stats.macs, stats.adds, stats.padding_slots)
+    pad = rx.padded_len() - rx.n_tokens
+    lib().hxm_op_stats_add(op, rx.n_tokens, pad, d1, d2, C.byref(c))
+    stats.macs, stats.adds, stats.padding_slots = c.macs, c.adds, c.padding_slots
 
 
 def _dtype_code(t: torch.Tensor) -> int:
@@ -44,7 +77,7 @@ def _check_reindex(rx: ReIndex) -> None:
 
 
 def esmm(x: torch.Tensor, weights: torch.Tensor, bias, rx: ReIndex, mode=WRITE, dest=None,
-         w_transposed: bool = False) -> torch.Tensor:
+         w_transposed: bool = False, stats: OpStats | None = None) -> torch.Tensor:
     """y[t] = x[t] . W[e(t)] + b[e(t)]  (es_ops.hpp:39-46).
 
     mode "write" returns a new N x D2 fp32 tensor (or writes ``dest``);
@@ -82,10 +115,11 @@ def esmm(x: torch.Tensor, weights: torch.Tensor, bias, rx: ReIndex, mode=WRITE, 
                          rx.idx.data_ptr(), _bound(rx),
                          HXM_ACCUMULATE if mode == ACCUMULATE else HXM_WRITE,
                          dest.data_ptr(), ws.data_ptr(), ws.numel(), _stream()), "esmm")
+    _count(stats, HXM_OP_ESMM, rx, d1, d2)
     return dest
 
 
-def ess(x: torch.Tensor, rx: ReIndex) -> torch.Tensor:
+def ess(x: torch.Tensor, rx: ReIndex, stats: OpStats | None = None) -> torch.Tensor:
     """out[e] = sum of rows routed to e (es_ops.hpp:49)."""
     _check_reindex(rx)
     _require_cuda(x, "x")
@@ -98,10 +132,12 @@ def ess(x: torch.Tensor, rx: ReIndex) -> torch.Tensor:
     check(lib().hxm_ess(_dtype_code(x), x.data_ptr(), x.shape[0], d, rx.v.data_ptr(),
                         rx.idx.data_ptr(), E, _bound(rx), out.data_ptr(), ws.data_ptr(),
                         ws.numel(), _stream()), "ess")
+    _count(stats, HXM_OP_ESS, rx, d, 0)
     return out
 
 
-def estmm(x1: torch.Tensor, x2: torch.Tensor, rx: ReIndex) -> torch.Tensor:
+def estmm(x1: torch.Tensor, x2: torch.Tensor, rx: ReIndex,
+          stats: OpStats | None = None) -> torch.Tensor:
     """out[e] = sum_{t in e} outer(x1[t], x2[t]) (es_ops.hpp:52-53)."""
     _check_reindex(rx)
     _require_cuda(x1, "x1")
@@ -119,6 +155,7 @@ def estmm(x1: torch.Tensor, x2: torch.Tensor, rx: ReIndex) -> torch.Tensor:
     check(lib().hxm_estmm(_dtype_code(x1), x1.data_ptr(), x2.data_ptr(), x1.shape[0], d1, d2,
                           rx.v.data_ptr(), rx.idx.data_ptr(), E, _bound(rx), out.data_ptr(),
                           ws.data_ptr(), ws.numel(), _stream()), "estmm")
+    _count(stats, HXM_OP_ESTMM, rx, d1, d2)
     return out
 
 
@@ -130,7 +167,7 @@ class EsfkResult:
 
 
 def esfk(x: torch.Tensor, g: torch.Tensor, w_t: torch.Tensor, rx: ReIndex,
-         w_transposed: bool = False) -> EsfkResult:
+         w_transposed: bool = False, stats: OpStats | None = None) -> EsfkResult:
     """Fused backward of one MLP (es_ops.hpp:55-65).  ``w_t`` is E x D2 x D1
     as in the reference; with ``w_transposed`` pass the forward weights
     E x D1 x D2 instead (no transpose copy)."""
@@ -142,5 +179,21 @@ def esfk(x: torch.Tensor, g: torch.Tensor, w_t: torch.Tensor, rx: ReIndex,
     wd1 = w_t.shape[2] if w_transposed else w_t.shape[1]
     if w_t.shape[0] != rx.num_experts() or wd1 != g.shape[1]:
         raise ShapeError("esfk: w_t must be E x D2 x D1 for g of width D2")
-    return EsfkResult(esmm(g, w_t, None, rx, w_transposed=w_transposed), ess(g, rx),
-                      estmm(x, g, rx))
+    for t, nm in ((x, "x"), (g, "g"), (w_t, "w_t")):
+        _require_cuda(t, nm)
+    if x.dtype != g.dtype or w_t.dtype != g.dtype:
+        raise ValueError("esfk: x, g and w_t must share a dtype")
+    x, g, w_t = x.contiguous(), g.contiguous(), w_t.contiguous()
+    n, d1, d2, E = x.shape[0], x.shape[1], g.shape[1], rx.num_experts()
+    wd2 = w_t.shape[1] if w_transposed else w_t.shape[2]
+    if wd2 != d1:
+        raise ShapeError("esfk: w_t must be E x D2 x D1 for g of width D2")
+    f = dict(dtype=torch.float32, device=x.device)
+    res = EsfkResult(torch.empty(n, d1, **f), torch.empty(E, d2, **f), torch.empty(E, d1, d2, **f))
+    ws = _ws(rx, d1, d2)
+    check(lib().hxm_esfk(_dtype_code(x), x.data_ptr(), g.data_ptr(), n, d1, d2, w_t.data_ptr(),
+                         int(w_transposed), rx.v.data_ptr(), rx.idx.data_ptr(), E, _bound(rx),
+                         res.grad_x.data_ptr(), res.grad_b.data_ptr(), res.grad_w.data_ptr(),
+                         ws.data_ptr(), ws.numel(), _stream()), "esfk")
+    _count(stats, HXM_OP_ESFK, rx, d1, d2)
+    return res

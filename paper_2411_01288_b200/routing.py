@@ -167,6 +167,31 @@ def build_reindex(assignment, n_experts: int, blk: int, validate: bool = True) -
 
 
 def build_reindex_all(r: RoutingChoice, blk: int, validate: bool = True):
-    """One ReIndex per routing choice (routing.cpp:72-80)."""
+    """One ReIndex per routing choice (routing.cpp:72-80), all k built by one
+    hxm_build_reindex_all call (three launches, choice = grid y)."""
+    if blk <= 0:
+        raise ValueError("build_reindex: blk must be >= 1")
+    # (no r.validate(): the reference builds each choice's index as given)
     a = r.to_device() if not isinstance(r.assignments, torch.Tensor) else r.assignments
-    return [build_reindex(a[i], r.n_experts, blk, validate) for i in range(r.k)]
+    _require_cuda(a, "assignments")
+    a = a.to(torch.int32).contiguous()
+    k, n, E = r.k, r.n_tokens, r.n_experts
+    L = lib()
+    bound = max(L.hxm_reindex_bound(n, E, blk), 1)
+    dev = a.device
+    v = torch.empty(k, bound, dtype=torch.int64, device=dev)
+    idx = torch.empty(k, E + 1, dtype=torch.int64, device=dev)
+    wsb = L.hxm_reindex_all_workspace_bytes(n, E, k)
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    check(L.hxm_build_reindex_all(a.data_ptr(), k, n, E, blk, v.data_ptr(), bound,
+                                  idx.data_ptr(), ws.data_ptr(), wsb, status.data_ptr(),
+                                  _stream()), "build_reindex_all")
+    out = [ReIndex(v[i], idx[i], blk, n, bound) for i in range(k)]
+    if validate:
+        if int(status.item()) != 0:
+            raise ValueError("build_reindex: expert id out of range")
+        ends = idx[:, -1].tolist()
+        for i, rx in enumerate(out):
+            rx.v = v[i, :ends[i]]
+    return out

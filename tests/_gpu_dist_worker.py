@@ -3,8 +3,14 @@
 Runs the CUDA layer through the TP choreography of paper_2411_01288_b200.dist
 (data_centric_step, DataCentricRunner, model_centric_step) on the ranks it is
 given and checks every output against the single-GPU layer on the global
-batch (bf16, scaled error <= 2e-2, plus a tighter 1e-5 check of TP vs single
-GPU -- the same device kernels see the same bf16 operands)."""
+batch.  Bar: scaled error <= 1e-5 of TP vs the single GPU -- the same device
+kernels see the same bf16 operands and the stash columns are computed
+identically, so only the fp32 summation order of the H-partials (model-
+centric) or of the rank partials (data-centric gradient reductions) differs.
+The one exception is the multi-layer pipeline at P > 1: its inter-layer
+activations are re-rounded to bf16, where a 1e-7 fp32 difference can flip a
+rounding, so its layers keep the 2e-2 bf16 bar against the sequential
+stack."""
 import os
 import sys
 
@@ -123,7 +129,9 @@ def main():
         errs[f"pipe_gw2_{l}"] = scaled(pr.grads[l].gw2, g_seq[l].gw2)
         errs[f"pipe_gb1_{l}"] = scaled(pr.grads[l].gb1, g_seq[l].gb1)
         errs[f"pipe_gx_{l}"] = scaled(pr.grads[l].gx, g_seq[l].gx[lo:hi])
-    bad = {k_: v for k_, v in errs.items() if not v <= 2e-2}
+    def bar(key):
+        return 2e-2 if key.startswith("pipe_") and P > 1 else 1e-5
+    bad = {k_: v for k_, v in errs.items() if not v <= bar(k_)}
     print(f"rank {r}: worst {max(errs.values()):.2e}", "FAIL" if bad else "OK", bad or "")
     dist.destroy_process_group()
     sys.exit(1 if bad else 0)

@@ -1,0 +1,105 @@
+"""GPU parity at the BASELINE.json shapes: y, the stash and all five
+gradients of the CUDA layer against the fp64 oracle, at each config's real
+per-expert GEMM sizes (the reduction length of ESTMM is the expert's slot
+count, so token subsamples would not exercise it).
+
+The checker is oracle/fast.py (one BLAS GEMM per expert segment), pinned to
+the loop-order C oracle at 1e-12 by tests/test_oracle.py, fed the same
+bf16-rounded weights / activations / g_y the device sees.  Bar: scaled error
+max|a-b| / (1 + max|ref|) <= 2e-2 (BASELINE.json north_star, bf16;
+reference test_oracles.hpp:60-62).
+
+  c2  32 experts top-2, d 384, ffn 1536, N = 16384 (full size, 1 GPU)
+  c3  32 experts top-2, d 1024, ffn 4096, N = 16384 (the per-GPU batch of the
+      data-centric configuration, full size)
+  c4  64 experts top-2, d 1024, ffn 4096, N = 4096 (dims of the model-centric
+      configuration; 64 slots per expert on average)
+  c5  64 experts top-2, d 768, ffn 3072, N = 16384 with bench.py's skew90
+      routing: ~15 k slots on experts 0 and 1 (split-K ESTMM over 2048-slot
+      chunks) and ~25 on each of the other 62 (full size)
+"""
+import os
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+RTOL_BF16 = 2e-2
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def host(t):
+    return t.detach().to(torch.float64).cpu().numpy()
+
+
+def _routing(cfg, N, E, k, seed):
+    import paper_2411_01288_b200 as H
+    if cfg == "c5":
+        sys.path.insert(0, ROOT)
+        from bench import skew90_routing
+        return skew90_routing(N, E, k, seed)
+    return H.synthesize_routing(N, E, k, "uniform", seed)
+
+
+def _run(cfg, E, k, D, Hd, N, seed):
+    import fast as F
+
+    import paper_2411_01288_b200 as H
+    p, x = H.make_random_params(E, D, Hd, D, "gelu", seed=seed, n_tokens=N)
+    r = _routing(cfg, N, E, k, seed)
+    gy = torch.randn(N, D, generator=torch.Generator().manual_seed(seed + 7)).to(
+        "cuda", torch.bfloat16)
+    fw = H.moe_forward(x, p, r)
+    g = H.moe_backward(fw.stash, p, gy)
+    torch.cuda.synchronize()
+    got = {"y": host(fw.y)}
+    for key in ("gw1", "gb1", "gw2", "gb2", "gx"):
+        got[key] = host(getattr(g, key))
+    dact0, y20 = (host(t) for t in fw.stash.export(0))
+    a = r.assignments
+    xh, w1, b1, w2, b2 = (host(t) for t in (x, p.w1, p.b1, p.w2, p.b2))
+    del fw, g, x, p
+    torch.cuda.empty_cache()
+    y, y1, y2 = F.moe_forward(xh, w1, b1, w2, b2, a, "gelu")
+    errs = {"y": O.scaled_err(got["y"], y),
+            "dact_0": O.scaled_err(dact0, F.act_derivative("gelu", y1[0])),
+            "y2_0": O.scaled_err(y20, y2[0])}
+    go = F.moe_backward(xh, w1, w2, a, y1, y2, host(gy), "gelu")
+    for key in ("gw1", "gb1", "gw2", "gb2", "gx"):
+        errs[key] = O.scaled_err(got[key], go[key])
+    print(cfg, {k_: f"{v:.2e}" for k_, v in errs.items()})
+    bad = {k_: v for k_, v in errs.items() if not v <= RTOL_BF16}
+    assert not bad, bad
+    return a
+
+
+def test_c2_full_size_vs_oracle():
+    _run("c2", 32, 2, 384, 1536, 16384, 1)
+
+
+def test_c3_full_size_vs_oracle():
+    _run("c3", 32, 2, 1024, 4096, 16384, 2)
+
+
+def test_c4_dims_vs_oracle():
+    _run("c4", 64, 2, 1024, 4096, 4096, 4)
+
+
+def test_c5_skew_full_size_vs_oracle():
+    a = _run("c5", 64, 2, 768, 3072, 16384, 5)
+    counts = np.bincount(a.ravel(), minlength=64)
+    # the shape the test is meant to exercise: two hot experts above the
+    # 8192-slot single-chunk ESTMM limit, 62 near-empty ones
+    assert counts[0] > 8192 and counts[1] > 8192
+    assert counts[2:].max() < 200

@@ -190,7 +190,10 @@ def test_operators_vs_reference_fixtures(golden_dir, dtype, rtol):
         assert O.scaled_err(host(got_tm), want_tm) <= rtol, (i, "estmm")
         f = H.esfk(dev(x, dtype), dev(x2, dtype), dev(w, dtype), rx, w_transposed=True)
         want_gx = O.esmm(x2, np.ascontiguousarray(np.transpose(w, (0, 2, 1))), None, orx)
-        assert O.scaled_err(host(f.grad_x), want_gx) <= rtol, (i, "esfk")
+        assert O.scaled_err(host(f.grad_x), want_gx) <= rtol, (i, "esfk grad_x")
+        # es_ops.cpp:210-247: grad_b = ess(g), grad_w = estmm(x, g)
+        assert O.scaled_err(host(f.grad_b), O.ess(x2, orx)) <= rtol, (i, "esfk grad_b")
+        assert O.scaled_err(host(f.grad_w), O.estmm(x, x2, orx)) <= rtol, (i, "esfk grad_w")
 
 
 @pytest.mark.parametrize("E,n,d1,d2,blk", [
@@ -439,3 +442,56 @@ def test_cpp_dropin():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failures" in r.stdout
+
+
+@pytest.mark.parametrize("n,E,k,blk,dist", [
+    (16384, 32, 2, 8, "uniform"),    # c2 routing
+    (131072, 64, 2, 8, "uniform"),   # c4 routing
+    (777, 5, 3, 3, "zipf:1.2"),
+    (10, 4, 4, 1, "uniform"),        # k == E
+])
+def test_build_reindex_all_bitexact(n, E, k, blk, dist):
+    """build_reindex_all (routing.cpp:72-80): one index per choice, all k in
+    one batched call, each bit-exact with the reference order."""
+    H = hx()
+    a = O.synthesize_routing(n, E, k, dist, n + k)
+    out = H.build_reindex_all(H.RoutingChoice(n, E, k, a), blk)
+    assert len(out) == k
+    for i in range(k):
+        want = O.build_reindex(a[i], E, blk)
+        assert np.array_equal(out[i].idx.cpu().numpy(), want.idx), i
+        assert np.array_equal(out[i].v.cpu().numpy(), want.v), i
+    bad = a.copy()
+    bad[k - 1, n // 2] = E
+    with pytest.raises(ValueError):
+        H.build_reindex_all(H.RoutingChoice(n, E, k, bad), blk)
+
+
+def test_op_stats_counters():
+    """OpStats (es_ops.hpp:17-24): macs == N*D1*D2 for esmm / estmm, adds ==
+    N*D for ess, padding_slots == rx.padding() per operator pass; esfk counts
+    its three passes (test_es_ops.cpp:270-287)."""
+    H = hx()
+    rng = np.random.default_rng(3)
+    n, E, d1, d2 = 37, 3, 5, 4
+    a = rng.integers(0, E, size=n).astype(np.int32)
+    rx = H.build_reindex(a, E, 8)
+    pads = rx.padding()
+    x = dev(rng.standard_normal((n, d1)))
+    g = dev(rng.standard_normal((n, d2)))
+    w = dev(rng.standard_normal((E, d1, d2)))
+    s = H.OpStats()
+    H.esmm(x, w, None, rx, stats=s)
+    assert (s.macs, s.adds, s.padding_slots) == (n * d1 * d2, 0, pads)
+    s.reset()
+    H.ess(g, rx, stats=s)
+    assert (s.macs, s.adds, s.padding_slots) == (0, n * d2, pads)
+    s.reset()
+    H.estmm(x, g, rx, stats=s)
+    assert (s.macs, s.adds, s.padding_slots) == (n * d1 * d2, 0, pads)
+    s.reset()
+    f = H.esfk(x, g, w, rx, w_transposed=True, stats=s)
+    assert (s.macs, s.adds, s.padding_slots) == (2 * n * d1 * d2, n * d2, 3 * pads)
+    assert s.total_ops() == 2 * n * d1 * d2 + n * d2
+    orx = O.build_reindex(a, E, 8)
+    assert O.scaled_err(host(f.grad_w), O.estmm(host(x), host(g), orx)) <= RTOL_F32

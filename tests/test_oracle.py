@@ -147,3 +147,37 @@ def test_routing_validation_matches_reference():
     assert O.c_lib().orc_validate_routing(dup, 2, 10, 4) == 2
     with pytest.raises(ValueError):
         O.synthesize_routing(4, 2, 3)  # k > E (test_routing.cpp:103-106)
+
+
+# ------------------------------------------------ fast (BLAS) restatement --
+@pytest.mark.parametrize("E,k,din,hid,dout,n,act,dist,seed", [
+    (8, 1, 24, 40, 16, 300, "gelu", "uniform", 1),
+    (16, 2, 32, 48, 32, 500, "gelu", "zipf:1.3", 2),
+    (5, 3, 12, 20, 6, 77, "relu", "uniform", 3),
+    (32, 2, 16, 16, 16, 40, "identity", "uniform", 4),   # many empty experts
+    (4, 2, 8, 8, 8, 0, "gelu", "uniform", 5),            # no tokens
+])
+def test_fast_oracle_matches_c_oracle(E, k, din, hid, dout, n, act, dist, seed):
+    """oracle/fast.py (one BLAS GEMM per expert segment) is pinned to the
+    loop-order C oracle at 1e-12 scaled error before the GPU parity tests use
+    it at the BASELINE shapes."""
+    import fast as F
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((n, din))
+    w1 = 0.5 * rng.standard_normal((E, din, hid)); b1 = rng.standard_normal((E, hid))
+    w2 = 0.5 * rng.standard_normal((E, hid, dout)); b2 = rng.standard_normal((E, dout))
+    a = O.synthesize_routing(n, E, k, dist, seed) if n else np.zeros((k, 0), np.int32)
+    gy = rng.standard_normal((n, dout))
+    y, y1, y2 = O.moe_forward(x, w1, b1, w2, b2, a, 8, act)
+    g = O.moe_backward(x, w1, w2, a, y1, y2, gy, 8, act)
+    fy, fy1, fy2 = F.moe_forward(x, w1, b1, w2, b2, a, act)
+    fg = F.moe_backward(x, w1, w2, a, fy1, fy2, gy, act)
+    assert O.scaled_err(fy, y) <= 1e-12
+    assert O.scaled_err(fy1, y1) <= 1e-12 and O.scaled_err(fy2, y2) <= 1e-12
+    for key in ("gw1", "gb1", "gw2", "gb2", "gx"):
+        assert O.scaled_err(fg[key], g[key]) <= 1e-12, key
+    if n:
+        rx = O.build_reindex(a[0], E, 8)
+        assert O.scaled_err(F.esmm(x, w1, b1, a[0], E), O.esmm(x, w1, b1, rx)) <= 1e-12
+        assert O.scaled_err(F.ess(x, a[0], E), O.ess(x, rx)) <= 1e-12
+        assert O.scaled_err(F.estmm(x, gy, a[0], E), O.estmm(x, gy, rx)) <= 1e-12
