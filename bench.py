@@ -175,22 +175,25 @@ def _ref_rate(O, cfg, n, threads):
 
 
 def ref_sample_tokens(O, cfg, threads, seconds):
-    """Tokens per reference step: >= REF_MIN_PER_THREAD tokens per thread (so
-    the per-call fixed costs -- transpose_experts of the whole weight set,
+    """Tokens per reference step: at least REF_MIN_PER_THREAD tokens per thread
+    (so the per-call fixed costs -- transpose_experts of the whole weight set,
     moe_layer.cpp:91-92 -- are amortised as in one full-batch call), grown to
-    about `seconds` of work, never above N.  Independent of --steps."""
+    about `seconds` of work, never above N.  Independent of --steps, and the
+    same sample for the reference arm and the cpu_baseline leg."""
     probe = min(cfg["N"], threads * 64)
     rate = _ref_rate(O, cfg, probe, threads)
     n = max(threads * REF_MIN_PER_THREAD, int(rate * seconds))
-    n = min(cfg["N"], n, max(probe, int(rate * seconds * 4)))  # large dims: bounded
+    n = min(cfg["N"], n)
     return max(threads, n // threads * threads)
 
 
-REF_MIN_PER_THREAD = 512
+REF_MIN_PER_THREAD = 1024
+REF_SAMPLE_SECONDS = 20.0   # work per reference step (c2: the full 16384-token batch)
+REF_RUN_BUDGET_S = 150.0    # --impl reference: timed steps stop once this is spent
 
 
-def cpu_baseline(cfg, max_seconds=20.0):
-    """Reference CPU path (oracle/_ref) on a bounded token sample: all host
+def cpu_baseline(cfg):
+    """Reference CPU path (oracle/_ref) on the reference arm's sample: all host
     threads on disjoint token shards, plus a 1-core figure (the reference is
     single-threaded)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -198,13 +201,9 @@ def cpu_baseline(cfg, max_seconds=20.0):
     if not O.ref_available():
         return None
     threads = max(1, min(os.cpu_count() or 1, 64))
-    n = ref_sample_tokens(O, cfg, threads, max_seconds)
+    n = ref_sample_tokens(O, cfg, threads, REF_SAMPLE_SECONDS)
     E, k, D, H = cfg["E"], cfg["k"], cfg["D"], cfg["H"]
     t = O.ref_time_layer(E, k, D, H, D, n, 8, threads, 1)
-    if t < 0.5 * max_seconds and n < cfg["N"]:  # the probe underestimated the rate
-        n = min(cfg["N"], int(n * max_seconds * 0.8 / max(t, 1e-3)))
-        n = max(threads, n // threads * threads)
-        t = O.ref_time_layer(E, k, D, H, D, n, 8, threads, 1)
     # one core: a single moe_forward + moe_backward call of ~10 s of work
     n1 = max(64, min(cfg["N"], int(n / t / threads * 10.0)))
     t1 = O.ref_time_layer(E, k, D, H, D, n1, 8, 1, 1)
@@ -220,8 +219,11 @@ def cpu_baseline(cfg, max_seconds=20.0):
 def run_reference(args, cfg, rank, ws):
     """--impl reference: the reference's CPU implementation of the same path
     (oracle/_ref = the unmodified moekit sources), all host threads on
-    disjoint token shards; each step a fixed sample (>= 512 tokens per thread,
-    about 8 s of work, independent of --steps)."""
+    disjoint token shards.  Every timed step is the same sample as the
+    cpu_baseline leg (>= 1024 tokens per thread, c2: the full batch),
+    independent of --steps; the timed steps stop after REF_RUN_BUDGET_S so a
+    large --steps still ends within a few minutes (steps_timed says how many
+    ran).  Warm-up steps are small samples (page faults / caches only)."""
     if rank != 0:
         return
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -231,21 +233,23 @@ def run_reference(args, cfg, rank, ws):
         return
     threads = max(1, min(os.cpu_count() or 1, 64))
     E, k, D, H = cfg["E"], cfg["k"], cfg["D"], cfg["H"]
-    n = ref_sample_tokens(O, cfg, threads, 8.0)
-    # warm-up: caches / page faults only, on a small sample (a CPU path has
-    # no JIT or autotuning to warm)
+    n = ref_sample_tokens(O, cfg, threads, REF_SAMPLE_SECONDS)
     nw = max(threads, min(n, threads * 32))
     for _ in range(args.warmup):
         O.ref_time_layer(E, k, D, H, D, nw, 8, threads, 1)
-    times = [O.ref_time_layer(E, k, D, H, D, n, 8, threads, 1) for _ in range(args.steps)]
+    times = []
+    while len(times) < args.steps and (not times or sum(times) < REF_RUN_BUDGET_S):
+        times.append(O.ref_time_layer(E, k, D, H, D, n, 8, threads, 1))
     total = sum(times)
-    val = n * args.steps / total
+    val = n * len(times) / total
     sample = (f"{n} of {cfg['N']} tokens per step ({n // threads} per thread), {threads} "
-              f"threads on disjoint token shards; warm-up steps {nw} tokens")
+              f"threads on disjoint token shards; {len(times)} of {args.steps} steps timed "
+              f"(run budget {REF_RUN_BUDGET_S:.0f} s); warm-up steps {nw} tokens")
     out = {
         "impl": "reference", "metric": "MoE layer fwd+bwd tokens/sec", "value": val,
         "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "steps_timed": len(times),
+        "ms_per_step": 1000 * total / len(times), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "desc": cfg["desc"], "E": E, "k": k, "d": D,
                    "ffn": H, "tokens": cfg["N"]},

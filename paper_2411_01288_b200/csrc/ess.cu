@@ -138,7 +138,7 @@ __device__ __forceinline__ void ess_item_rows(const EssArgs& a, int ti) {
   for (int g = 0; g < GPL; ++g)
 #pragma unroll
     for (int i = 0; i < VEC; ++i) acc[g][i] = 0.f;
-  constexpr int U = 2;  // rows in flight per warp (x GPL groups per lane)
+  constexpr int U = 4;  // rows in flight per warp (x GPL groups per lane)
   for (int r0 = warp; r0 < nrows; r0 += W * U) {
     float v[U][GPL][VEC];
     int rr[U];
@@ -359,33 +359,6 @@ hxm_status gather_typed(const void* src, RowMap map, int64_t d, const IdxT* idx,
 // finishes its last ESS item.
 template <class T, int VEC>
 __global__ void __launch_bounds__(NT) bwd_prologue(BwdPrologue b) {
-  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x;
-  const int64_t gthreads = static_cast<int64_t>(gridDim.x) * NT;
-  zero_f32(b.gx, b.gx_elems, gtid, gthreads);
-  // split experts: kParts (64) block-sized parts of each first chunk's slices
-  constexpr int kParts = 64;
-  const int nk = *b.n_ktiles;
-  for (int it = blockIdx.x; it < nk * kParts; it += gridDim.x) {
-    const int ti = it / kParts, part = it % kParts;
-    const SegTile t = b.ktiles[ti];
-    if (!(t.flags & 1) || (ti > 0 && b.ktiles[ti - 1].expert == t.expert)) continue;
-    for (int o = 0; o < 2; ++o) {
-      float* out = o == 0 ? b.gw2 : b.gw1;
-      const int64_t slice = o == 0 ? b.gw2_slice : b.gw1_slice;
-      if (!out) continue;
-      out += static_cast<int64_t>(t.expert) * slice;
-      // float4 granules (slices are multiples of 4 when d1 or d2 is)
-      const int64_t per = ceil_div(ceil_div(slice, kParts), 4) * 4;
-      const int64_t lo = part * per, hi = min(slice, lo + per);
-      const bool v4 = slice % 4 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0;
-      if (v4) {
-        for (int64_t i = lo + 4 * threadIdx.x; i < hi; i += 4 * NT)
-          *reinterpret_cast<float4*>(out + i) = make_float4(0.f, 0.f, 0.f, 0.f);
-      } else {
-        for (int64_t i = lo + threadIdx.x; i < hi; i += NT) out[i] = 0.f;
-      }
-    }
-  }
   const EssArgs& a = b.es;
   const int col_groups = static_cast<int>((a.d + VEC - 1) / VEC);
   const bool rows = VEC > 1 && col_groups <= 32 * 2 && a.d % VEC == 0;
@@ -441,6 +414,41 @@ __global__ void __launch_bounds__(NT) bwd_prologue(BwdPrologue b) {
     for (int it = blockIdx.x; it < items; it += gridDim.x) {
       ess_item<T, VEC>(a, it / slabs, it % slabs);
       arrive(it / slabs);
+    }
+  }
+  // g_x = 0 and the split experts' gW slices = 0 after the (latency-bound)
+  // ESS items: on the blocks without an item when at least a quarter of the
+  // grid has none (their stores then overlap the items' loads), else on all
+  const int items = rows ? *a.n_tiles : *a.n_tiles * slabs;
+  const int zb0 = (items < static_cast<int>(gridDim.x) &&
+                   static_cast<int>(gridDim.x) - items >= static_cast<int>(gridDim.x) / 4)
+                      ? items : 0;
+  if (static_cast<int>(blockIdx.x) < zb0) return;
+  const int zblk = blockIdx.x - zb0, nzb = gridDim.x - zb0;
+  zero_f32(b.gx, b.gx_elems, static_cast<int64_t>(zblk) * NT + threadIdx.x,
+           static_cast<int64_t>(nzb) * NT);
+  // split experts: kParts (64) block-sized parts of each first chunk's slices
+  constexpr int kParts = 64;
+  const int nk = *b.n_ktiles;
+  for (int it = zblk; it < nk * kParts; it += nzb) {
+    const int ti = it / kParts, part = it % kParts;
+    const SegTile t = b.ktiles[ti];
+    if (!(t.flags & 1) || (ti > 0 && b.ktiles[ti - 1].expert == t.expert)) continue;
+    for (int o = 0; o < 2; ++o) {
+      float* out = o == 0 ? b.gw2 : b.gw1;
+      const int64_t slice = o == 0 ? b.gw2_slice : b.gw1_slice;
+      if (!out) continue;
+      out += static_cast<int64_t>(t.expert) * slice;
+      // float4 granules (slices are multiples of 4 when d1 or d2 is)
+      const int64_t per = ceil_div(ceil_div(slice, kParts), 4) * 4;
+      const int64_t lo = part * per, hi = min(slice, lo + per);
+      const bool v4 = slice % 4 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0;
+      if (v4) {
+        for (int64_t i = lo + 4 * threadIdx.x; i < hi; i += 4 * NT)
+          *reinterpret_cast<float4*>(out + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
+        for (int64_t i = lo + threadIdx.x; i < hi; i += NT) out[i] = 0.f;
+      }
     }
   }
 }

@@ -172,6 +172,22 @@ bool umma_supports_estmm(int64_t d1, int64_t d2);
 // CTA-pair ESMM (dense A, 256-row tiles): BN must split into whole B halves
 bool umma2_supports_esmm(int64_t d1, int64_t d2, bool w_trans);
 
+// esfk (es_ops.cpp:210-247): grad_x = esmm(g, W^T / w_t), grad_b = ess(g),
+// grad_w = estmm(x, g) over the caller's ReIndex.  simt: one launch (fp32);
+// umma (esfk.cu, bf16): a gather / ESS prologue + one tcgen05 launch that
+// runs the grad-x and grad-W tiles side by side.  w_trans as in EsmmArgs
+// for the grad-x GEMM (0: w is E x d2 x d1, 1: w is E x d1 x d2).
+hxm_status simt_esfk(hxm_dtype dt, const void* x, const void* g, int64_t n, int64_t d1,
+                     int64_t d2, const void* w, int w_trans, const int64_t* v, const int64_t* idx,
+                     int64_t E, int64_t np_bound, float* grad_x, float* grad_b, float* grad_w,
+                     cudaStream_t st);
+hxm_status umma_esfk(const void* x, const void* g, int64_t n, int64_t d1, int64_t d2,
+                     const void* w, int w_trans, const int64_t* v, const int64_t* idx,
+                     int64_t E, int64_t np_bound, float* grad_x, float* grad_b, float* grad_w,
+                     void* ws, size_t ws_bytes, cudaStream_t st);
+bool esfk_umma_ok(int64_t d1, int64_t d2);
+size_t esfk_ws_bytes(int64_t np_bound, int64_t E, int64_t d1, int64_t d2);
+
 // zero out[e] for experts whose ESTMM is split over several chunks
 hxm_status zero_split_experts(const SegTile* tiles, const int32_t* n_tiles,
                               int max_tiles, int64_t slice, float* out,

@@ -80,7 +80,9 @@ OpWs carve(Arena& ar, int64_t np_bound, int64_t E, int64_t d1, int64_t d2) {
   w.bound64 = np_bound + 63 * E;
   w.sorted = ar.take<char>(static_cast<size_t>(std::max<int64_t>(w.bound64, 1)) *
                            std::max(d1, d2) * 2);
-  w.sorted2 = ar.take<char>(static_cast<size_t>(std::max<int64_t>(w.bound64, 1)) * d2 * 2);
+  // (both widths: hxm_esfk runs the ESMM with d1 and d2 swapped on one workspace)
+  w.sorted2 = ar.take<char>(static_cast<size_t>(std::max<int64_t>(w.bound64, 1)) *
+                            std::max(d1, d2) * 2);
   w.idx64 = ar.take<int32_t>(E + 1);
   w.max_ktiles64 = static_cast<int>(max_tiles(w.bound64, E, kEstmmSplit));
   w.ktiles64 = ar.take<SegTile>(w.max_ktiles64);
@@ -101,7 +103,8 @@ size_t hxm_op_workspace_bytes(int64_t n, int64_t E, int64_t np_bound, int64_t d1
   (void)n;
   Arena ar(nullptr, 0);
   carve(ar, np_bound, E, d1, d2);
-  return ar.used;
+  // the same workspace also serves hxm_esfk's expert-sorted layout
+  return std::max(ar.used, esfk_ws_bytes(np_bound, E, d1, d2));
 }
 
 hxm_status hxm_esmm(hxm_dtype dt, const void* x, int64_t n, int64_t d1, const void* w,
@@ -245,15 +248,28 @@ hxm_status hxm_esfk(hxm_dtype dt, const void* x, const void* g, int64_t n, int64
                     const int64_t* idx, int64_t E, int64_t np_bound, float* grad_x,
                     float* grad_b, float* grad_w, void* ws, size_t ws_bytes,
                     hxm_stream_t stream) {
-  // es_ops.cpp:210-221; the three operators' work runs back to back on one
-  // stream (the combined work list of the reference is a scheduling device;
-  // the results are the same tensors).
-  // grad_x = esmm(g, w_t): g has d2 columns, output d1.  w_t is E x d2 x d1,
-  // i.e. the un-transposed weights E x d1 x d2 read as W^T (w_transposed=1).
-  HXM_RETURN_IF(hxm_esmm(dt, g, n, d2, w_t, E, d1, w_transposed, nullptr, v, idx, np_bound,
-                         HXM_WRITE, grad_x, ws, ws_bytes, stream));
-  HXM_RETURN_IF(hxm_ess(dt, g, n, d2, v, idx, E, np_bound, grad_b, ws, ws_bytes, stream));
-  return hxm_estmm(dt, x, g, n, d1, d2, v, idx, E, np_bound, grad_w, ws, ws_bytes, stream);
+  // es_ops.cpp:210-221 checks (structure / token counts are the host
+  // wrapper's; here: extents and buffers)
+  if (!valid_dtype(dt)) return invalid_arg("esfk: unknown dtype");
+  if (!v || !idx || E < 1) return shape_error("es-ops: malformed re-index vector");
+  if (n < 0 || d1 < 0 || d2 < 0) return shape_error("esfk: negative extent");
+  if (!grad_x || !grad_b || !grad_w || !w_t) return invalid_arg("esfk: null tensor");
+  if (n > 0x7fffffffLL || np_bound > 0x7fffffffLL) return invalid_arg("esfk: n too large");
+  if (n > 0 && (!x || !g)) return invalid_arg("esfk: null tensor");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (d1 == 0 || d2 == 0) return HXM_OK;
+  // the reference's combined work list (grad-x tiles, grad-b tiles, grad-W
+  // tiles) as one device work list: bf16 -> gather/ESS prologue + one
+  // tcgen05 launch running grad-x and grad-W side by side (esfk.cu); fp32 ->
+  // one SIMT launch (simt.cu)
+  if (dt == HXM_BF16 && esfk_umma_ok(d1, d2)) {
+    if (ws_bytes < esfk_ws_bytes(np_bound, E, d1, d2)) return invalid_arg("esfk: workspace too small");
+    return umma_esfk(x, g, n, d1, d2, w_t, w_transposed, v, idx, E, np_bound, grad_x, grad_b,
+                     grad_w, ws, ws_bytes, st);
+  }
+  ProfScope ps(st, "esfk_simt", 6.0 * n * d1 * d2, WORK_FLOP);
+  return simt_esfk(dt, x, g, n, d1, d2, w_t, w_transposed, v, idx, E, np_bound, grad_x, grad_b,
+                   grad_w, st);
 }
 
 }  // extern "C"

@@ -212,68 +212,6 @@ hxm_status build_impl(const int32_t* a, int64_t n, int64_t E, int64_t blk,
   return HXM_OK;
 }
 
-// ----------------------------------------------------------- tilers -----
-// tiles of at most `rows` positions per expert segment; min_one: experts
-// with an empty segment still get one (empty) tile -- used by ESTMM so that
-// their zero gradient is written (es_ops.cpp:202 zero-initialised output).
-// flags: bit 0 = the expert spans several tiles (split), bit 1 = empty
-// segment; with `counts` (real slots per expert) bit 2 is set and bits 8..
-// hold how many of the tile's rows are real (the rest are -1 pads).
-template <class IdxT, int NT = 1024>
-__device__ void tile_pass(const IdxT* __restrict__ idx, int E, int rows, int min_one,
-                          SegTile* __restrict__ tiles, int32_t* __restrict__ tile_off,
-                          int32_t* __restrict__ n_tiles, const int32_t* counts = nullptr,
-                          int split_rows = 0) {
-  using Scan = cub::BlockScan<int32_t, NT>;
-  __shared__ typename Scan::TempStorage tmp;
-  __shared__ int32_t carry;
-  __syncthreads();
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int e0 = 0; e0 < E; e0 += NT) {
-    const int e = e0 + threadIdx.x;
-    int32_t nt = 0;
-    int64_t b = 0, len = 0, re = rows;
-    if (e < E) {
-      b = idx[e];
-      len = static_cast<int64_t>(idx[e + 1]) - b;
-      if (split_rows > 0 && len > rows) re = split_rows;
-      nt = static_cast<int32_t>((len + re - 1) / re);
-      if (nt == 0 && min_one) nt = 1;
-    }
-    int32_t excl, agg;
-    Scan(tmp).ExclusiveSum(nt, excl, agg);
-    if (e < E) {
-      const int32_t off = carry + excl;
-      tile_off[e] = off;
-      const int split = nt > 1 ? 1 : 0;
-      const int empty = len == 0 ? 2 : 0;
-      for (int j = 0; j < nt; ++j) {
-        SegTile t;
-        t.expert = e;
-        t.begin = static_cast<int>(b + static_cast<int64_t>(j) * re);
-        const int64_t hi = b + static_cast<int64_t>(j + 1) * re;
-        t.end = static_cast<int>(hi < b + len ? hi : b + len);
-        if (len == 0) t.end = t.begin;
-        t.flags = split | empty;
-        if (counts) {
-          const int64_t real = b + counts[e] - t.begin;
-          const int vr = static_cast<int>(real < 0 ? 0 : (real > t.end - t.begin ? t.end - t.begin : real));
-          t.flags |= 4 | (vr << 8);
-        }
-        tiles[off + j] = t;
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) carry += agg;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    tile_off[E] = carry;
-    *n_tiles = carry;
-  }
-}
-
 template <class IdxT>
 __global__ void build_tiles(const IdxT* __restrict__ idx, int E, TileSpec a, TileSpec b,
                             TileSpec c, int count) {
@@ -520,6 +458,210 @@ __global__ void __launch_bounds__(kThreads) fwd_prologue(FwdPrologue a) {
   pro_ts(7);
 }
 
+
+// ---------------------------------------- one-barrier forward prologue --
+// Same outputs as fwd_prologue (bit-identical v / idx / tiles, y = 0, the
+// expert-sorted x copy) with ONE grid barrier instead of three:
+//   A  block b owns the contiguous slots [b*S, (b+1)*S) as S/32 groups of 32:
+//      per group, __match_any_sync gives every slot its rank among equal
+//      experts and the group's per-expert counts (smem, no atomics); the
+//      group counts are scanned in place, the block's counts published.
+//   -- grid.sync --
+//   B  every block sums the published counts itself (experts' totals and the
+//      counts of the blocks before it: G x E ints from L2), scans the padded
+//      totals into idx, places its own slots (position = idx[e] + earlier
+//      blocks + earlier groups + rank in group -- the reference's stable
+//      token-order placement, routing.cpp:64-68) and copies their x rows to
+//      the sorted positions; pads (-1 in v, zero rows in x_s) are spread over
+//      the blocks by expert; y is zeroed first so its stores overlap the
+//      index arithmetic.  The last three blocks write the three tile tables.
+constexpr int kFastMaxE = 256;
+constexpr int kFastMaxGroups = 32;
+__global__ void __launch_bounds__(kThreads) fwd_prologue_1b(FwdPrologue a) {
+  namespace cg = cooperative_groups;
+  pro_ts(0);
+  cg::grid_group grid = cg::this_grid();
+  const int E = a.E;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int groups = a.chunk / 32;  // S = a.chunk slots per block
+  const int64_t s0 = static_cast<int64_t>(blockIdx.x) * a.chunk;
+  __shared__ int32_t gh[kFastMaxGroups][kFastMaxE];  // per-group counts -> exclusive scan
+  __shared__ int32_t tot[kFastMaxE + 1];
+  __shared__ int32_t bef[kFastMaxE];
+  __shared__ int32_t sidx[kFastMaxE + 1];
+  __shared__ int32_t part[kThreads];
+  extern __shared__ int32_t dyn[];
+  int32_t* se = dyn;             // [S] expert of slot i (-1: invalid / past the end)
+  int32_t* sr = dyn + a.chunk;   // [S] rank of slot i among its group's equal experts
+  // ---- A: group histograms and ranks --------------------------------------
+  if (a.zero_i32 && blockIdx.x == 0)
+    for (int i = threadIdx.x; i < a.zero_n; i += kThreads) a.zero_i32[i] = 0;
+  for (int j = warp; j < groups; j += kWarps) {
+    for (int e = lane; e < E; e += 32) gh[j][e] = 0;
+    __syncwarp();
+    const int64_t s = s0 + 32 * j + lane;
+    int e = s < a.n_slots ? a.a[s] : -1;
+    if (s < a.n_slots && (e < 0 || e >= E)) {
+      if (a.status) atomicExch(a.status, HXM_ERR_INVALID_ARG);
+      e = -1;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    se[32 * j + lane] = e;
+    sr[32 * j + lane] = __popc(peers & ((1u << lane) - 1u));
+    if (e >= 0 && (__ffs(peers) - 1) == lane) gh[j][e] = __popc(peers);
+    // per-token distinctness of the k choices (routing.cpp:30-39): a slot
+    // checks the later choices of its token
+    if (a.status && a.k > 1 && e >= 0) {
+      const int ci = static_cast<int>(s / a.n_tok);
+      const int64_t t = s - ci * a.n_tok;
+      for (int c2 = ci + 1; c2 < a.k; ++c2)
+        if (a.a[c2 * a.n_tok + t] == e) atomicExch(a.status, HXM_ERR_INVALID_ARG);
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += kThreads) {
+    int32_t run = 0;
+    for (int j = 0; j < groups; ++j) {
+      const int32_t c = gh[j][e];
+      gh[j][e] = run;
+      run += c;
+    }
+    a.cnt[static_cast<int64_t>(blockIdx.x) * E + e] = run;
+  }
+  pro_ts(1);
+  grid.sync();
+  pro_ts(2);
+  // ---- B: y = 0 (stores overlap the index arithmetic) ---------------------
+  {
+    const int64_t gtid = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    zero_f32(a.y, a.y_elems, gtid, static_cast<int64_t>(gridDim.x) * kThreads);
+  }
+  // totals and the counts of the blocks before this one: thread (r, e) sums
+  // rows r, r + R, ... of the G x E count table (E <= kThreads), then the R
+  // row groups are added in a fixed order
+  {
+    const int R = kThreads / E;
+    const int r = threadIdx.x / E, e = threadIdx.x % E;
+    int32_t t_all = 0, t_bef = 0;
+    if (r < R) {
+      const int G = gridDim.x, me = blockIdx.x;
+#pragma unroll 4
+      for (int b = r; b < G; b += R) {
+        const int32_t c = __ldcg(a.cnt + static_cast<int64_t>(b) * E + e);
+        t_all += c;
+        t_bef += b < me ? c : 0;
+      }
+    }
+    part[threadIdx.x] = t_all;
+    __syncthreads();
+    if (threadIdx.x < E) {
+      int32_t s = 0;
+      for (int q = 0; q < R; ++q) s += part[q * E + threadIdx.x];
+      tot[threadIdx.x] = s;
+    }
+    __syncthreads();
+    part[threadIdx.x] = t_bef;
+    __syncthreads();
+    if (threadIdx.x < E) {
+      int32_t s = 0;
+      for (int q = 0; q < R; ++q) s += part[q * E + threadIdx.x];
+      bef[threadIdx.x] = s;
+    }
+    __syncthreads();
+  }
+  block_idx<int32_t>(tot, E, a.blk, sidx, a.capacity);
+  if (blockIdx.x == 0)
+    for (int e = threadIdx.x; e <= E; e += kThreads) a.idx[e] = sidx[e];
+  // placement of this block's slots (slot id = flat assignment position)
+  const int S = a.chunk;
+  for (int i = threadIdx.x; i < S; i += kThreads) {
+    const int e = se[i];
+    int32_t pos = -1;
+    if (e >= 0) {
+      const int32_t within = bef[e] + gh[i / 32][e] + sr[i];
+      if (a.capacity <= 0 || within < a.capacity) {
+        pos = sidx[e] + within;
+        a.v[pos] = static_cast<int32_t>(s0 + i);
+      }
+    }
+    sr[i] = pos;  // reused: the sorted position of slot i (-1: none)
+  }
+  // pads of the experts this block owns: -1 in v, zero rows in x_s
+  const char* X = static_cast<const char*>(a.x);
+  char* XS = static_cast<char*>(a.xs);
+  const int64_t rb = a.row_bytes;
+  for (int e = blockIdx.x; e < E; e += gridDim.x) {
+    const int64_t tt = tot[e];
+    const int64_t kept = (a.capacity > 0 && tt > a.capacity) ? a.capacity : tt;
+    const int64_t p0 = static_cast<int64_t>(sidx[e]) + kept, p1 = sidx[e + 1];
+    for (int64_t p = p0 + threadIdx.x; p < p1; p += kThreads) a.v[p] = -1;
+    if (a.x)
+      for (int64_t p = p0 + warp; p < p1; p += kWarps) zero_row(XS + p * rb, rb, lane, a.unit);
+  }
+  // the three tilings on the last three blocks
+  {
+    const int tb = static_cast<int>(gridDim.x) - 1 - static_cast<int>(blockIdx.x);
+    const bool one = gridDim.x < 3;
+    if (tb == 0)
+      tile_pass<int32_t, kThreads>(sidx, E, a.s0.rows, a.s0.min_one, a.s0.tiles, a.s0.tile_off,
+                                   a.s0.n_tiles, tot, a.s0.split_rows);
+    if (one ? tb == 0 : tb == 1)
+      tile_pass<int32_t, kThreads>(sidx, E, a.s1.rows, a.s1.min_one, a.s1.tiles, a.s1.tile_off,
+                                   a.s1.n_tiles, tot, a.s1.split_rows);
+    if (one ? tb == 0 : tb == 2)
+      tile_pass<int32_t, kThreads>(sidx, E, a.s2.rows, a.s2.min_one, a.s2.tiles, a.s2.tile_off,
+                                   a.s2.n_tiles, tot, a.s2.split_rows);
+  }
+  pro_ts(3);
+  if (!a.x) return;
+  __syncthreads();
+  // ---- B': x rows of this block's slots to their sorted positions ---------
+  // each warp a contiguous run of the block's slots, 8 rows in flight
+  const int per = (S + kWarps - 1) / kWarps;
+  const int i0 = warp * per, i1 = min(S, i0 + per);
+  if (a.unit == 16) {
+    const int upr = static_cast<int>(rb / 16);
+    for (int r0 = i0; r0 < i1; r0 += 8) {
+      const char* src[8];
+      int64_t dpos[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = r0 + u;
+        const int32_t pos = i < i1 ? sr[i] : -1;
+        dpos[u] = pos;
+        src[u] = pos < 0 ? nullptr : X + ((s0 + i) % a.n_tok) * rb;
+      }
+      for (int c0 = 0; c0 < upr; c0 += 64) {
+        uint4 buf[8][2];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+          for (int m = 0; m < 2; ++m) {
+            const int o = c0 + m * 32 + lane;
+            buf[u][m] = (src[u] && o < upr) ? __ldg(reinterpret_cast<const uint4*>(src[u]) + o)
+                                            : make_uint4(0u, 0u, 0u, 0u);
+          }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (dpos[u] < 0) continue;
+          uint4* dst = reinterpret_cast<uint4*>(XS + dpos[u] * rb);
+#pragma unroll
+          for (int m = 0; m < 2; ++m) {
+            const int o = c0 + m * 32 + lane;
+            if (o < upr) dst[o] = buf[u][m];
+          }
+        }
+      }
+    }
+  } else {
+    for (int i = i0; i < i1; ++i) {
+      const int32_t pos = sr[i];
+      if (pos >= 0) copy_row(X + ((s0 + i) % a.n_tok) * rb, XS + pos * rb, rb, lane, a.unit);
+    }
+  }
+  pro_ts(4);
+}
+
 }  // namespace
 
 size_t reindex_ws_bytes(int64_t n, int64_t E, int64_t k) {
@@ -548,6 +690,44 @@ template hxm_status launch_tiles<int64_t>(const int64_t*, int64_t, int, bool, Se
                                           int32_t*, int32_t*, cudaStream_t, int);
 
 hxm_status launch_fwd_prologue(FwdPrologue a, cudaStream_t st) {
+  static int occ_cache[64] = {0};
+  static size_t occ_smem[64] = {0};
+  static int occ1_cache[64] = {0};
+  static size_t occ1_smem[64] = {0};
+  int dev = 0;
+  HXM_TRY_CUDA(cudaGetDevice(&dev));
+  dev = dev < 64 ? dev : 63;
+  const char* ge = std::getenv("HXM_PRO_BLOCKS");
+  const int per_sm = ge ? std::max(1, std::atoi(ge)) : 2;
+  const char* g1 = std::getenv("HXM_PRO1");  // 0: the three-barrier prologue
+  // one-barrier prologue: S = 32 * groups slots per block, every block
+  // co-resident, the group counts in static smem
+  if (!(g1 && g1[0] == '0') && a.E <= kFastMaxE) {
+    const int64_t slots_max = static_cast<int64_t>(sm_count()) * per_sm;
+    const int groups = static_cast<int>(std::max<int64_t>(1, ceil_div(a.n_slots, 32 * slots_max)));
+    if (groups <= kFastMaxGroups) {
+      a.chunk = 32 * groups;
+      a.nchunks = static_cast<int>(std::max<int64_t>(1, ceil_div(a.n_slots, a.chunk)));
+      Arena ar(a.ws, a.ws_bytes);
+      a.cnt = ar.take<int32_t>(static_cast<size_t>(a.nchunks) * a.E + 1);
+      a.base = nullptr;
+      a.total = nullptr;
+      if (ar.overflow) return invalid_arg("layer prologue: workspace too small");
+      const size_t smem = 2 * static_cast<size_t>(a.chunk) * sizeof(int32_t);
+      if (occ1_smem[dev] != smem) {
+        HXM_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1_cache[dev],
+                                                                   fwd_prologue_1b, kThreads, smem));
+        occ1_smem[dev] = smem;
+      }
+      if (static_cast<int64_t>(occ1_cache[dev]) * sm_count() >= a.nchunks) {
+        void* args[] = {&a};
+        HXM_TRY_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fwd_prologue_1b),
+                                                 dim3(a.nchunks), dim3(kThreads), args, smem, st));
+        HXM_CHECK_LAUNCH();
+        return HXM_OK;
+      }
+    }
+  }
   a.chunk = pick_chunk(a.n_slots);
   a.nchunks = static_cast<int>(ceil_div(a.n_slots, a.chunk));
   Arena ar(a.ws, a.ws_bytes);
@@ -559,11 +739,6 @@ hxm_status launch_fwd_prologue(FwdPrologue a, cudaStream_t st) {
                                (align_up(a.E + 1, 4) + static_cast<size_t>(kWarps) * a.E) *
                                    sizeof(int32_t));
   // per-device cache of the kernel attribute / occupancy query
-  static int occ_cache[64] = {0};
-  static size_t occ_smem[64] = {0};
-  int dev = 0;
-  HXM_TRY_CUDA(cudaGetDevice(&dev));
-  dev = dev < 64 ? dev : 63;
   if (occ_smem[dev] != smem) {
     if (smem > 48 * 1024)
       HXM_TRY_CUDA(cudaFuncSetAttribute(fwd_prologue, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -574,8 +749,6 @@ hxm_status launch_fwd_prologue(FwdPrologue a, cudaStream_t st) {
   }
   const int occ = occ_cache[dev];
   if (occ < 1) return invalid_arg("layer prologue: cannot be resident");
-  const char* ge = std::getenv("HXM_PRO_BLOCKS");
-  const int per_sm = ge ? std::max(1, std::atoi(ge)) : 2;
   const int grid = sm_count() * std::min(occ, per_sm);
   void* args[] = {&a};
   HXM_TRY_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fwd_prologue), dim3(grid),

@@ -1,5 +1,7 @@
 // routing.cuh -- internal routing / tiling entry points (see routing.cu).
 #pragma once
+#include <cub/block/block_scan.cuh>
+
 #include "common.cuh"
 
 namespace hxm {
@@ -24,6 +26,69 @@ struct TileSpec {
                        // chunk per expert unless it is heavily skewed)
 };
 int64_t max_tiles(int64_t n_padded_bound, int64_t E, int rows);
+
+// ----------------------------------------------------------- tilers -----
+// tiles of at most `rows` positions per expert segment; min_one: experts
+// with an empty segment still get one (empty) tile -- used by ESTMM so that
+// their zero gradient is written (es_ops.cpp:202 zero-initialised output).
+// flags: bit 0 = the expert spans several tiles (split), bit 1 = empty
+// segment; with `counts` (real slots per expert) bit 2 is set and bits 8..
+// hold how many of the tile's rows are real (the rest are -1 pads).
+template <class IdxT, int NT = 1024>
+__device__ void tile_pass(const IdxT* __restrict__ idx, int E, int rows, int min_one,
+                          SegTile* __restrict__ tiles, int32_t* __restrict__ tile_off,
+                          int32_t* __restrict__ n_tiles, const int32_t* counts = nullptr,
+                          int split_rows = 0) {
+  using Scan = cub::BlockScan<int32_t, NT>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int32_t carry;
+  __syncthreads();
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int e0 = 0; e0 < E; e0 += NT) {
+    const int e = e0 + threadIdx.x;
+    int32_t nt = 0;
+    int64_t b = 0, len = 0, re = rows;
+    if (e < E) {
+      b = idx[e];
+      len = static_cast<int64_t>(idx[e + 1]) - b;
+      if (split_rows > 0 && len > rows) re = split_rows;
+      nt = static_cast<int32_t>((len + re - 1) / re);
+      if (nt == 0 && min_one) nt = 1;
+    }
+    int32_t excl, agg;
+    Scan(tmp).ExclusiveSum(nt, excl, agg);
+    if (e < E) {
+      const int32_t off = carry + excl;
+      tile_off[e] = off;
+      const int split = nt > 1 ? 1 : 0;
+      const int empty = len == 0 ? 2 : 0;
+      for (int j = 0; j < nt; ++j) {
+        SegTile t;
+        t.expert = e;
+        t.begin = static_cast<int>(b + static_cast<int64_t>(j) * re);
+        const int64_t hi = b + static_cast<int64_t>(j + 1) * re;
+        t.end = static_cast<int>(hi < b + len ? hi : b + len);
+        if (len == 0) t.end = t.begin;
+        t.flags = split | empty;
+        if (counts) {
+          const int64_t real = b + counts[e] - t.begin;
+          const int vr = static_cast<int>(real < 0 ? 0 : (real > t.end - t.begin ? t.end - t.begin : real));
+          t.flags |= 4 | (vr << 8);
+        }
+        tiles[off + j] = t;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += agg;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    tile_off[E] = carry;
+    *n_tiles = carry;
+  }
+}
+
 
 // The layer forward's prologue in one cooperative launch: k-choice slot index
 // (v, idx; bit-exact with build_reindex_slots), routing validation into

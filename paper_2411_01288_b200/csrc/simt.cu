@@ -13,6 +13,7 @@
 // along K (blockIdx.z) with fp32 atomic reductions, so the fp32 layer at
 // c1's sizes (a few hundred CTAs of long K loops) fills the 148 SMs.
 #include "kernels.cuh"
+#include "routing.cuh"
 
 namespace hxm {
 namespace {
@@ -101,14 +102,10 @@ __device__ __forceinline__ void mma_tile(const float (&As)[BK][BM], const float 
 // the partial sums add up in the destination; the bias goes with split 0).
 // Double-buffered smem: the next k-step's tiles load while this one computes.
 template <class T, bool VEC>
-__global__ void __launch_bounds__(NT) esmm_simt_kernel(EsmmArgs a) {
-  const int ti = blockIdx.y;
-  if (ti >= *a.n_tiles) return;
-  const SegTile tile = a.tiles[ti];
-  const int n0 = blockIdx.x * BN;
+__device__ __forceinline__ void esmm_simt_body(const EsmmArgs& a, const SegTile tile, const int n0,
+                                               const int64_t kb, const int64_t ke,
+                                               const bool lead) {
   const int64_t K = a.d1, N = a.d2;
-  const int64_t kper = ceil_div(ceil_div(K, BK), gridDim.z) * BK;
-  const int64_t kb = blockIdx.z * kper, ke = min(K, kb + kper);
   const T* A = static_cast<const T*>(a.a);
   const T* W = static_cast<const T*>(a.w) + static_cast<int64_t>(tile.expert) * K * N;
   __shared__ __align__(16) float As[2][BK][BM];
@@ -138,7 +135,6 @@ __global__ void __launch_bounds__(NT) esmm_simt_kernel(EsmmArgs a) {
     buf ^= 1;
   }
   // epilogue
-  const bool lead = blockIdx.z == 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int r = ty * 4 + i;
@@ -184,22 +180,28 @@ __global__ void __launch_bounds__(NT) esmm_simt_kernel(EsmmArgs a) {
   }
 }
 
-// ESTMM: 64 x 64 output tile per CTA, K = the chunk's token positions in
-// steps of 16; blockIdx.z splits the positions (the output is then pre-zeroed
-// and every split reduces with atomicAdd).
+// ESMM: 64-row segment tile x 64 columns per CTA (blockIdx.x = column block,
+// y = tile); blockIdx.z splits K for the fp32 reduction epilogue (EPI_ATOMIC:
+// the partial sums add up in the destination; the bias goes with split 0).
 template <class T, bool VEC>
-__global__ void __launch_bounds__(NT) estmm_simt_kernel(EstmmArgs a) {
+__global__ void __launch_bounds__(NT) esmm_simt_kernel(EsmmArgs a) {
   const int ti = blockIdx.y;
   if (ti >= *a.n_tiles) return;
-  const SegTile tile = a.tiles[ti];
+  const int64_t K = a.d1;
+  const int64_t kper = ceil_div(ceil_div(K, BK), gridDim.z) * BK;
+  const int64_t kb = blockIdx.z * kper, ke = min(K, kb + kper);
+  esmm_simt_body<T, VEC>(a, a.tiles[ti], blockIdx.x * BN, kb, ke, blockIdx.z == 0);
+}
+
+// ESTMM: 64 x 64 output tile per CTA over positions [pb, pe) of a chunk;
+// `reduce`: atomicAdd into a pre-zeroed output instead of a store.
+template <class T, bool VEC>
+__device__ __forceinline__ void estmm_simt_body(const EstmmArgs& a, const SegTile tile,
+                                                const int m0, const int n0, const int64_t pb,
+                                                const int64_t pe, const bool reduce) {
   const int64_t D1 = a.d1, D2 = a.d2;
-  const int mt = static_cast<int>(ceil_div(D1, BM));
-  const int m0 = (blockIdx.x % mt) * BM, n0 = (blockIdx.x / mt) * BN;
   const T* X1 = static_cast<const T*>(a.x1);
   const T* X2 = static_cast<const T*>(a.x2);
-  const int64_t len = tile.end - tile.begin;
-  const int64_t per = ceil_div(ceil_div(len, BK), gridDim.z) * BK;
-  const int64_t pb = tile.begin + blockIdx.z * per, pe = pb + per < tile.end ? pb + per : static_cast<int64_t>(tile.end);
   __shared__ __align__(16) float As[BK][BM];
   __shared__ __align__(16) float Bs[BK][BN];
   __shared__ int r1[BK], r2[BK];
@@ -240,7 +242,6 @@ __global__ void __launch_bounds__(NT) estmm_simt_kernel(EstmmArgs a) {
     __syncthreads();
   }
   float* out = a.out + static_cast<int64_t>(tile.expert) * D1 * D2;
-  const bool reduce = (tile.flags & 1) || gridDim.z > 1;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int64_t m = m0 + ty * 4 + i;
@@ -252,6 +253,89 @@ __global__ void __launch_bounds__(NT) estmm_simt_kernel(EstmmArgs a) {
       if (reduce) atomicAdd(out + m * D2 + n, acc[i][j]);
       else out[m * D2 + n] = acc[i][j];
     }
+  }
+}
+
+// ESTMM: 64 x 64 output tile per CTA, K = the chunk's token positions in
+// steps of 16; blockIdx.z splits the positions (the output is then pre-zeroed
+// and every split reduces with atomicAdd).
+template <class T, bool VEC>
+__global__ void __launch_bounds__(NT) estmm_simt_kernel(EstmmArgs a) {
+  const int ti = blockIdx.y;
+  if (ti >= *a.n_tiles) return;
+  const SegTile tile = a.tiles[ti];
+  const int mt = static_cast<int>(ceil_div(a.d1, BM));
+  const int m0 = (blockIdx.x % mt) * BM, n0 = (blockIdx.x / mt) * BN;
+  const int64_t len = tile.end - tile.begin;
+  const int64_t per = ceil_div(ceil_div(len, BK), gridDim.z) * BK;
+  const int64_t pb = tile.begin + blockIdx.z * per,
+                pe = pb + per < tile.end ? pb + per : static_cast<int64_t>(tile.end);
+  estmm_simt_body<T, VEC>(a, tile, m0, n0, pb, pe, (tile.flags & 1) || gridDim.z > 1);
+}
+
+// ESFK (es_ops.cpp:210-247) in ONE launch on the fp32 path: the 1-D grid is
+// the reference's combined work list -- [grad-x ESMM tiles | grad-b ESS
+// columns | grad-W ESTMM tiles] -- over the caller's ReIndex directly (tiles
+// found by a per-block scan of the segment lengths, rows gathered through v).
+// Every output element has exactly one writer (no split-K, no atomics), so
+// the launch needs no pre-zeroing and is deterministic.
+struct EsfkSimt {
+  EsmmArgs gx;   // a = g (K = d2), w = w_t, out = grad_x (EPI_WRITE), maps via v
+  EstmmArgs gw;  // x1 = x, x2 = g, out = grad_w
+  const void* g;
+  int64_t d2;
+  float* grad_b;
+  const int64_t* idx;
+  const int64_t* v;
+  int E;
+  int r0, r1;  // block ranges: [0, r0) ESMM, [r0, r1) ESS, [r1, grid) ESTMM
+  int gx_cb;   // ESMM column blocks (ceil(d1 / 64))
+};
+
+template <class T, bool VEC>
+__global__ void __launch_bounds__(NT) esfk_simt_kernel(EsfkSimt f) {
+  extern __shared__ int32_t toff[];  // E + 1: exclusive scan of 64-row tiles per expert
+  const int b = blockIdx.x, E = f.E;
+  if (b < f.r0) {
+    if (threadIdx.x == 0) {
+      int32_t run = 0;
+      for (int e = 0; e < E; ++e) {
+        toff[e] = run;
+        run += static_cast<int32_t>(ceil_div(f.idx[e + 1] - f.idx[e], BM));
+      }
+      toff[E] = run;
+    }
+    __syncthreads();
+    const int ti = b / f.gx_cb, cb = b % f.gx_cb;
+    if (ti >= toff[E]) return;
+    int lo = 0, hi = E;  // last e with toff[e] <= ti
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) / 2;
+      if (toff[mid] <= ti) lo = mid; else hi = mid;
+    }
+    const int64_t begin = f.idx[lo] + static_cast<int64_t>(ti - toff[lo]) * BM;
+    const int64_t end = min(f.idx[lo + 1], begin + BM);
+    const SegTile t{lo, static_cast<int>(begin), static_cast<int>(end), 0};
+    esmm_simt_body<T, VEC>(f.gx, t, cb * BN, 0, f.gx.d1, true);
+  } else if (b < f.r1) {
+    // grad_b[e][c]: thread per column, the segment's rows in order
+    const int cblk = static_cast<int>(ceil_div(f.d2, NT));
+    const int e = (b - f.r0) / cblk;
+    const int64_t c = static_cast<int64_t>((b - f.r0) % cblk) * NT + threadIdx.x;
+    if (c >= f.d2) return;
+    const T* G = static_cast<const T*>(f.g);
+    float s = 0.f;
+    for (int64_t p = f.idx[e]; p < f.idx[e + 1]; ++p) {
+      const int64_t t = f.v[p];
+      if (t >= 0) s += to_f32(G[t * f.d2 + c]);
+    }
+    f.grad_b[static_cast<int64_t>(e) * f.d2 + c] = s;
+  } else {
+    const int mt = static_cast<int>(ceil_div(f.gw.d1, BM)), nt = static_cast<int>(ceil_div(f.gw.d2, BN));
+    const int j = b - f.r1;
+    const int e = j / (mt * nt), rem = j % (mt * nt);
+    const SegTile t{e, static_cast<int>(f.idx[e]), static_cast<int>(f.idx[e + 1]), 0};
+    estmm_simt_body<T, VEC>(f.gw, t, (rem % mt) * BM, (rem / mt) * BN, t.begin, t.end, false);
   }
 }
 
@@ -308,6 +392,59 @@ hxm_status simt_estmm(hxm_dtype dt, const EstmmArgs& a, cudaStream_t st) {
   else if (vec) estmm_simt_kernel<float, true><<<grid, NT, 0, st>>>(a);
   else estmm_simt_kernel<float, false><<<grid, NT, 0, st>>>(a);
   HXM_CHECK_LAUNCH();
+  return HXM_OK;
+}
+
+hxm_status simt_esfk(hxm_dtype dt, const void* x, const void* g, int64_t n, int64_t d1,
+                     int64_t d2, const void* w, int w_trans, const int64_t* v, const int64_t* idx,
+                     int64_t E, int64_t np_bound, float* grad_x, float* grad_b, float* grad_w,
+                     cudaStream_t st) {
+  EsfkSimt f{};
+  f.gx.a = g;
+  f.gx.amap = map_v64(v);
+  f.gx.a_rows = n;
+  f.gx.n_experts = E;
+  f.gx.w = w;
+  f.gx.w_trans = w_trans;
+  f.gx.d1 = d2;  // K
+  f.gx.d2 = d1;  // N
+  f.gx.epi = EPI_WRITE;
+  f.gx.out_f32 = grad_x;
+  f.gx.omap = map_v64(v);
+  f.gw.x1 = x;
+  f.gw.m1 = map_v64(v);
+  f.gw.x2 = g;
+  f.gw.m2 = map_v64(v);
+  f.gw.d1 = d1;
+  f.gw.d2 = d2;
+  f.gw.out = grad_w;
+  f.g = g;
+  f.d2 = d2;
+  f.grad_b = grad_b;
+  f.idx = idx;
+  f.v = v;
+  f.E = static_cast<int>(E);
+  f.gx_cb = static_cast<int>(ceil_div(d1, BN));
+  const int64_t tiles = max_tiles(np_bound, E, BM);
+  const int64_t r0 = tiles * f.gx_cb;
+  const int64_t r1 = r0 + E * ceil_div(d2, NT);
+  const int64_t nb = r1 + E * ceil_div(d1, BM) * ceil_div(d2, BN);
+  if (nb > 0x7fffffffLL) return invalid_arg("esfk: grid too large");
+  f.r0 = static_cast<int>(r0);
+  f.r1 = static_cast<int>(r1);
+  const size_t smem = (static_cast<size_t>(E) + 1) * sizeof(int32_t);
+  const bool vec = dt == HXM_F32 && d1 % 4 == 0 && d2 % 4 == 0 && vec_ok(x) && vec_ok(g) && vec_ok(w);
+  const void* kern = dt == HXM_BF16 ? reinterpret_cast<const void*>(esfk_simt_kernel<__nv_bfloat16, false>)
+                     : vec ? reinterpret_cast<const void*>(esfk_simt_kernel<float, true>)
+                           : reinterpret_cast<const void*>(esfk_simt_kernel<float, false>);
+  if (smem > 48 * 1024)
+    HXM_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+  void* args[] = {&f};
+  if (nb > 0) {
+    HXM_TRY_CUDA(cudaLaunchKernel(kern, dim3(static_cast<unsigned>(nb)), dim3(NT), args, smem, st));
+    HXM_CHECK_LAUNCH();
+  }
   return HXM_OK;
 }
 
