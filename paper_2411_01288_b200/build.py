@@ -36,7 +36,7 @@ def _headers():
     out = []
     for d in (CSRC, os.path.join(ROOT, "include")):
         for f in os.listdir(d):
-            if f.endswith((".cuh", ".h", ".hpp")):
+            if f.endswith((".cuh", ".h", ".hpp", ".inc")):
                 out.append(os.path.join(d, f))
     return out
 

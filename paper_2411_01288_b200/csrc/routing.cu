@@ -489,7 +489,7 @@ __global__ void __launch_bounds__(kThreads) fwd_prologue_1b(FwdPrologue a) {
   __shared__ int32_t tot[kFastMaxE + 1];
   __shared__ int32_t bef[kFastMaxE];
   __shared__ int32_t sidx[kFastMaxE + 1];
-  __shared__ int32_t part[kThreads];
+  __shared__ __align__(16) int32_t part4[2 * kThreads * 4];
   extern __shared__ int32_t dyn[];
   int32_t* se = dyn;             // [S] expert of slot i (-1: invalid / past the end)
   int32_t* sr = dyn + a.chunk;   // [S] rank of slot i among its group's equal experts
@@ -531,44 +531,50 @@ __global__ void __launch_bounds__(kThreads) fwd_prologue_1b(FwdPrologue a) {
   pro_ts(1);
   grid.sync();
   pro_ts(2);
-  // ---- B: y = 0 (stores overlap the index arithmetic) ---------------------
+  // ---- B: totals and the counts of the blocks before this one -------------
+  // thread (r, q) reads the int4 column group q (experts 4q..4q+3) of rows
+  // r, r + R, ... of the G x E count table, eight rows in flight at a time
+  // (one L2 round trip per batch), then the R row groups are added in a
+  // fixed order.  E % 4 == 0 and E <= 256 on this path.
   {
-    const int64_t gtid = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
-    zero_f32(a.y, a.y_elems, gtid, static_cast<int64_t>(gridDim.x) * kThreads);
-  }
-  // totals and the counts of the blocks before this one: thread (r, e) sums
-  // rows r, r + R, ... of the G x E count table (E <= kThreads), then the R
-  // row groups are added in a fixed order
-  {
-    const int R = kThreads / E;
-    const int r = threadIdx.x / E, e = threadIdx.x % E;
-    int32_t t_all = 0, t_bef = 0;
+    const int Q = E / 4, R = kThreads / Q;
+    const int r = threadIdx.x / Q, q = threadIdx.x % Q;
+    const int G = gridDim.x, me = blockIdx.x;
+    int4 t_all = make_int4(0, 0, 0, 0), t_bef = make_int4(0, 0, 0, 0);
     if (r < R) {
-      const int G = gridDim.x, me = blockIdx.x;
-#pragma unroll 4
-      for (int b = r; b < G; b += R) {
-        const int32_t c = __ldcg(a.cnt + static_cast<int64_t>(b) * E + e);
-        t_all += c;
-        t_bef += b < me ? c : 0;
+      const int4* cnt4 = reinterpret_cast<const int4*>(a.cnt);
+      for (int b0 = r; b0 < G; b0 += 8 * R) {
+        int4 c[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int b = b0 + u * R;
+          c[u] = b < G ? __ldcg(cnt4 + static_cast<int64_t>(b) * Q + q) : make_int4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int b = b0 + u * R;
+          t_all.x += c[u].x; t_all.y += c[u].y; t_all.z += c[u].z; t_all.w += c[u].w;
+          if (b < me) { t_bef.x += c[u].x; t_bef.y += c[u].y; t_bef.z += c[u].z; t_bef.w += c[u].w; }
+        }
       }
     }
-    part[threadIdx.x] = t_all;
+    int4* p4 = reinterpret_cast<int4*>(part4);
+    p4[threadIdx.x] = t_all;
+    p4[kThreads + threadIdx.x] = t_bef;
     __syncthreads();
     if (threadIdx.x < E) {
-      int32_t s = 0;
-      for (int q = 0; q < R; ++q) s += part[q * E + threadIdx.x];
+      const int qq = threadIdx.x / 4, j = threadIdx.x % 4;
+      int32_t s = 0, sb = 0;
+      for (int rr = 0; rr < R; ++rr) {
+        s += part4[(rr * Q + qq) * 4 + j];
+        sb += part4[(kThreads + rr * Q + qq) * 4 + j];
+      }
       tot[threadIdx.x] = s;
-    }
-    __syncthreads();
-    part[threadIdx.x] = t_bef;
-    __syncthreads();
-    if (threadIdx.x < E) {
-      int32_t s = 0;
-      for (int q = 0; q < R; ++q) s += part[q * E + threadIdx.x];
-      bef[threadIdx.x] = s;
+      bef[threadIdx.x] = sb;
     }
     __syncthreads();
   }
+  pro_ts(3);
   block_idx<int32_t>(tot, E, a.blk, sidx, a.capacity);
   if (blockIdx.x == 0)
     for (int e = threadIdx.x; e <= E; e += kThreads) a.idx[e] = sidx[e];
@@ -598,6 +604,12 @@ __global__ void __launch_bounds__(kThreads) fwd_prologue_1b(FwdPrologue a) {
     if (a.x)
       for (int64_t p = p0 + warp; p < p1; p += kWarps) zero_row(XS + p * rb, rb, lane, a.unit);
   }
+  pro_ts(4);
+  // y = 0: its stores overlap the tile passes and this block's row copies
+  {
+    const int64_t gtid = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    zero_f32(a.y, a.y_elems, gtid, static_cast<int64_t>(gridDim.x) * kThreads);
+  }
   // the three tilings on the last three blocks
   {
     const int tb = static_cast<int>(gridDim.x) - 1 - static_cast<int>(blockIdx.x);
@@ -612,7 +624,7 @@ __global__ void __launch_bounds__(kThreads) fwd_prologue_1b(FwdPrologue a) {
       tile_pass<int32_t, kThreads>(sidx, E, a.s2.rows, a.s2.min_one, a.s2.tiles, a.s2.tile_off,
                                    a.s2.n_tiles, tot, a.s2.split_rows);
   }
-  pro_ts(3);
+  pro_ts(5);
   if (!a.x) return;
   __syncthreads();
   // ---- B': x rows of this block's slots to their sorted positions ---------
@@ -659,7 +671,8 @@ __global__ void __launch_bounds__(kThreads) fwd_prologue_1b(FwdPrologue a) {
       if (pos >= 0) copy_row(X + ((s0 + i) % a.n_tok) * rb, XS + pos * rb, rb, lane, a.unit);
     }
   }
-  pro_ts(4);
+  __syncthreads();
+  pro_ts(6);
 }
 
 }  // namespace
@@ -702,7 +715,7 @@ hxm_status launch_fwd_prologue(FwdPrologue a, cudaStream_t st) {
   const char* g1 = std::getenv("HXM_PRO1");  // 0: the three-barrier prologue
   // one-barrier prologue: S = 32 * groups slots per block, every block
   // co-resident, the group counts in static smem
-  if (!(g1 && g1[0] == '0') && a.E <= kFastMaxE) {
+  if (!(g1 && g1[0] == '0') && a.E <= kFastMaxE && a.E % 4 == 0) {
     const int64_t slots_max = static_cast<int64_t>(sm_count()) * per_sm;
     const int groups = static_cast<int>(std::max<int64_t>(1, ceil_div(a.n_slots, 32 * slots_max)));
     if (groups <= kFastMaxGroups) {

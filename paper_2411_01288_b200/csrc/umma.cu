@@ -56,7 +56,9 @@ hxm_status umma_estmm(const EstmmArgs& a, cudaStream_t st) {
   const bool ga = a.m1.kind != MAP_DENSE, gb = a.m2.kind != MAP_DENSE;
   // CTA pairs (M = 256 output rows per pair) when both operands are dense
   // and the output rows tile evenly
-  const int CG = (!ga && !gb && a.d1 % 256 == 0 && pick_bn2(a.d2, true) > 0) ? 2 : 1;
+  const char* env = std::getenv("HXM_CTA_PAIR");  // 0: single-CTA tiles everywhere
+  const bool pair_ok = !(env && env[0] == '0');
+  const int CG = (pair_ok && !ga && !gb && a.d1 % 256 == 0 && pick_bn2(a.d2, true) > 0) ? 2 : 1;
   const int bn = CG == 2 ? pick_bn2(a.d2, true) : pick_bn(a.d2);
   UParams prm{};
   HXM_RETURN_IF(prep_estmm(a, CG, bn, prm));

@@ -16,3 +16,4 @@ buf = (ctypes.c_ulonglong * 8)()
 L.hxm_debug_prologue_ts(buf)
 t = list(buf)
 print("phase ns:", [t[i+1]-t[i] for i in range(7)], "total", t[7]-t[0])
+print("phase us:", [round((t[i+1]-t[i])/1000, 2) if 0 <= t[i+1]-t[i] < 10**9 else None for i in range(7)])
