@@ -195,7 +195,25 @@ typedef struct hxm_layer_desc {
                          kept, overflow is dropped (zero contribution),
                          shortfall rows are zero padding that the GEMMs
                          process.  Must be a multiple of 64. */
+  int32_t weight_shards; /* 0 or 1: w1 / b1 / w2 in the reference layout
+                         (E x D_i x H, E x H, E x H x D_o).  P > 1:
+                         shard-major -- the data-centric TP cache filled by
+                         an all-gather of P hidden shards straight into one
+                         buffer, no repacking (dist_sim.cpp:367-368):
+                         w1 P x E x D_i x h, b1 P x E x h, w2 P x E x h x D_o
+                         with h = H / P (bf16 tcgen05 path; h a multiple of
+                         64 and of the GEMMs' tile widths,
+                         hxm_layer_weight_shards_ok). */
+  int32_t reserved0;
+  void* weights_ready;  /* cudaEvent_t or NULL: the forward waits on it
+                         after its routing prologue and before the first
+                         kernel that reads w1 / b1 / w2 -- the cache fill
+                         (on a side stream) overlaps the index build. */
 } hxm_layer_desc;
+
+/* 1 if the layer can read shard-major weights split P ways (see
+ * hxm_layer_desc.weight_shards), else 0. */
+int hxm_layer_weight_shards_ok(const hxm_layer_desc* desc, int32_t n_shards);
 
 size_t hxm_layer_workspace_bytes(const hxm_layer_desc* desc);
 

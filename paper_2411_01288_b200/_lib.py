@@ -37,7 +37,8 @@ class LayerDesc(C.Structure):
     _fields_ = [("n_tokens", C.c_int64), ("n_experts", C.c_int64), ("k", C.c_int64),
                 ("d_in", C.c_int64), ("hidden", C.c_int64), ("d_out", C.c_int64),
                 ("activation", C.c_int32), ("dtype", C.c_int32), ("add_b2", C.c_int32),
-                ("capacity", C.c_int32)]
+                ("capacity", C.c_int32), ("weight_shards", C.c_int32),
+                ("reserved0", C.c_int32), ("weights_ready", C.c_void_p)]
 
 
 MAX_PEERS = 8
@@ -85,6 +86,7 @@ SIGNATURES = {
     "hxm_moe_stash_export": (C.c_int, [C.POINTER(LayerDesc), _p, _i64, _p, _p, _p]),
     "hxm_layer_forward_macs": (C.c_uint64, [C.POINTER(LayerDesc)]),
     "hxm_layer_path": (C.c_int, [C.POINTER(LayerDesc)]),
+    "hxm_layer_weight_shards_ok": (C.c_int, [C.POINTER(LayerDesc), C.c_int32]),
     "hxm_op_stats_add": (None, [C.c_int, _i64, _i64, _i64, _i64, _p]),
     "hxm_synthesize_routing": (C.c_int, [_i64, _i64, _i64, C.c_char_p, C.c_uint64, _p]),
     "hxm_make_layer_inputs": (None, [C.c_uint64, _i64, _i64, _i64, _i64, _i64, C.c_double, _p,

@@ -8,6 +8,8 @@
 #include <vector>
 
 #include <cstdlib>
+#include <map>
+#include <mutex>
 
 #include "common.cuh"
 
@@ -31,14 +33,16 @@ int sm_count() {
   return n;
 }
 
-// A non-blocking side stream per device plus two fork/join events, for
-// independent work that runs beside the main stream (recorded into CUDA
-// graphs as parallel branches under stream capture).
-SideStream side_stream() {
-  static SideStream cached[64];
+// A non-blocking side stream plus fork/join events per (device, caller
+// stream), for independent work that runs beside the caller's stream
+// (recorded into CUDA graphs as parallel branches under stream capture).
+SideStream side_stream(cudaStream_t caller) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, SideStream> cache;
   int dev = 0;
   cudaGetDevice(&dev);
-  SideStream& s = cached[dev < 64 ? dev : 0];
+  std::lock_guard<std::mutex> lock(mu);
+  SideStream& s = cache[{dev, caller}];
   if (!s.st) {
     cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming);

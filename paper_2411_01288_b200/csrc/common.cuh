@@ -63,7 +63,36 @@ struct SideStream {
   cudaStream_t st = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
 };
-SideStream side_stream();  // per device, created on first use
+// A side stream and fork/join events of its own for each (device, caller
+// stream): independent callers never share events or serialise through one
+// side stream.  Created on first use (thread-safe).
+SideStream side_stream(cudaStream_t caller);
+// Fork `side` off `main` now; the destructor joins it back (records `join`
+// on the side stream and makes `main` wait), also on early error returns,
+// so a stream capture never ends with an unjoined branch.
+class SideBranch {
+ public:
+  SideBranch(cudaStream_t main, const SideStream& side) : main_(main), side_(side) {
+    ok_ = cudaEventRecord(side_.fork, main_) == cudaSuccess &&
+          cudaStreamWaitEvent(side_.st, side_.fork, 0) == cudaSuccess;
+  }
+  ~SideBranch() { join(); }
+  bool ok() const { return ok_; }
+  cudaError_t join() {
+    if (joined_) return cudaSuccess;
+    joined_ = true;
+    cudaError_t e = cudaEventRecord(side_.join, side_.st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(main_, side_.join, 0);
+    return e;
+  }
+  SideBranch(const SideBranch&) = delete;
+  SideBranch& operator=(const SideBranch&) = delete;
+
+ private:
+  cudaStream_t main_;
+  SideStream side_;
+  bool ok_ = false, joined_ = false;
+};
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) {
   return (a + b - 1) / b;

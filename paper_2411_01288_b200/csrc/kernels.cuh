@@ -67,6 +67,8 @@ struct EsmmArgs {
   const hxm_peer_rows* peer;  // EPI_ATOMIC: rows reduced into their owners' buffers
   float* colsum;    // BWD_ACT (tcgen05): per-(tile, CTA, lane group) column sums of out1,
                     // [((tile * CG + cta) * 4 + group) x d2] -> colsum_combine
+  int w_shards;     // > 1: w (and, for FWD_ACT, bias) shard-major [P][E][..]: the H axis
+  int w_split_k;    // split in P slices -- K (d1) when set, else N (d2); tcgen05 only
 };
 
 struct EstmmArgs {
@@ -171,6 +173,10 @@ bool umma_supports_esmm(int64_t d1, int64_t d2);
 bool umma_supports_estmm(int64_t d1, int64_t d2);
 // CTA-pair ESMM (dense A, 256-row tiles): BN must split into whole B halves
 bool umma2_supports_esmm(int64_t d1, int64_t d2, bool w_trans);
+// the tile widths the tcgen05 launchers pick for an output width n
+// (single CTA / CTA pair with MN-major or K-major B)
+int umma_pick_bn(int64_t n);
+int umma_pick_bn2(int64_t n, bool b_mn);
 
 // esfk (es_ops.cpp:210-247): grad_x = esmm(g, W^T / w_t), grad_b = ess(g),
 // grad_w = estmm(x, g) over the caller's ReIndex.  simt: one launch (fp32);

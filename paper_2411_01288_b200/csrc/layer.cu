@@ -19,6 +19,8 @@
 //    GEMM reads W K-major;
 //  * y and gx accumulate over choices with fp32 reductions into zeroed
 //    buffers (the memory-efficient scheme, moe_layer.cpp:61-63).
+#include <memory>
+
 #include "kernels.cuh"
 #include "routing.cuh"
 
@@ -127,7 +129,24 @@ hxm_status check_desc(const hxm_layer_desc* d) {
     return invalid_arg("moe layer: capacity must be 0 or a positive multiple of 64");
   if (static_cast<int64_t>(d->capacity) * d->n_experts > 0x7fffffffLL)
     return invalid_arg("moe layer: capacity * E exceeds int32 row range");
+  if (d->weight_shards < 0 || d->weight_shards > 64)
+    return invalid_arg("moe layer: weight_shards must be 0..64");
   return HXM_OK;
+}
+
+// shard-major weights: every GEMM that reads W must keep its boxes inside
+// one shard (h % 64 for the K-split uses; h % the CTA's B width for the
+// N-split ones) -- the tile widths are those the tcgen05 launchers pick
+bool shards_ok(const hxm_layer_desc& d, const LayerWs& w, int64_t P) {
+  if (P <= 1) return true;
+  if (w.rows_a < kUmmaRows || d.hidden % P != 0) return false;
+  const int64_t h = d.hidden / P;
+  if (h % 64 != 0) return false;
+  const int CG = w.rows_a == kUmma2Rows ? 2 : 1;
+  // N = H for fwd1 (W1, MN-major) and bwd_act (W2^T, K-major)
+  const int bn_f = CG == 2 ? umma_pick_bn2(d.hidden, true) : umma_pick_bn(d.hidden);
+  const int bn_b = CG == 2 ? umma_pick_bn2(d.hidden, false) : umma_pick_bn(d.hidden);
+  return bn_f > 0 && bn_b > 0 && h % (bn_f / CG) == 0 && h % (bn_b / CG) == 0;
 }
 
 // stash export: sorted row p (slot s = choice*N + t) -> token-order fp32
@@ -166,6 +185,13 @@ int hxm_layer_path(const hxm_layer_desc* d) {
   Arena ar(nullptr, 0);
   const LayerWs w = carve(ar, *d);
   return w.rows_a == kUmma2Rows ? 2 : (w.rows_a == kUmmaRows ? 1 : 0);
+}
+
+int hxm_layer_weight_shards_ok(const hxm_layer_desc* d, int32_t n_shards) {
+  if (check_desc(d) != HXM_OK) return 0;
+  Arena ar(nullptr, 0);
+  const LayerWs w = carve(ar, *d);
+  return shards_ok(*d, w, n_shards) ? 1 : 0;
 }
 
 uint64_t hxm_layer_forward_macs(const hxm_layer_desc* d) {
@@ -224,6 +250,8 @@ hxm_status layer_forward(const hxm_layer_desc* d, const void* x, const void* w1,
   Arena ar(ws, ws_bytes);
   LayerWs w = carve(ar, *d);
   if (ar.overflow) return invalid_arg("moe_forward: workspace too small");
+  if (!shards_ok(*d, w, d->weight_shards))
+    return invalid_arg("moe_forward: shard-major weights unsupported for this shape");
   HXM_RETURN_IF(check_peer(yp, d, w, "moe_forward_tp"));
   const hxm_dtype dt = static_cast<hxm_dtype>(d->dtype);
   const int64_t N = d->n_tokens, E = d->n_experts, slots = d->k * N;
@@ -265,6 +293,9 @@ hxm_status layer_forward(const hxm_layer_desc* d, const void* x, const void* w1,
     HXM_RETURN_IF(launch_fwd_prologue(pro, st));
   }
   if (N == 0) return HXM_OK;
+  // the cache fill of shard-major weights overlapped the index build
+  if (d->weights_ready)
+    HXM_TRY_CUDA(cudaStreamWaitEvent(st, reinterpret_cast<cudaEvent_t>(d->weights_ready), 0));
   const RowMap slot = map_slot(w.v, N);
   // (1) y1 = x W1 + b1 ; y2 = F(y1)          (moe_layer.cpp:56-57)
   EsmmArgs a1{};
@@ -274,6 +305,8 @@ hxm_status layer_forward(const hxm_layer_desc* d, const void* x, const void* w1,
   a1.n_experts = E;
   a1.w = w1;
   a1.w_trans = 0;
+  a1.w_shards = static_cast<int>(d->weight_shards);  // W1 [P][E][D_i][h]: N (H) split
+  a1.w_split_k = 0;
   a1.d1 = d->d_in;
   a1.d2 = d->hidden;
   a1.bias = b1;
@@ -301,6 +334,7 @@ hxm_status layer_forward(const hxm_layer_desc* d, const void* x, const void* w1,
   a2.amap = map_dense();
   a2.a_rows = w.bound;
   a2.w = w2;
+  a2.w_split_k = 1;  // W2 [P][E][h][D_o]: K (H) split
   a2.d1 = d->hidden;
   a2.d2 = d->d_out;
   a2.bias = d->add_b2 ? b2 : nullptr;
@@ -332,6 +366,8 @@ hxm_status layer_backward(const hxm_layer_desc* d, const void* x, const void* w1
   Arena ar(ws, ws_bytes);
   LayerWs w = carve(ar, *d);
   if (ar.overflow) return invalid_arg("moe_backward: workspace too small");
+  if (!shards_ok(*d, w, d->weight_shards))
+    return invalid_arg("moe_backward: shard-major weights unsupported for this shape");
   HXM_RETURN_IF(check_peer(gxp, d, w, "moe_backward_tp"));
   HXM_RETURN_IF(check_shards(gw1p, d, w, "moe_backward_dc gW1"));
   HXM_RETURN_IF(check_shards(gw2p, d, w, "moe_backward_dc gW2"));
@@ -409,6 +445,8 @@ hxm_status layer_backward(const hxm_layer_desc* d, const void* x, const void* w1
   b6.n_experts = E;
   b6.w = w2;
   b6.w_trans = 1;  // W2 is E x H x Do; use W2[e]^T (Do x H)
+  b6.w_shards = static_cast<int>(d->weight_shards);  // N (H) split
+  b6.w_split_k = 0;
   b6.d1 = Do;
   b6.d2 = H;
   b6.tiles = w.tiles_a;
@@ -429,7 +467,7 @@ hxm_status layer_backward(const hxm_layer_desc* d, const void* x, const void* w1
   // bf16 tile per (tile, CTA)), then a deterministic per-expert combine
   b6.colsum = w.colsum;
   HXM_RETURN_IF(launch_esmm(dt, b6, st));
-  SideStream side{};
+  std::unique_ptr<SideBranch> branch;  // joined on every return path
   const char* se = std::getenv("HXM_SIDE");
   const bool use_side = !(se && se[0] == '0');
   if (w.colsum && !use_side) {
@@ -440,14 +478,16 @@ hxm_status layer_backward(const hxm_layer_desc* d, const void* x, const void* w1
   } else if (w.colsum) {
     // the gb1 combine is independent of gW1 / gx: it runs on the side
     // stream beside them (a parallel branch of the captured graph)
-    side = side_stream();
-    HXM_TRY_CUDA(cudaEventRecord(side.fork, st));
-    HXM_TRY_CUDA(cudaStreamWaitEvent(side.st, side.fork, 0));
+    const SideStream side = side_stream(st);
+    branch.reset(new SideBranch(st, side));
+    if (!branch->ok()) {
+      set_error("moe_backward: side-stream fork failed");
+      return HXM_ERR_CUDA;
+    }
     const int parts = (w.rows_a / kUmmaRows) * 4;  // per tile: CTAs x TMEM lane groups
     HXM_RETURN_IF(launch_colsum_combine(
         w.colsum, w.tiles_a_off, static_cast<int>(E), parts, H, gb1, side.st, "gb1_combine",
         (static_cast<double>(max_tiles(w.bound, E, w.rows_a)) * parts + E) * H * 4.0));
-    HXM_TRY_CUDA(cudaEventRecord(side.join, side.st));
   } else {
     es.x = w.g1s;
     es.map = map_dense();
@@ -482,6 +522,7 @@ hxm_status layer_backward(const hxm_layer_desc* d, const void* x, const void* w1
   b10.a_rows = w.bound;
   b10.w = w1;
   b10.w_trans = 1;  // W1 is E x Di x H; use W1[e]^T (H x Di)
+  b10.w_split_k = 1;  // K (H) split
   b10.d1 = H;
   b10.d2 = Di;
   b10.epi = EPI_ATOMIC;
@@ -494,7 +535,7 @@ hxm_status layer_backward(const hxm_layer_desc* d, const void* x, const void* w1
   b10.out1 = nullptr;
   b10.y1s = nullptr;
   HXM_RETURN_IF(launch_esmm(dt, b10, st));
-  if (side.st) HXM_TRY_CUDA(cudaStreamWaitEvent(st, side.join, 0));
+  if (branch) HXM_TRY_CUDA(branch->join());
   return HXM_OK;
 }
 

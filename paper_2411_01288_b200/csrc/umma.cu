@@ -25,6 +25,8 @@ bool umma_supports_esmm(int64_t d1, int64_t d2) {
   return d1 > 0 && d2 > 0 && d1 % 64 == 0 && d2 % 64 == 0 && d1 < (1 << 30) && d2 < (1 << 30);
 }
 bool umma_supports_estmm(int64_t d1, int64_t d2) { return umma_supports_esmm(d1, d2); }
+int umma_pick_bn(int64_t n) { return pick_bn(n); }
+int umma_pick_bn2(int64_t n, bool b_mn) { return pick_bn2(n, b_mn); }
 bool umma2_supports_esmm(int64_t d1, int64_t d2, bool w_trans) {
   return umma_supports_esmm(d1, d2) && pick_bn2(d2, !w_trans) > 0;
 }

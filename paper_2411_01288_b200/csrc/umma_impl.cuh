@@ -232,6 +232,22 @@ __device__ __forceinline__ void tma_3d_cg2(void* dst, const CUtensorMap* map, ui
       "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+__device__ __forceinline__ void tma_5d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                       int c1, int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+__device__ __forceinline__ void tma_5d_cg2(void* dst, const CUtensorMap* map, uint32_t bar, int c0,
+                                           int c1, int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
 __device__ __forceinline__ void tma_4d_cg2(void* dst, const CUtensorMap* map, uint32_t bar, int c0,
                                            int c1, int c2, int c3) {
   asm volatile(
@@ -450,6 +466,13 @@ struct UParams {
   int dbg_noload;
   unsigned long long* trace;  // debug timeline (HXM_TRACE), null normally
   int b_sw64;  // CG = 2, MN-major B halves of 32-column multiples: 64B-swizzled boxes
+  // shard-major weights (data-centric TP cache, hxm_layer_desc.weight_shards):
+  // W is [P][E][..] with the H axis split into P slices of w_shard_h; the B
+  // map gains a shard dimension.  w_shard_k: the split H axis is K (else N).
+  int w_shard_h;
+  int w_shard_k;
+  int bias_shard_h;  // MODE 1: b1 is [P][E][h] (0: E x N)
+  int n_experts;
   int l2hint;  // MODE 1/2: L2 eviction-priority hints on the stash stores
   int reverse; // walk the work items last to first
   int n_peer;            // EPI_ATOMIC: > 0 -> row t reduces into peer[t / peer_rows]
@@ -471,6 +494,37 @@ struct UParams {
   float* est_out;
   const char* label;
 };
+
+// B operand box of one k-block: W[e] (MN-major, 4D view / 5D shard-major)
+// or W^T use (K-major, 3D view / 4D shard-major).  `nb` = this CTA's first B
+// column, k0 = the k-block's first K row.
+template <int CG>
+__device__ __forceinline__ void load_w_box(const UParams& p, void* sb, uint64_t* bar_local,
+                                           uint32_t bar_lead, int k0, int nb, int e) {
+  const int bw = p.b_sw64 ? 32 : 64;
+  const int h = p.w_shard_h;
+  if (p.b_kmajor) {
+    if (h == 0) {
+      if constexpr (CG == 2) tma_3d_cg2(sb, &p.tmB, bar_lead, k0, nb, e);
+      else tma_3d(sb, &p.tmB, bar_local, k0, nb, e);
+    } else {
+      const int c0 = p.w_shard_k ? k0 % h : k0, c1 = p.w_shard_k ? nb : nb % h;
+      const int sh = p.w_shard_k ? k0 / h : nb / h;
+      if constexpr (CG == 2) tma_4d_cg2(sb, &p.tmB, bar_lead, c0, c1, e, sh);
+      else tma_4d(sb, &p.tmB, bar_local, c0, c1, e, sh);
+    }
+  } else {
+    if (h == 0) {
+      if constexpr (CG == 2) tma_4d_cg2(sb, &p.tmB, bar_lead, 0, k0, nb / bw, e);
+      else tma_4d(sb, &p.tmB, bar_local, 0, k0, nb / bw, e);
+    } else {
+      const int c1 = p.w_shard_k ? k0 % h : k0, c2 = (p.w_shard_k ? nb : nb % h) / bw;
+      const int sh = p.w_shard_k ? k0 / h : nb / h;
+      if constexpr (CG == 2) tma_5d_cg2(sb, &p.tmB, bar_lead, 0, c1, c2, e, sh);
+      else tma_5d(sb, &p.tmB, bar_local, 0, c1, c2, e, sh);
+    }
+  }
+}
 
 // CG = CTAs per UMMA (cta_group): with CG = 2 a CTA pair runs M = 256 tiles,
 // each CTA holding 128 rows of A / D and half (BN/2) of the B columns.
@@ -621,20 +675,15 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
                 if (rank == 0) mbar_arrive_tx(&full[s], 2 * ((p.dbg_noload & 8) ? kABytes : C::kBBytes));
                 const int nb = n0 + static_cast<int>(rank) * (BN / 2);
                 if (p.dbg_noload & 8) tma_2d_cg2(sa, &p.tmA, fb, kb * BK, t.begin + static_cast<int>(rank) * BM);
-                else if (p.b_kmajor) tma_3d_cg2(sb, &p.tmB, fb, kb * BK, nb, t.expert);
-                else tma_4d_cg2(sb, &p.tmB, fb, 0, kb * BK, nb / (p.b_sw64 ? 32 : 64), t.expert);
+                else load_w_box<2>(p, sb, nullptr, fb, kb * BK, nb, t.expert);
               } else {
                 // the leader expects both CTAs' bytes; the peer's loads
                 // only complete_tx on it (no second remote arrive)
                 if (rank == 0) mbar_arrive_tx(&full[s], 2 * C::kStage);
                 tma_2d_cg2(sa, &p.tmA, fb, kb * BK, t.begin + static_cast<int>(rank) * BM);
                 const int nb = n0 + static_cast<int>(rank) * (BN / 2);
-                if (p.b_kmajor) {
-                  tma_3d_cg2(sb, &p.tmB, fb, kb * BK, nb, t.expert);
-                } else {
-                  // all of this CTA's swizzle-atom column chunks in one 4D box
-                  tma_4d_cg2(sb, &p.tmB, fb, 0, kb * BK, nb / (p.b_sw64 ? 32 : 64), t.expert);
-                }
+                // all of this CTA's swizzle-atom column chunks in one box
+                load_w_box<2>(p, sb, nullptr, fb, kb * BK, nb, t.expert);
               }
             }
           } else {
@@ -647,13 +696,7 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
             } else if (el) {
               tma_2d(sa, &p.tmA, &full[s], kb * BK, t.begin);
             }
-            if (el) {
-              if (p.b_kmajor) {
-                tma_3d(sb, &p.tmB, &full[s], kb * BK, n0, t.expert);
-              } else {
-                tma_4d(sb, &p.tmB, &full[s], 0, kb * BK, n0 / 64, t.expert);
-              }
-            }
+            if (el) load_w_box<1>(p, sb, &full[s], 0u, kb * BK, n0, t.expert);
           }
           __syncwarp();
           if (++s == C::kStages) { s = 0; ph ^= 1; }
@@ -846,8 +889,11 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
     float* gbias = bias_s + half * HB;
     const bool bias_smem = MODE == 1 && p.bias != nullptr;
     auto bias_at = [&](const SegTile& tt, int ww) {
-      return __ldg(p.bias + static_cast<int64_t>(tt.expert) * p.N + (ww % per_item) * BN + half * HB +
-                   lg * kBq + lane);
+      const int col = (ww % per_item) * BN + half * HB + lg * kBq + lane;
+      const int hb = p.bias_shard_h;
+      return __ldg(p.bias + (hb == 0 ? static_cast<int64_t>(tt.expert) * p.N + col
+                                     : (static_cast<int64_t>(col / hb) * p.n_experts + tt.expert) *
+                                               hb + col % hb));
     };
     if (bias_smem && lane < kBq && cluster < total) gbias[lg * kBq + lane] = bias_at(t_cur, wmap(cluster));
     int y_iss = 0;  // MODE 2 (elected thread): global F'(y1) chunks issued so far
@@ -1457,31 +1503,50 @@ hxm_status prep_esmm(const EsmmArgs& a, const int CG, const int bn, UParams& prm
     if (!make_map(&prm.tmA, a.a, 2, dims, strides, box))
       return invalid_arg("umma_esmm: cannot encode the A tensor map");
   }
-  // B: W[e] (E x d1 x d2, MN-major) or W^T use (E x d2 x d1, K-major)
+  // B: W[e] (E x d1 x d2, MN-major) or W^T use (E x d2 x d1, K-major).
+  // Shard-major weights (a.w_shards = P > 1): the split H axis (K when
+  // a.w_split_k, else N) is [P][E][..h..], one more map dimension (the shard)
+  // outermost; a box never straddles two shards (h % 64 == 0 for K, h % the
+  // CTA's B width for N -- checked here).
   {
     const int64_t E = a.n_experts;
+    const int64_t P = a.w_shards > 1 ? a.w_shards : 1;
+    const bool sk = P > 1 && a.w_split_k, sn = P > 1 && !a.w_split_k;
+    const int64_t hk = sk ? a.d1 / P : a.d1;  // K rows per shard (or all)
+    const int64_t hn = sn ? a.d2 / P : a.d2;  // N columns per shard (or all)
+    if (P > 1) {
+      const int64_t hsplit = sk ? a.d1 : a.d2;
+      if (hsplit % P != 0 || (hsplit / P) % 64 != 0 || (sn && (hsplit / P) % (bn / CG) != 0))
+        return invalid_arg("umma_esmm: shard-major weights need H / P a multiple of 64 and of "
+                           "the CTA's B tile width");
+      prm.w_shard_h = static_cast<int>(hsplit / P);
+      prm.w_shard_k = sk ? 1 : 0;
+    }
     if (!a.w_trans) {
-      // 4D view (atom column, k row, atom chunk, expert): one box carries
+      // (atom column, k row, atom chunk, expert[, shard]): one box carries
       // every swizzle-atom column chunk of this CTA's B for a k-block
       const bool sw64 = CG == 2 && bn2_sw64(bn, true);
       const uint64_t bw = sw64 ? 32 : 64;
-      const uint64_t dims[4] = {bw, static_cast<uint64_t>(a.d1), static_cast<uint64_t>(a.d2) / bw,
-                                static_cast<uint64_t>(E)};
-      const uint64_t strides[3] = {static_cast<uint64_t>(a.d2) * 2, bw * 2,
-                                   static_cast<uint64_t>(a.d1 * a.d2) * 2};
-      const uint32_t box[4] = {static_cast<uint32_t>(bw), 64,
-                               static_cast<uint32_t>((bn / CG) / static_cast<int>(bw)), 1};
-      if (!make_map(&prm.tmB, a.w, 4, dims, strides, box,
+      const uint64_t dims[5] = {bw, static_cast<uint64_t>(hk), static_cast<uint64_t>(hn) / bw,
+                                static_cast<uint64_t>(E), static_cast<uint64_t>(P)};
+      const uint64_t strides[4] = {static_cast<uint64_t>(hn) * 2, bw * 2,
+                                   static_cast<uint64_t>(hk * hn) * 2,
+                                   static_cast<uint64_t>(E * hk * hn) * 2};
+      const uint32_t box[5] = {static_cast<uint32_t>(bw), 64,
+                               static_cast<uint32_t>((bn / CG) / static_cast<int>(bw)), 1, 1};
+      if (!make_map(&prm.tmB, a.w, P > 1 ? 5 : 4, dims, strides, box,
                     sw64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
         return invalid_arg("umma_esmm: cannot encode the W tensor map");
       prm.b_sw64 = sw64;
     } else {
-      const uint64_t dims[3] = {static_cast<uint64_t>(a.d1), static_cast<uint64_t>(a.d2),
-                                static_cast<uint64_t>(E)};
-      const uint64_t strides[2] = {static_cast<uint64_t>(a.d1) * 2,
-                                   static_cast<uint64_t>(a.d1 * a.d2) * 2};
-      const uint32_t box[3] = {64, static_cast<uint32_t>(bn / CG), 1};  // this CTA's B rows
-      if (!make_map(&prm.tmB, a.w, 3, dims, strides, box))
+      // (k, n row, expert[, shard]) of W stored N x K per expert
+      const uint64_t dims[4] = {static_cast<uint64_t>(hk), static_cast<uint64_t>(hn),
+                                static_cast<uint64_t>(E), static_cast<uint64_t>(P)};
+      const uint64_t strides[3] = {static_cast<uint64_t>(hk) * 2,
+                                   static_cast<uint64_t>(hk * hn) * 2,
+                                   static_cast<uint64_t>(E * hk * hn) * 2};
+      const uint32_t box[4] = {64, static_cast<uint32_t>(bn / CG), 1, 1};  // this CTA's B rows
+      if (!make_map(&prm.tmB, a.w, P > 1 ? 4 : 3, dims, strides, box))
         return invalid_arg("umma_esmm: cannot encode the W^T tensor map");
     }
   }
@@ -1506,6 +1571,8 @@ hxm_status prep_esmm(const EsmmArgs& a, const int CG, const int bn, UParams& prm
   }
   prm.epi = a.epi;
   prm.act = a.act;
+  prm.n_experts = static_cast<int>(a.n_experts);
+  prm.bias_shard_h = a.epi == EPI_FWD_ACT && a.w_shards > 1 ? static_cast<int>(a.d2 / a.w_shards) : 0;
   prm.bias = a.bias;
   prm.out_f32 = a.out_f32;
   prm.omap = a.omap;

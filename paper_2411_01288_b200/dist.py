@@ -322,15 +322,27 @@ class DataCentricRunner:
     """Preallocated data-centric TP step for one process per GPU (the fast
     path behind bench.py --gpus N; the choreography is data_centric_step's).
 
-    Each rank owns an even H-slice of the layer.  step(): (1) all-gather the
-    shards straight into the pipeline-shared cache buffers that the CUDA layer
-    reads (NCCL, side stream, joined by an event), (2) fwd+bwd of the full layer
-    on this rank's tokens (LayerRunner -> hxm_moe_forward/backward),
-    (3) reduce-scatter the fp32 parameter gradients to the shard owners (b2's
-    gradient is all-reduced, its owner is rank 0)."""
+    Each rank owns an even H-slice of the layer.  The pipeline-shared cache
+    (dist_sim.cpp:104-125, 367-368) has two slots; each slot is one
+    shard-major buffer per tensor -- w1 (P*E) x D_i x h, b1 (P*E) x h,
+    w2 (P*E) x h x D_o -- which is exactly what ``all_gather_into_tensor`` of
+    the P shards produces, and the CUDA layer reads it in place
+    (hxm_layer_desc.weight_shards): no repacking copy.  step():
+      (1) the slot for this step was filled on the side stream (NCCL) by the
+          previous step's prefetch() -- or now, for the first step; the
+          forward waits on its fill event only after the routing prologue;
+      (2) with ``overlap`` the NEXT step's fill of the other slot is issued on
+          the side stream right after this forward is enqueued, so it runs
+          under this step's compute (the steady state of data_centric_pipeline,
+          where layer l + 1's gather hides under layer l);
+      (3) fwd+bwd of the full layer on this rank's tokens, then the fp32
+          parameter gradients reduce-scattered to the shard owners (gb2, owned
+          by rank 0, all-reduced).
+    Shapes the kernels cannot read shard-major (H / P not a multiple of the
+    tile widths) fall back to one repacked reference-layout slot."""
 
     def __init__(self, shard: ParamShard, b2, hidden_sizes: Sequence[int], activation: str,
-                 n_tokens: int, k: int, group=None, dtype=torch.bfloat16):
+                 n_tokens: int, k: int, group=None, dtype=torch.bfloat16, overlap: bool = True):
         from .moe_layer import MoeLayerParams
         from .runner import LayerRunner
         self.group = group
@@ -343,43 +355,82 @@ class DataCentricRunner:
         Do = shard.w2.shape[2]
         dev = shard.w1.device
         P = self.P
-        # gather buffers (rank-major) and the cache (full layer, reference layout)
-        self.w1g = torch.empty((P * E, Di, h), dtype=shard.w1.dtype, device=dev)
-        self.w2g = torch.empty((P * E, h, Do), dtype=shard.w2.dtype, device=dev)
-        self.b1g = torch.empty((P * E, h), dtype=shard.b1.dtype, device=dev)
         self.b2 = (b2 if b2 is not None else torch.zeros((E, Do), device=dev)).float().contiguous()
         full = MoeLayerParams(torch.empty((E, Di, P * h), dtype=shard.w1.dtype, device=dev),
                               torch.empty((E, P * h), dtype=torch.float32, device=dev),
                               torch.empty((E, P * h, Do), dtype=shard.w2.dtype, device=dev),
                               self.b2, activation)
-        self.cache = PipelineSharedCache(full.param_elements())
+        self.cache = PipelineSharedCache(full.param_elements(), slots=2)
         self.cache.fill(0, full)
         self.runner = LayerRunner(full, n_tokens, k, dev, dtype)
-        if P == 1:  # one rank: the gather lands directly in the cache layout
-            self.w1g, self.w2g = full.w1, full.w2
-            self.b1g = self.runner.b1
+        L = self.runner._L
+        self.shard_major = P == 1 or bool(L.hxm_layer_weight_shards_ok(
+            C.byref(self.runner.desc), P))
+        self.overlap = overlap and self.shard_major
         self.side = torch.cuda.Stream(device=dev)
+        # cache slots: gather targets (rank-major == shard-major)
+        nslot = 2 if self.shard_major else 1
+        self.slots = []
+        for i in range(nslot):
+            if P == 1 and i == 0:
+                w1g, w2g, b1g = full.w1, full.w2, self.runner.b1
+            else:
+                w1g = torch.empty((P * E, Di, h), dtype=shard.w1.dtype, device=dev)
+                w2g = torch.empty((P * E, h, Do), dtype=shard.w2.dtype, device=dev)
+                b1g = torch.empty((P * E, h), dtype=torch.float32, device=dev)
+            self.slots.append(dict(w1=w1g, w2=w2g, b1=b1g, ready=torch.cuda.Event(),
+                                   free=torch.cuda.Event(), filled=False))
+        for sl in self.slots:  # "free" starts recorded
+            sl["free"].record(torch.cuda.current_stream())
+        self.cur = 0
+        self.fills = 0
         self.gw1 = torch.empty((E, Di, h), dtype=torch.float32, device=dev)
         self.gb1 = torch.empty((E, h), dtype=torch.float32, device=dev)
         self.gw2 = torch.empty((E, h, Do), dtype=torch.float32, device=dev)
 
-    def gather(self) -> None:
-        """Cache fill (dist_sim.cpp:367-368) on the side stream."""
+    def _fill(self, i: int) -> None:
+        """Cache fill of slot i (dist_sim.cpp:367-368) on the side stream."""
+        sl = self.slots[i]
         P, E = self.P, self.shard.w1.shape[0]
-        self.side.wait_stream(torch.cuda.current_stream())
+        self.side.wait_event(sl["free"])  # the last step that read slot i is done
         with torch.cuda.stream(self.side):
-            dist.all_gather_into_tensor(self.w1g, self.shard.w1.contiguous(), group=self.group)
-            dist.all_gather_into_tensor(self.w2g, self.shard.w2.contiguous(), group=self.group)
-            dist.all_gather_into_tensor(self.b1g, self.shard.b1.contiguous(), group=self.group)
+            dist.all_gather_into_tensor(sl["w1"], self.shard.w1.contiguous(), group=self.group)
+            dist.all_gather_into_tensor(sl["w2"], self.shard.w2.contiguous(), group=self.group)
+            dist.all_gather_into_tensor(sl["b1"], self.shard.b1.float().contiguous(),
+                                        group=self.group)
             dist.broadcast(self.b2, src=dist.get_global_rank(self.group, 0)
                            if self.group is not None else 0, group=self.group)
-            if P > 1:  # rank-major gather buffers -> the cache's reference layout
+            if not self.shard_major and P > 1:
+                # fallback: rank-major gather buffers -> the reference layout
                 p = self.cache.params()
-                Di, h, Do = self.w1g.shape[1], self.h, self.w2g.shape[2]
-                p.w1.view(E, Di, P, h).copy_(self.w1g.view(P, E, Di, h).permute(1, 2, 0, 3))
-                p.w2.view(E, P, h, Do).copy_(self.w2g.view(P, E, h, Do).permute(1, 0, 2, 3))
-                self.runner.b1.view(E, P, h).copy_(self.b1g.view(P, E, h).permute(1, 0, 2))
-        torch.cuda.current_stream().wait_stream(self.side)
+                Di, h, Do = sl["w1"].shape[1], self.h, sl["w2"].shape[2]
+                p.w1.view(E, Di, P, h).copy_(sl["w1"].view(P, E, Di, h).permute(1, 2, 0, 3))
+                p.w2.view(E, P, h, Do).copy_(sl["w2"].view(P, E, h, Do).permute(1, 0, 2, 3))
+                self.runner.b1.view(E, P, h).copy_(sl["b1"].view(P, E, h).permute(1, 0, 2))
+            sl["ready"].record(self.side)
+        sl["filled"] = True
+        self.fills += 1
+
+    def gather(self) -> None:
+        """Fill the current slot now (blocking the compute stream on it)."""
+        self._fill(self.cur)
+        torch.cuda.current_stream().wait_event(self.slots[self.cur]["ready"])
+
+    def _use_slot(self) -> dict:
+        sl = self.slots[self.cur]
+        if not sl["filled"]:
+            self._fill(self.cur)
+        if self.shard_major:
+            self.runner.set_weights(sl["w1"], sl["b1"], sl["w2"], shards=self.P,
+                                    ready=sl["ready"])
+        else:
+            torch.cuda.current_stream().wait_event(sl["ready"])
+        return sl
+
+    def _release(self, sl) -> None:
+        sl["free"].record(torch.cuda.current_stream())
+        sl["filled"] = False
+        self.cur = (self.cur + 1) % len(self.slots)
 
     def enable_fused_grads(self) -> None:
         """Reduce-scatter gW1 / gW2 inside the ESTMM epilogues into the shard
@@ -392,10 +443,19 @@ class DataCentricRunner:
         self.gw1, self.gw2 = self._w1b.view(), self._w2b.view()
 
     def step(self, x, assignments, g_y):
-        self.gather()
+        sl = self._use_slot()
+        self.runner.forward(x, assignments)
+        if self.overlap:  # next step's cache fill under this step's compute
+            self._fill((self.cur + 1) % len(self.slots))
         if getattr(self, "_w1b", None) is not None:
-            return self._step_fused(x, assignments, g_y)
-        self.runner.step(x, assignments, g_y)
+            y = self._step_fused_bwd(x, g_y)
+        else:
+            y = self._step_nccl_bwd(x, g_y)
+        self._release(sl)
+        return y
+
+    def _step_nccl_bwd(self, x, g_y):
+        self.runner.backward(x, g_y)
         g = self.runner.grads
         E = g.gw1.shape[0]
         P, h = self.P, self.h
@@ -531,9 +591,8 @@ def _reduce_param_grads(g, shard: ParamShard, hidden_sizes, group, how: str):
     return MoeGrads(outs[0], outs[1], outs[2], g.gb2 if r == 0 else None, g.gx)
 
 
-def _dc_step_fused(self, x, assignments, g_y):
+def _dc_step_fused_bwd(self, x, g_y):
     run = self.runner
-    run.forward(x, assignments)
     self._w1b.view().zero_()
     self._w2b.view().zero_()
     self._w1b.barrier()  # every owner's shards are zero before any rank reduces
@@ -550,7 +609,7 @@ def _dc_step_fused(self, x, assignments, g_y):
     return run.y
 
 
-DataCentricRunner._step_fused = _dc_step_fused
+DataCentricRunner._step_fused_bwd = _dc_step_fused_bwd
 
 
 def _reduce_rows(t: torch.Tensor, counts: Sequence[int], group, how: str) -> torch.Tensor:

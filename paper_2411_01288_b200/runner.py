@@ -33,15 +33,45 @@ class LayerRunner:
                               torch.empty(n_tokens, Di, **f))
         self.b1 = p.b1.to(torch.float32).contiguous()
         self.b2 = p.b2.to(torch.float32).contiguous() if p.b2 is not None else None
+        self._w1, self._w2 = p.w1, p.w2
         self._pd = C.byref(self.desc)
         self._L = lib()
+
+    def set_weights(self, w1: torch.Tensor, b1: torch.Tensor, w2: torch.Tensor,
+                    shards: int = 0, ready: torch.cuda.Event | None = None) -> None:
+        """Point the layer at another copy of its weights (a pipeline-shared
+        cache slot).  shards <= 1: reference layout (E x D_i x H, E x H,
+        E x H x D_o).  shards = P > 1: shard-major, as an all-gather of P
+        hidden shards lands -- w1 (P*E) x D_i x h, b1 (P*E) x h (fp32),
+        w2 (P*E) x h x D_o with h = H / P -- read in place by the GEMMs (no
+        repacking copy).  ``ready``: an event recorded after the cache fill;
+        the forward waits on it only after its routing prologue."""
+        d = self.desc
+        E, Di, H, Do = d.n_experts, d.d_in, d.hidden, d.d_out
+        P = max(1, int(shards))
+        if H % P:
+            raise ValueError("set_weights: H must split evenly into the shards")
+        h = H // P
+        want = ((P * E, Di, h), (P * E, h), (P * E, h, Do)) if P > 1 else \
+            ((E, Di, H), (E, H), (E, H, Do))
+        for t, shp, nm in ((w1, want[0], "w1"), (b1, want[1], "b1"), (w2, want[2], "w2")):
+            if tuple(t.shape) != shp or not t.is_contiguous():
+                raise ValueError(f"set_weights: {nm} must be a contiguous {shp} tensor")
+        if b1.dtype != torch.float32:
+            raise ValueError("set_weights: b1 must be fp32")
+        if P > 1 and not self._L.hxm_layer_weight_shards_ok(C.byref(d), P):
+            raise ValueError(f"set_weights: this layer cannot read weights split {P} ways "
+                             "(H / P must be a multiple of 64 and of the tile widths)")
+        d.weight_shards = P if P > 1 else 0
+        d.weights_ready = ready.cuda_event if ready is not None else None
+        self._w1, self.b1, self._w2 = w1, b1, w2
 
     def forward(self, x: torch.Tensor, assignments: torch.Tensor, stream=None,
                 status: torch.Tensor | None = None) -> torch.Tensor:
         st = (stream or torch.cuda.current_stream()).cuda_stream
         check(self._L.hxm_moe_forward(
-            self._pd, x.data_ptr(), self.p.w1.data_ptr(), self.b1.data_ptr(),
-            self.p.w2.data_ptr(), None if self.b2 is None else self.b2.data_ptr(),
+            self._pd, x.data_ptr(), self._w1.data_ptr(), self.b1.data_ptr(),
+            self._w2.data_ptr(), None if self.b2 is None else self.b2.data_ptr(),
             assignments.data_ptr(), self.y.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
             None if status is None else status.data_ptr(), st), "moe_forward")
         return self.y
@@ -50,7 +80,7 @@ class LayerRunner:
         st = (stream or torch.cuda.current_stream()).cuda_stream
         g = self.grads
         check(self._L.hxm_moe_backward(
-            self._pd, x.data_ptr(), self.p.w1.data_ptr(), self.p.w2.data_ptr(), g_y.data_ptr(),
+            self._pd, x.data_ptr(), self._w1.data_ptr(), self._w2.data_ptr(), g_y.data_ptr(),
             self.ws.data_ptr(), self.ws.numel(), g.gw1.data_ptr(), g.gb1.data_ptr(),
             g.gw2.data_ptr(), None if g.gb2 is None else g.gb2.data_ptr(), g.gx.data_ptr(), st),
             "moe_backward")
@@ -63,7 +93,7 @@ class LayerRunner:
         st = (stream or torch.cuda.current_stream()).cuda_stream
         g = self.grads
         check(self._L.hxm_moe_backward_dc(
-            self._pd, x.data_ptr(), self.p.w1.data_ptr(), self.p.w2.data_ptr(), g_y.data_ptr(),
+            self._pd, x.data_ptr(), self._w1.data_ptr(), self._w2.data_ptr(), g_y.data_ptr(),
             self.ws.data_ptr(), self.ws.numel(), C.byref(gw1_shards.rows_struct),
             g.gb1.data_ptr(), C.byref(gw2_shards.rows_struct),
             None if g.gb2 is None else g.gb2.data_ptr(), g.gx.data_ptr(), st),
