@@ -320,6 +320,46 @@ hxm_status hxm_moe_backward_dc(const hxm_layer_desc* desc, const void* x,
                                const hxm_peer_rows* gw2_shards, float* gb2,
                                float* gx, hxm_stream_t stream);
 
+/* ------------------------------------------------------------------------
+ * Tensor-parallel collectives over NCCL (the reference simulates them
+ * in-process, dist_sim.cpp:127-176).  `comm` is an ncclComm_t (void*): one
+ * the host created itself, or hxm_nccl_comm_init's.  NCCL is loaded at run
+ * time; without it these return HXM_ERR_NCCL.  All run on `stream`.
+ * ---------------------------------------------------------------------- */
+hxm_status hxm_nccl_get_unique_id(unsigned char id[128]);
+hxm_status hxm_nccl_comm_init(void** comm, int32_t n_ranks, const unsigned char id[128],
+                              int32_t rank);
+hxm_status hxm_nccl_comm_destroy(void* comm);
+
+/* Data-centric (run_data_centric, dist_sim.cpp:352-452).  The cache is one
+ * buffer of hxm_dc_cache_bytes(desc) holding the whole layer shard-major
+ * (desc: the FULL layer, H = P * h); hxm_dc_cache_views gives the w1 / b1 /
+ * w2 pointers to pass to hxm_moe_forward / hxm_moe_backward(_dc) with
+ * desc.weight_shards = P.  hxm_dc_fill_cache all-gathers this rank's shards
+ * (w1 E x D_i x h, b1 fp32 E x h, w2 E x h x D_o) into it
+ * (PipelineSharedCache::fill, dist_sim.cpp:367-368); HXM_ERR_CACHE when
+ * cache_bytes is too small (CacheError, dist_sim.cpp:104-125).
+ * hxm_dc_allreduce_grads sums the parameter gradients over the ranks in
+ * place (dist_sim.cpp:397-399; gb2 may be NULL). */
+size_t hxm_dc_cache_bytes(const hxm_layer_desc* desc);
+hxm_status hxm_dc_cache_views(const hxm_layer_desc* desc, void* cache, void** w1,
+                              float** b1, void** w2);
+hxm_status hxm_dc_fill_cache(void* comm, const hxm_layer_desc* desc, const void* w1_shard,
+                             const float* b1_shard, const void* w2_shard, void* cache,
+                             size_t cache_bytes, hxm_stream_t stream);
+hxm_status hxm_dc_allreduce_grads(void* comm, const hxm_layer_desc* desc, float* gw1,
+                                  float* gb1, float* gw2, float* gb2, hxm_stream_t stream);
+
+/* Model-centric (run_model_centric, dist_sim.cpp:454-601): all_gather_rows
+ * of equal per-rank row counts (x, g_y: any dtype, row_bytes each) and of
+ * the k x n_local routing (out k x P*n_local, choice-major as
+ * RoutingChoice); all_reduce_sum (fp32, in place) of the partial y / g_x. */
+hxm_status hxm_tp_allgather_rows(void* comm, const void* local, int64_t rows_per_rank,
+                                 int64_t row_bytes, void* out, hxm_stream_t stream);
+hxm_status hxm_tp_allgather_assignments(void* comm, const int32_t* local, int64_t k,
+                                        int64_t n_local, int32_t* out, hxm_stream_t stream);
+hxm_status hxm_tp_allreduce_sum(void* comm, float* buf, int64_t n_elems, hxm_stream_t stream);
+
 /* Peer-shareable device memory and its IPC handles (64 bytes). */
 hxm_status hxm_peer_malloc(size_t bytes, void** ptr);
 hxm_status hxm_peer_free(void* ptr);

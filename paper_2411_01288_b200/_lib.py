@@ -28,6 +28,10 @@ class CacheError(RuntimeError):
     """moekit::CacheError (reference core/include/moekit/dist_sim.hpp:55-58)."""
 
 
+class NcclError(RuntimeError):
+    """HXM_ERR_NCCL: an NCCL collective of the C ABI failed (or NCCL is absent)."""
+
+
 class HexaMoeCudaError(RuntimeError):
     pass
 
@@ -87,6 +91,16 @@ SIGNATURES = {
     "hxm_layer_forward_macs": (C.c_uint64, [C.POINTER(LayerDesc)]),
     "hxm_layer_path": (C.c_int, [C.POINTER(LayerDesc)]),
     "hxm_layer_weight_shards_ok": (C.c_int, [C.POINTER(LayerDesc), C.c_int32]),
+    "hxm_nccl_get_unique_id": (C.c_int, [_p]),
+    "hxm_nccl_comm_init": (C.c_int, [_p, C.c_int32, _p, C.c_int32]),
+    "hxm_nccl_comm_destroy": (C.c_int, [_p]),
+    "hxm_dc_cache_bytes": (_sz, [C.POINTER(LayerDesc)]),
+    "hxm_dc_cache_views": (C.c_int, [C.POINTER(LayerDesc), _p, _p, _p, _p]),
+    "hxm_dc_fill_cache": (C.c_int, [_p, C.POINTER(LayerDesc), _p, _p, _p, _p, _sz, _p]),
+    "hxm_dc_allreduce_grads": (C.c_int, [_p, C.POINTER(LayerDesc), _p, _p, _p, _p, _p]),
+    "hxm_tp_allgather_rows": (C.c_int, [_p, _p, _i64, _i64, _p, _p]),
+    "hxm_tp_allgather_assignments": (C.c_int, [_p, _p, _i64, _i64, _p, _p]),
+    "hxm_tp_allreduce_sum": (C.c_int, [_p, _p, _i64, _p]),
     "hxm_op_stats_add": (None, [C.c_int, _i64, _i64, _i64, _i64, _p]),
     "hxm_synthesize_routing": (C.c_int, [_i64, _i64, _i64, C.c_char_p, C.c_uint64, _p]),
     "hxm_make_layer_inputs": (None, [C.c_uint64, _i64, _i64, _i64, _i64, _i64, C.c_double, _p,
@@ -164,4 +178,6 @@ def check(status: int, what: str = "") -> None:
         raise ValueError(msg)
     if status == HXM_ERR_CACHE:
         raise CacheError(msg)
+    if status == HXM_ERR_NCCL:
+        raise NcclError(msg)
     raise HexaMoeCudaError(f"[status {status}] {msg}")

@@ -80,7 +80,7 @@ def build(verbose: bool = False, extra=()) -> str:
         # is reached through cudaGetDriverEntryPoint, so the library loads on
         # a machine without libcuda (the CPU build container).
         cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
-               "-o", LIB, *objs]
+               "-o", LIB, *objs, "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

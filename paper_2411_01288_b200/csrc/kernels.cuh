@@ -169,6 +169,10 @@ hxm_status simt_estmm(hxm_dtype dt, const EstmmArgs& a, cudaStream_t st);
 // do not cover (d1/d2 not multiples of 64), which the caller reports.
 hxm_status umma_esmm(const EsmmArgs& a, cudaStream_t st);
 hxm_status umma_estmm(const EstmmArgs& a, cudaStream_t st);
+// 256 x 384 whole-tile CTA-pair reduction GEMM (umma_wide.cu): EPI_ATOMIC,
+// dense A, 256-row tiles, d2 == 384 (HXM_WIDE=0 disables)
+bool umma_wide_ok(const EsmmArgs& a);
+hxm_status umma_wide_esmm(const EsmmArgs& a, cudaStream_t st);
 bool umma_supports_esmm(int64_t d1, int64_t d2);
 bool umma_supports_estmm(int64_t d1, int64_t d2);
 // CTA-pair ESMM (dense A, 256-row tiles): BN must split into whole B halves

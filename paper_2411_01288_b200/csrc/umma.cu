@@ -33,6 +33,8 @@ bool umma2_supports_esmm(int64_t d1, int64_t d2, bool w_trans) {
 
 hxm_status umma_esmm(const EsmmArgs& a, cudaStream_t st) {
   if (a.max_tiles <= 0) return HXM_OK;
+  // 384-wide reduction GEMMs (c2's fwd2 / gx): whole-tile CTA pairs
+  if (umma_wide_ok(a)) return umma_wide_esmm(a, st);
   const int CG = a.tile_rows == kUmma2Rows ? 2 : 1;
   if (a.tile_rows != kUmmaRows && CG == 1)
     return invalid_arg("umma_esmm: tiles must have 128 (or 256) rows");

@@ -472,6 +472,7 @@ struct UParams {
   int w_shard_h;
   int w_shard_k;
   int bias_shard_h;  // MODE 1: b1 is [P][E][h] (0: E x N)
+  int stream_k;      // MODE 0, reduction epilogue: equal k-block ranges per cluster
   int n_experts;
   int l2hint;  // MODE 1/2: L2 eviction-priority hints on the stash stores
   int reverse; // walk the work items last to first
@@ -633,6 +634,39 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
   // p.reverse: walk the items last to first, so a kernel that consumes the
   // previous kernel's output starts on the rows written last (L2-resident)
   auto wmap = [&](int wl) { return p.reverse ? total - 1 - wl : wl; };
+  // Work units of this cluster: (work item wl, k-blocks [lo, hi)).  Default:
+  // whole items wl = cluster, cluster + n_clusters, ... (round-robin: the
+  // pairs that work on the two N-tiles of an M-tile run side by side and
+  // share its A rows' HBM reads in L2).  Stream-K tail (MODE 0 with a
+  // reduction epilogue, p.stream_k): the full waves stay round-robin, the
+  // items of the last partial wave are flattened into (item, k-block) space
+  // and cut into n_clusters equal contiguous ranges, so no cluster idles
+  // through a partial wave; a tail item cut between two clusters is reduced
+  // twice (red.add), its bias added by the part holding k-block 0.
+  // hi = -1: the item's own length (ESTMM chunks).
+  struct Unit {
+    int wl, lo, hi;
+    bool ok;
+  };
+  const int nk_all = ESTMM ? 1 : p.K / BK;  // (stream_k is never set for ESTMM)
+  const int full_waves = p.stream_k ? total / n_clusters : 0;
+  const int tail0 = full_waves * n_clusters;  // first tail item
+  const long long tail_kb = p.stream_k ? static_cast<long long>(total - tail0) * nk_all : 0;
+  const int sk_g0 = static_cast<int>(tail_kb * cluster / n_clusters);
+  const int sk_g1 = static_cast<int>(tail_kb * (cluster + 1) / n_clusters);
+  auto unit_at = [&](int i) -> Unit {
+    if (!p.stream_k) {
+      const int wl = cluster + i * n_clusters;
+      return Unit{wl, 0, ESTMM ? -1 : nk_all, wl < total};
+    }
+    if (i < full_waves) return Unit{cluster + i * n_clusters, 0, nk_all, true};
+    const int j = i - full_waves;
+    const int it = sk_g0 / nk_all + j;  // tail-relative item
+    const int lo = j == 0 ? sk_g0 % nk_all : 0;
+    const int base = it * nk_all;
+    const int hi = sk_g1 - base < nk_all ? sk_g1 - base : nk_all;
+    return Unit{tail0 + it, lo, hi, base + lo < sk_g1};
+  };
 
   if (warp == 0) {
     // ================================ TMA producer =======================
@@ -643,13 +677,15 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
     int s = 0;
     uint32_t ph = 0;
     int pit_ = 0;
-    for (int wl = cluster; wl < total; wl += n_clusters, ++pit_) {
-      const int w = wmap(wl);
+    for (int ui = 0;; ++ui, ++pit_) {
+      const Unit u = unit_at(ui);
+      if (!u.ok) break;
+      const int w = wmap(u.wl);
       const SegTile t = p.tiles[w / per_item];
       const int rem = w % per_item;
       if (!ESTMM) {
         const int n0 = rem * BN;
-        const int nk = p.K / BK;
+        const int nk = u.hi;
         int rows[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -657,7 +693,7 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
           rows[i] = (p.a_gather && q < t.end) ? p.amap(q) : -1;
         }
         unsigned long long pw = 0;
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = u.lo; kb < nk; ++kb) {
           const long long tp0 = (kTrace && p.trace) ? clock64() : 0;
           mbar_wait(&empty[s], ph ^ 1);
           if (kTrace && p.trace) pw += clock64() - tp0;
@@ -796,10 +832,12 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
       int s = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
       int it_ = 0;
-      for (int wl = cluster; wl < total; wl += n_clusters, ++it_) {
-        const int w = wmap(wl);
+      for (int ui = 0;; ++ui, ++it_) {
+        const Unit u = unit_at(ui);
+        if (!u.ok) break;
+        const int w = wmap(u.wl);
         const int nk = ESTMM ? (p.tiles[w / per_item].end - p.tiles[w / per_item].begin + BK - 1) / BK
-                             : p.K / BK;
+                             : u.hi;
         if (lane == 0) TRACE(it_, 0);
         if constexpr (CG == 2) mbar_wait_cl(&tempty[acc], aph ^ 1);
         else mbar_wait(&tempty[acc], aph ^ 1);
@@ -807,7 +845,7 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
         unsigned long long wsum = 0;
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = u.lo; kb < nk; ++kb) {
           const long long tw0 = (kTrace && p.trace) ? clock64() : 0;
           if constexpr (CG == 2) mbar_wait_cl(&full[s], ph);
           else mbar_wait(&full[s], ph);
@@ -815,7 +853,7 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
           tc_fence_after();
           const uint32_t so = static_cast<uint32_t>(s) * kStageUnits;
           if (elect_one())
-            umma_kblock<CG>(d, a_lo + so, a_hi, a_step, b_lo + so, b_hi, b_step, idesc, kb == 0,
+            umma_kblock<CG>(d, a_lo + so, a_hi, a_step, b_lo + so, b_hi, b_step, idesc, kb == u.lo,
                             &empty[s], skip);
           __syncwarp();
           if (++s == C::kStages) { s = 0; ph ^= 1; }
@@ -878,7 +916,8 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
       return p.omap(qq);
     };
     int ep_it = 0;
-    SegTile t_cur = ESTMM || cluster >= total ? SegTile{0, 0, 0, 0} : tile_at(wmap(cluster));
+    const Unit u0 = unit_at(0);
+    SegTile t_cur = ESTMM || !u0.ok ? SegTile{0, 0, 0, 0} : tile_at(wmap(u0.wl));
     int orow_cur = ESTMM ? -1 : orow_of(t_cur);
     // MODE 1 bias: the column group's HB bias floats of the current item sit
     // in smem; lane l < HB / 4 of lane-group warp lg owns entry lg * HB / 4 + l,
@@ -895,15 +934,18 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
                                      : (static_cast<int64_t>(col / hb) * p.n_experts + tt.expert) *
                                                hb + col % hb));
     };
-    if (bias_smem && lane < kBq && cluster < total) gbias[lg * kBq + lane] = bias_at(t_cur, wmap(cluster));
+    if (bias_smem && lane < kBq && u0.ok) gbias[lg * kBq + lane] = bias_at(t_cur, wmap(u0.wl));
     int y_iss = 0;  // MODE 2 (elected thread): global F'(y1) chunks issued so far
-    for (int wl = cluster; wl < total; wl += n_clusters) {
-      const int w = wmap(wl);
+    for (int ui = 0;; ++ui) {
+      const Unit u = unit_at(ui);
+      if (!u.ok) break;
+      const int w = wmap(u.wl);
       const SegTile t = ESTMM ? p.tiles[w / per_item] : t_cur;
       const int rem = w % per_item;
       if (!ESTMM) {
-        const bool has_nx = wl + n_clusters < total;
-        const int w_nx = has_nx ? wmap(wl + n_clusters) : 0;
+        const Unit u_nx = unit_at(ui + 1);
+        const bool has_nx = u_nx.ok;
+        const int w_nx = has_nx ? wmap(u_nx.wl) : 0;
         const SegTile t_nx = has_nx ? tile_at(w_nx) : SegTile{0, 0, 0, 0};  // prefetch
         int orow_nx = -1;
         float bias_nx = 0.f;  // loaded during the last chunk (short register lifetime)
@@ -939,7 +981,7 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
         // MODE 0 bias of this warp's HB columns: every lane reads the same 32
         // floats per chunk (uniform-address LDG.128, one broadcast transaction
         // each, L1-resident) and adds them in f32x2 (MODE 1: from smem, below)
-        const bool has_bias = p.bias && !bwd && !dense_out;
+        const bool has_bias = p.bias && !bwd && !dense_out && u.lo == 0;  // stream-K: once
         const float4* bias4 =
             has_bias ? reinterpret_cast<const float4*>(p.bias + static_cast<int64_t>(t.expert) * N + n0)
                      : nullptr;
@@ -1572,6 +1614,18 @@ hxm_status prep_esmm(const EsmmArgs& a, const int CG, const int bn, UParams& prm
   prm.epi = a.epi;
   prm.act = a.act;
   prm.n_experts = static_cast<int>(a.n_experts);
+  {
+    // stream-K tail for the reduction epilogue (fwd2 / gx), HXM_STREAMK=1:
+    // off by default -- a split tail item adds a third fp32 partial to its y /
+    // g_x rows, so with k = 2 the result would no longer be bit-reproducible
+    // (two addends onto zero commute exactly), and the measured gain is small
+    // (profiles/r2_notes.md)
+    static const bool sk = [] {
+      const char* e = std::getenv("HXM_STREAMK");
+      return e && e[0] == '1';
+    }();
+    prm.stream_k = (sk && a.epi == EPI_ATOMIC) ? 1 : 0;
+  }
   prm.bias_shard_h = a.epi == EPI_FWD_ACT && a.w_shards > 1 ? static_cast<int>(a.d2 / a.w_shards) : 0;
   prm.bias = a.bias;
   prm.out_f32 = a.out_f32;

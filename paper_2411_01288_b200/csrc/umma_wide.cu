@@ -1,0 +1,366 @@
+// umma_wide.cu -- the K = H reduction GEMMs of the layer (ESMM fwd2:
+// y += F(y1) W2 + b2, and ESMM gx: g_x += g_y1 W1^T; es_ops.cpp:47-81 in
+// accumulate mode over the k choices) on CTA pairs that own the WHOLE
+// 256 x 384 output tile when the output width is 384 (c2's D).
+//
+// Why: with 256 x 192 tiles (umma.cu) every A row block (the H-wide stash)
+// is streamed from L2 twice, once per N-half, and the kernels sit at the L2
+// throughput cap with the operand ring starved (profiles/r1b_notes.md 4, 15,
+// 23; the LTS cap is path-independent, B300_MICROARCH.md).  One pair per
+// 256 x 384 tile reads A once: per 64-deep k-block a CTA loads 16 KB of A +
+// 24 KB of B for two MMAs (N = 256 and N = 128, both cta_group::2) instead
+// of 2 x (16 + 12) KB -- 29 % fewer L2 bytes per FLOP.
+//
+// TMEM: the tile needs 384 accumulator columns, so the accumulator cannot be
+// double-buffered whole.  It is split: the N = 256 part always lives in
+// columns [0, 256), the N = 128 part alternates between [256, 384) and
+// [384, 512).  The epilogue drains the 256-column part first and releases
+// it, so the next tile's MMAs start while the epilogue still drains the
+// 128-column part of the previous one.
+//
+// Column mapping: CTA r loads B columns [192 r, 192 r + 192) as one box;
+// MMA1 (N = 256) covers CTA0's first 128 and CTA1's first 128 columns, MMA2
+// (N = 128) the last 64 of each.  Epilogue column group g (4 warps, one per
+// TMEM lane group) drains lo columns [128 g, 128 g + 128) and hi columns
+// [64 g, 64 g + 64), i.e. exactly the global columns [192 g, 192 g + 192).
+#include "umma_impl.cuh"
+
+namespace hxm {
+namespace {
+
+constexpr int kWideN = 384;                       // output columns per tile
+constexpr int kWideBHalf = kWideN / 2;            // B columns per CTA
+constexpr int kWideBBytes = kWideBHalf * BK * 2;  // 24 KB
+constexpr int kWideStage = kABytes + kWideBBytes; // 40 KB
+constexpr int kWideEW = 8;                        // epilogue warps per CTA
+constexpr int kWideStaging = kWideEW * 2048;
+constexpr int kWideStages = (232448 - 1024 - 256 - kWideStaging) / kWideStage;  // 5
+constexpr int kWideSmem = kWideStages * kWideStage + kWideStaging + 1024 + 256;
+constexpr int kWideThreads = 64 + 32 * kWideEW;
+
+// One 64-deep k-block of the wide tile: four K = 16 steps of MMA1 (N = 256,
+// accumulator d_lo) and MMA2 (N = 128, accumulator d_hi), then the commit
+// that frees the stage (multicast to both CTAs of the pair).
+__device__ __forceinline__ void wide_kblock(uint32_t d_lo, uint32_t d_hi, uint32_t a_lo,
+                                            uint32_t a_hi, uint32_t a_step, uint32_t b_lo,
+                                            uint32_t b_hi, uint32_t b_step, uint32_t b2_off,
+                                            uint32_t idesc1, uint32_t idesc2, uint32_t first,
+                                            uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p0, p1;\n"
+      ".reg .b64 da, db, db2;\n"
+      ".reg .b32 al, bl, b2l;\n"
+      "setp.ne.b32 p0, %11, 0;\n"
+      "setp.eq.b32 p1, %11, %11;\n"
+      "mov.b32 al, %2;\n"
+      "mov.b32 bl, %5;\n"
+      "add.u32 b2l, %5, %8;\n"
+      "mov.b64 da, {al, %3};\n"
+      "mov.b64 db, {bl, %6};\n"
+      "mov.b64 db2, {b2l, %6};\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %9, p0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%1], da, db2, %10, p0;\n"
+      "add.u32 al, al, %4;\n"
+      "add.u32 bl, bl, %7;\n"
+      "add.u32 b2l, b2l, %7;\n"
+      "mov.b64 da, {al, %3};\n"
+      "mov.b64 db, {bl, %6};\n"
+      "mov.b64 db2, {b2l, %6};\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %9, p1;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%1], da, db2, %10, p1;\n"
+      "add.u32 al, al, %4;\n"
+      "add.u32 bl, bl, %7;\n"
+      "add.u32 b2l, b2l, %7;\n"
+      "mov.b64 da, {al, %3};\n"
+      "mov.b64 db, {bl, %6};\n"
+      "mov.b64 db2, {b2l, %6};\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %9, p1;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%1], da, db2, %10, p1;\n"
+      "add.u32 al, al, %4;\n"
+      "add.u32 bl, bl, %7;\n"
+      "add.u32 b2l, b2l, %7;\n"
+      "mov.b64 da, {al, %3};\n"
+      "mov.b64 db, {bl, %6};\n"
+      "mov.b64 db2, {b2l, %6};\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %9, p1;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%1], da, db2, %10, p1;\n"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%12], %13;\n"
+      "}\n" ::"r"(d_lo),
+      "r"(d_hi), "r"(a_lo), "r"(a_hi), "r"(a_step), "r"(b_lo), "r"(b_hi), "r"(b_step),
+      "r"(b2_off), "r"(idesc1), "r"(idesc2), "r"(first ? 0u : 1u), "r"(smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kWideThreads, 1)
+    umma_wide_kernel(const __grid_constant__ UParams p) {
+  constexpr int CG = 2;
+  uint32_t rank = 0;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int cluster = blockIdx.x / CG, n_clusters = gridDim.x / CG;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* staging = smem + kWideStages * kWideStage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + kWideStaging);
+  uint64_t* empty = full + kWideStages;
+  uint64_t* tfull = empty + kWideStages;   // [2] by tile parity
+  uint64_t* tempty_lo = tfull + 2;         // [1] the N = 256 accumulator
+  uint64_t* tempty_hi = tempty_lo + 1;     // [2] the two N = 128 slots
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_hi + 2);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kWideStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty_hi[a], kWideEW * CG);
+    }
+    mbar_init(tempty_lo, kWideEW * CG);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t full_lead = mapa0(smem_u32(full));
+  const uint32_t tlo_lead = mapa0(smem_u32(tempty_lo));
+  const uint32_t thi_lead = mapa0(smem_u32(tempty_hi));
+
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int total = *p.n_tiles;  // one work item per 256-row tile (N = 384 whole)
+  auto wmap = [&](int wl) { return p.reverse ? total - 1 - wl : wl; };
+  const int nk = p.K / BK;
+
+  if (warp == 0) {
+    // ================================ TMA producer =======================
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&p.tmA) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&p.tmB) : "memory");
+    }
+    int s = 0;
+    uint32_t ph = 0;
+    for (int wl = cluster; wl < total; wl += n_clusters) {
+      const SegTile t = p.tiles[wmap(wl)];
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* sa = smem + s * kWideStage;
+        uint8_t* sb = sa + kABytes;
+        if (elect_one()) {
+          const uint32_t fb = full_lead + 8u * s;
+          if (rank == 0) mbar_arrive_tx(&full[s], 2 * kWideStage);
+          tma_2d_cg2(sa, &p.tmA, fb, kb * BK, t.begin + static_cast<int>(rank) * BM);
+          load_w_box<2>(p, sb, nullptr, fb, kb * BK, static_cast<int>(rank) * kWideBHalf,
+                        t.expert);
+        }
+        __syncwarp();
+        if (++s == kWideStages) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ================================ MMA issuer ==========================
+    if (rank == 0) {
+      const bool b_mn = !p.b_kmajor;
+      const uint32_t idesc1 = idesc_bf16(256, 0, b_mn ? 1 : 0, BM * CG);
+      const uint32_t idesc2 = idesc_bf16(128, 0, b_mn ? 1 : 0, BM * CG);
+      const uint32_t base = smem_u32(smem);
+      const uint64_t da0 = sdesc(base, 16, 1024);
+      const uint64_t db0 = b_mn ? sdesc(base + kABytes, 8192, 1024) : sdesc(base + kABytes, 16, 1024);
+      const uint32_t a_lo = static_cast<uint32_t>(da0), a_hi = static_cast<uint32_t>(da0 >> 32);
+      const uint32_t b_lo = static_cast<uint32_t>(db0), b_hi = static_cast<uint32_t>(db0 >> 32);
+      const uint32_t a_step = 2u, b_step = b_mn ? 128u : 2u;
+      // MMA2's B: the CTA's last 64 columns (MN-major: the third 8 KB atom
+      // column chunk) or rows 128..191 (K-major): 16 KB in, in 16-B units
+      const uint32_t b2_off = 16384u >> 4;
+      constexpr uint32_t kStageUnits = kWideStage >> 4;
+      int s = 0, it = 0;
+      uint32_t ph = 0, lo_ph = 0, hi_ph[2] = {0, 0};
+      for (int wl = cluster; wl < total; wl += n_clusters, ++it) {
+        const int hs = it & 1;
+        mbar_wait(tempty_lo, lo_ph ^ 1);
+        mbar_wait(&tempty_hi[hs], hi_ph[hs] ^ 1);
+        lo_ph ^= 1;
+        hi_ph[hs] ^= 1;
+        tc_fence_after();
+        const uint32_t d_lo = tmem, d_hi = tmem + 256 + 128 * hs;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t so = static_cast<uint32_t>(s) * kStageUnits;
+          if (elect_one())
+            wide_kblock(d_lo, d_hi, a_lo + so, a_hi, a_step, b_lo + so, b_hi, b_step, b2_off,
+                        idesc1, idesc2, kb == 0, &empty[s]);
+          __syncwarp();
+          if (++s == kWideStages) { s = 0; ph ^= 1; }
+        }
+        if (elect_one()) umma_commit_cg2(&tfull[it & 1]);
+        __syncwarp();
+      }
+    }
+    __syncwarp();
+  } else {
+    // ================================ epilogue ============================
+    const int lg = warp & 3;
+    const int g = (warp - 2) / 4;  // column group: global columns [192 g, 192 g + 192)
+    uint8_t* stg = staging + (warp - 2) * 2048;
+    const int N = p.N;
+    uint32_t tf_ph[2] = {0, 0};
+    int it = 0;
+    for (int wl = cluster; wl < total; wl += n_clusters, ++it) {
+      const int w = wmap(wl);
+      const SegTile t = p.tiles[w];
+      const int hs = it & 1;
+      // this lane's token-order output row
+      int orow = -1;
+      {
+        const int qq = t.begin + static_cast<int>(rank) * BM + lg * 32 + lane;
+        if (qq < t.end) orow = p.omap(qq);
+      }
+      const float* bias = p.bias ? p.bias + static_cast<int64_t>(t.expert) * N : nullptr;
+      mbar_wait(&tfull[it & 1], tf_ph[it & 1]);
+      tf_ph[it & 1] ^= 1;
+      tc_fence_after();
+      const uint32_t lane_base = tmem + (static_cast<uint32_t>(lg * 32) << 16);
+      // one 32-column chunk (TMEM registers r) -> bias -> fp32 rows scattered
+      // to token order through the per-warp swizzled staging tile (8 row
+      // segments of 64 B per reduction instruction)
+      auto emit = [&](const uint32_t (&r)[32], const int gcol) {
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        if (bias) {
+          const float4* b4 = reinterpret_cast<const float4*>(bias + gcol);
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 b = __ldg(b4 + i / 4);
+            v[i] += b.x; v[i + 1] += b.y; v[i + 2] += b.z; v[i + 3] += b.w;
+          }
+        }
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<float4*>(stg + lane * 64 + ((j ^ ((lane >> 1) & 3)) * 16)) =
+                make_float4(v[16 * h2 + 4 * j], v[16 * h2 + 4 * j + 1], v[16 * h2 + 4 * j + 2],
+                            v[16 * h2 + 4 * j + 3]);
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int rr = i * 8 + lane / 4, cc = lane % 4;
+            const int orr = __shfl_sync(0xffffffffu, orow, rr);
+            const float4 val =
+                *reinterpret_cast<const float4*>(stg + rr * 64 + ((cc ^ ((rr >> 1) & 3)) * 16));
+            if (orr < 0) continue;
+            const int n = gcol + 16 * h2 + cc * 4;
+            if (p.n_peer > 0) {
+              const int owner = static_cast<int>(orr / p.peer_rows);
+              float* o = p.peer[owner] + (orr - owner * p.peer_rows) * N + n;
+              red_add_v4_sys(o, val.x, val.y, val.z, val.w);
+            } else {
+              red_add_v4(p.out_f32 + static_cast<int64_t>(orr) * N + n, val.x, val.y, val.z,
+                         val.w);
+            }
+          }
+        }
+      };
+      // the lo accumulator (4 chunks) is loaded into registers at once and
+      // released before any of it is reduced, so the next tile's MMAs start
+      // after ~4 TMEM loads instead of after the whole lo epilogue
+      {
+        uint32_t rl[4][32];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld32_async(lane_base + 128 * g + 32 * c, rl[c]);
+        tmem_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cl(tlo_lead);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) emit(rl[c], 192 * g + 32 * c);
+      }
+      {
+        uint32_t rh[2][32];
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          tmem_ld32_async(lane_base + 256 + 128 * hs + 64 * g + 32 * c, rh[c]);
+        tmem_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cl(thi_lead + 8u * hs);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) emit(rh[c], 192 * g + 128 + 32 * c);
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (threadIdx.x == 0 && p.n_peer > 0) asm volatile("fence.sc.sys;" ::: "memory");
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(kTmemCols));
+  }
+}
+
+}  // namespace
+
+bool umma_wide_ok(const EsmmArgs& a) {
+  static const bool on = [] {
+    const char* e = std::getenv("HXM_WIDE");
+    return !(e && e[0] == '0');
+  }();
+  return on && a.epi == EPI_ATOMIC && a.tile_rows == kUmma2Rows && a.d2 == kWideN &&
+         a.amap.kind == MAP_DENSE && a.d1 % BK == 0;
+}
+
+hxm_status umma_wide_esmm(const EsmmArgs& a, cudaStream_t st) {
+  if (a.max_tiles <= 0) return HXM_OK;
+  UParams prm{};
+  HXM_RETURN_IF(prep_esmm(a, 2, kWideN, prm));
+  prm.stream_k = 0;
+  static bool attr_set[64] = {false};
+  int dev = 0;
+  HXM_TRY_CUDA(cudaGetDevice(&dev));
+  dev = dev < 64 ? dev : 63;
+  if (!attr_set[dev]) {
+    HXM_TRY_CUDA(cudaFuncSetAttribute(umma_wide_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kWideSmem));
+    attr_set[dev] = true;
+  }
+  const int sms = sm_count();
+  if (sms <= 0) return invalid_arg("tcgen05 path: no CUDA device");
+  const int grid = std::max(1, std::min(sms / 2, a.max_tiles)) * 2;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kWideThreads);
+  cfg.dynamicSmemBytes = kWideSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl_on()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  attr[na].id = cudaLaunchAttributeClusterDimension;
+  attr[na].val.clusterDim.x = 2;
+  attr[na].val.clusterDim.y = 1;
+  attr[na].val.clusterDim.z = 1;
+  ++na;
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  HXM_TRY_CUDA(cudaLaunchKernelEx(&cfg, umma_wide_kernel, prm));
+  HXM_CHECK_LAUNCH();
+  return HXM_OK;
+}
+
+}  // namespace hxm

@@ -1,4 +1,4 @@
-# gpu tests (all, no -x) + smoke
 set -x
 timeout 2400 python -m pytest tests -m gpu -q -rf --timeout 1800 > gpurun_out/pytest_gpu.log 2>&1
 echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
