@@ -8,6 +8,7 @@
 //   ess_partial : one CTA per <=128-position segment tile -> partial[tile][D]
 //   ess_combine : out[e][d] = sum of e's tile partials in tile order.
 #include <cooperative_groups.h>
+#include <type_traits>
 
 #include "kernels.cuh"
 
@@ -498,30 +499,44 @@ __global__ void relayout_index(const int64_t* __restrict__ idx, int E, int32_t* 
   }
 }
 
-template <class T>
+// One warp per new position; the expert by binary search over idx64 (its
+// first kIdxSmem entries staged in shared memory once per block).  Rows move
+// as VEC-element vectors (VEC = 8: 16 B per lane when both row pitches and the
+// base pointers are 16 B aligned, else scalar).
+template <class T, int VEC>
 __global__ void __launch_bounds__(NT) gather_relayout(const T* __restrict__ x1, int64_t d1,
                                                       const T* __restrict__ x2, int64_t d2,
                                                       const int64_t* __restrict__ v,
                                                       const int64_t* __restrict__ idx,
                                                       const int32_t* __restrict__ idx64, int E,
                                                       T* __restrict__ o1, T* __restrict__ o2) {
-  // one warp per new position; the expert by binary search over idx64
-  const int64_t np = idx64[E];
+  constexpr int kIdxSmem = 2048;
+  __shared__ int32_t s64[kIdxSmem + 1];
+  const bool in_smem = E <= kIdxSmem;
+  if (in_smem)
+    for (int e = threadIdx.x; e <= E; e += NT) s64[e] = idx64[e];
+  __syncthreads();
+  const int32_t* i64 = in_smem ? s64 : idx64;
+  const int64_t np = i64[E];
   const int lane = threadIdx.x % 32;
   const int64_t nw = static_cast<int64_t>(gridDim.x) * (NT / 32);
+  using V = typename std::conditional<VEC == 8, uint4, T>::type;
+  const V zero = {};
   for (int64_t p = static_cast<int64_t>(blockIdx.x) * (NT / 32) + threadIdx.x / 32; p < np;
        p += nw) {
     int lo = 0, hi = E;  // last e with idx64[e] <= p
     while (hi - lo > 1) {
       const int mid = (lo + hi) / 2;
-      if (idx64[mid] <= p) lo = mid; else hi = mid;
+      if (i64[mid] <= p) lo = mid; else hi = mid;
     }
-    const int64_t off = p - idx64[lo];
+    const int64_t off = p - i64[lo];
     const int64_t src = off < idx[lo + 1] - idx[lo] ? v[idx[lo] + off] : -1;
-    for (int64_t c = lane; c < d1; c += 32)
-      o1[p * d1 + c] = src >= 0 ? x1[src * d1 + c] : from_f32<T>(0.f);
-    for (int64_t c = lane; c < d2; c += 32)
-      o2[p * d2 + c] = src >= 0 ? x2[src * d2 + c] : from_f32<T>(0.f);
+    const V* s1 = reinterpret_cast<const V*>(x1 + (src >= 0 ? src : 0) * d1);
+    const V* s2 = reinterpret_cast<const V*>(x2 + (src >= 0 ? src : 0) * d2);
+    V* t1 = reinterpret_cast<V*>(o1 + p * d1);
+    V* t2 = reinterpret_cast<V*>(o2 + p * d2);
+    for (int64_t c = lane; c < d1 / VEC; c += 32) t1[c] = src >= 0 ? s1[c] : zero;
+    for (int64_t c = lane; c < d2 / VEC; c += 32) t2[c] = src >= 0 ? s2[c] : zero;
   }
 }
 
@@ -535,9 +550,13 @@ hxm_status launch_estmm_relayout(const void* x1, int64_t d1, const void* x2, int
   HXM_CHECK_LAUNCH();
   const int blocks = static_cast<int>(std::max<int64_t>(
       1, std::min<int64_t>(ceil_div(bound, NT / 32), static_cast<int64_t>(sm_count()) * 8)));
-  gather_relayout<__nv_bfloat16><<<blocks, NT, 0, st>>>(
-      static_cast<const __nv_bfloat16*>(x1), d1, static_cast<const __nv_bfloat16*>(x2), d2, v,
-      idx, idx64, E, static_cast<__nv_bfloat16*>(o1), static_cast<__nv_bfloat16*>(o2));
+  using B = __nv_bfloat16;
+  const bool vec = d1 % 8 == 0 && d2 % 8 == 0 &&
+                   ((reinterpret_cast<uintptr_t>(x1) | reinterpret_cast<uintptr_t>(x2) |
+                     reinterpret_cast<uintptr_t>(o1) | reinterpret_cast<uintptr_t>(o2)) % 16) == 0;
+  auto kern = vec ? gather_relayout<B, 8> : gather_relayout<B, 1>;
+  kern<<<blocks, NT, 0, st>>>(static_cast<const B*>(x1), d1, static_cast<const B*>(x2), d2, v,
+                              idx, idx64, E, static_cast<B*>(o1), static_cast<B*>(o2));
   HXM_CHECK_LAUNCH();
   return HXM_OK;
 }
