@@ -173,6 +173,33 @@ hxm_status umma_estmm(const EstmmArgs& a, cudaStream_t st);
 // dense A, 256-row tiles, d2 == 384 (HXM_WIDE=0 disables)
 bool umma_wide_ok(const EsmmArgs& a);
 hxm_status umma_wide_esmm(const EsmmArgs& a, cudaStream_t st);
+// Chained layer GEMMs (umma_chain.cu), one persistent CTA-pair kernel over
+// 128-column hidden chunks: forward fwd1 -> fwd2 (y1 = x W1 + b1, F / F'
+// stash, y += F W2 + b2), backward bwd_act -> gx (g_y1 = (g_y W2^T) F', gb1
+// column sums, g_x += g_y1 W1^T).  GEMM2's output width must be 384, GEMM1's
+// K a multiple of 192 up to 384; 256-row tiles; no shard-major weights, no
+// peer rows (HXM_CHAIN=0 disables).
+struct ChainArgs {
+  bool bwd;
+  const void* a;   // GEMM1 A rows (bf16): x_s (forward) / g_y_s (backward)
+  int64_t rows;    // rows behind a / the stashes
+  const void* w1;  // E x d_in x H
+  const void* w2;  // E x H x d_out
+  const float* b1; // forward: E x H
+  const float* b2; // forward: E x d_out or null
+  int64_t n_experts, d_in, hidden, d_out;
+  const SegTile* tiles;
+  const int32_t* n_tiles;
+  int max_tiles;
+  int act;
+  void* dact;       // F'(y1) stash, rows x H: written (forward) / read (backward)
+  void* chunk_out;  // F(y1) (forward) / g_y1 (backward) stash, rows x H
+  float* out;       // y (forward) / g_x (backward), zeroed; rows via omap
+  float* colsum;    // backward: gb1 partials (the BWD_ACT layout), or null
+  RowMap omap;
+};
+bool umma_chain_ok(bool bwd, int64_t d_in, int64_t hidden, int64_t d_out, int tile_rows);
+hxm_status umma_chain(const ChainArgs& a, cudaStream_t st);
 bool umma_supports_esmm(int64_t d1, int64_t d2);
 bool umma_supports_estmm(int64_t d1, int64_t d2);
 // CTA-pair ESMM (dense A, 256-row tiles): BN must split into whole B halves

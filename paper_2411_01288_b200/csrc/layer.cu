@@ -327,6 +327,36 @@ hxm_status layer_forward(const hxm_layer_desc* d, const void* x, const void* w1,
   a1.omap = slot;
   a1.out1 = w.y1s;
   a1.out2 = w.y2s;
+  if (dt == HXM_BF16 && d->weight_shards <= 1 && !yp &&
+      umma_chain_ok(false, d->d_in, d->hidden, d->d_out, w.rows_a)) {
+    // (1) + (2) as one chained launch: the F(y1) chunks feed the second GEMM
+    // from shared memory (umma_chain.cu); the stash is written as before
+    ChainArgs c{};
+    c.bwd = false;
+    c.a = w.xs;
+    c.rows = w.bound;
+    c.w1 = w1;
+    c.b1 = b1;
+    c.w2 = w2;
+    c.b2 = d->add_b2 ? b2 : nullptr;
+    c.n_experts = E;
+    c.d_in = d->d_in;
+    c.hidden = d->hidden;
+    c.d_out = d->d_out;
+    c.tiles = w.tiles_a;
+    c.n_tiles = w.n_tiles_a;
+    c.max_tiles = a1.max_tiles;
+    c.act = d->activation;
+    c.dact = w.y1s;
+    c.chunk_out = w.y2s;
+    c.out = y;
+    c.omap = slot;
+    // x_s, W1, W2 read; F', F written; y (fp32) written once
+    const double bytes = a1.bytes + w2bytes + 4.0 * N * d->d_out;
+    ProfScope ps(st, "esmm_fwd_chain", a1.work + 2.0 * kn * d->hidden * d->d_out, WORK_FLOP,
+                 bytes);
+    return umma_chain(c, st);
+  }
   HXM_RETURN_IF(launch_esmm(dt, a1, st));
   // (2) y += y2 W2 + b2 over all choices     (moe_layer.cpp:61-63)
   EsmmArgs a2 = a1;
@@ -466,7 +496,38 @@ hxm_status layer_backward(const hxm_layer_desc* d, const void* x, const void* w1
   // tcgen05 path: fused into the g_y1 epilogue (column sums of the stored
   // bf16 tile per (tile, CTA)), then a deterministic per-expert combine
   b6.colsum = w.colsum;
-  HXM_RETURN_IF(launch_esmm(dt, b6, st));
+  // (6,7) + (10) chained (umma_chain.cu): the g_y1 chunks feed the g_x GEMM
+  // from shared memory; g_y1 is still stashed for gW1 and its gb1 column sums
+  // are fused as above
+  const bool chain = dt == HXM_BF16 && d->weight_shards <= 1 && !gxp &&
+                     umma_chain_ok(true, Di, H, Do, w.rows_a);
+  if (chain) {
+    ChainArgs c{};
+    c.bwd = true;
+    c.a = w.gys;
+    c.rows = w.bound;
+    c.w1 = w1;
+    c.w2 = w2;
+    c.n_experts = E;
+    c.d_in = Di;
+    c.hidden = H;
+    c.d_out = Do;
+    c.tiles = w.tiles_a;
+    c.n_tiles = w.n_tiles_a;
+    c.max_tiles = b6.max_tiles;
+    c.act = d->activation;
+    c.dact = w.y1s;
+    c.chunk_out = w.g1s;
+    c.out = gx;
+    c.colsum = w.colsum;
+    c.omap = slot;
+    // sorted g_y, W2, F'(y1) and W1 read, g_y1 written, gx (fp32) written
+    const double bytes = b6.bytes + static_cast<double>(E) * Di * H * esz + 4.0 * N * Di;
+    ProfScope ps(st, "esmm_bwd_chain", b6.work + 2.0 * kn * H * Di, WORK_FLOP, bytes);
+    HXM_RETURN_IF(umma_chain(c, st));
+  } else {
+    HXM_RETURN_IF(launch_esmm(dt, b6, st));
+  }
   std::unique_ptr<SideBranch> branch;  // joined on every return path
   const char* se = std::getenv("HXM_SIDE");
   const bool use_side = !(se && se[0] == '0');
@@ -534,7 +595,7 @@ hxm_status layer_backward(const hxm_layer_desc* d, const void* x, const void* w1
   b10.peer = gxp;  // fused reduce-scatter into the token owners' rows
   b10.out1 = nullptr;
   b10.y1s = nullptr;
-  HXM_RETURN_IF(launch_esmm(dt, b10, st));
+  if (!chain) HXM_RETURN_IF(launch_esmm(dt, b10, st));
   if (branch) HXM_TRY_CUDA(branch->join());
   return HXM_OK;
 }
