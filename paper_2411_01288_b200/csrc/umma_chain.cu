@@ -67,6 +67,9 @@ struct ChainParams {
   CUtensorMap tmW2;  // W2 as (64, H, d_out / 64, E), box 64 x 64 x 3
   CUtensorMap tmF;   // bf16 chunk output stash (F / g_y1): (H, rows), box 64 x 128
   CUtensorMap tmFs;  // the same, box 64 x 32 (segment-end slices)
+  CUtensorMap tmD;   // F'(y1) stash (H, rows), box 64 x 128
+  CUtensorMap tmDs;  // F'(y1) stash, box 64 x 32
+  int fp_tma;        // F' through the chunk buffer by TMA (1) or per-row global access (0)
   __nv_bfloat16* dact;  // F'(y1) stash, row stride H: written (forward) / read (backward)
   const float* b1;      // forward: E x H
   const float* b2;      // forward: E x 384 or null
@@ -205,7 +208,8 @@ __global__ void __launch_bounds__(kChThreads, 1)
   uint64_t* f_empty = f_full + 1;
   uint64_t* acc2_full = f_empty + 1;
   uint64_t* acc2_empty = acc2_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc2_empty + 1);
+  uint64_t* fp_full = acc2_empty + 1;  // backward: F'(y1) chunk landed in the F buffer
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fp_full + 1);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kChStages; ++s) {
@@ -220,6 +224,7 @@ __global__ void __launch_bounds__(kChThreads, 1)
     mbar_init(f_empty, 1);
     mbar_init(acc2_full, 1);
     mbar_init(acc2_empty, kChEW * CG);
+    mbar_init(fp_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -442,7 +447,7 @@ __global__ void __launch_bounds__(kChThreads, 1)
     const int r = lg * 32 + lane; // this thread's row of the CTA's 128
     const bool elect = ew == 0 && lane == 0;
     const int H = p.H;
-    uint32_t f1ph = 0, feph = 0, f2ph = 0;
+    uint32_t f1ph = 0, feph = 0, f2ph = 0, fpph = 0;
     int gch = 0;  // running chunk count (bias slots)
     long long te[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const long long tk0 = (TR && p.trace) ? clock64() : 0;
@@ -489,7 +494,7 @@ __global__ void __launch_bounds__(kChThreads, 1)
         if (wr_bias) bnext = bias_val(c + 1 < nC ? t.expert : next_e, c + 1 < nC ? c + 1 : 0);
         // backward: this row's F'(y1) chunk, loaded before the accumulator wait
         uint4 dv[4] = {};
-        if (BWD && slice_ok) {
+        if (BWD && !p.fp_tma && slice_ok) {
           const __nv_bfloat16* src = dact_row + c * kChNC;
 #pragma unroll
           for (int j = 0; j < 2; ++j)
@@ -525,7 +530,7 @@ __global__ void __launch_bounds__(kChThreads, 1)
           }
           // F' straight to the stash (this row's 64 bytes of the chunk)
           // (two 256-bit stores: whole 32-byte sectors, no partial-sector writes)
-          if (slice_ok) {
+          if (!p.fp_tma && slice_ok) {
             __nv_bfloat16* dst = dact_row + c * kChNC;
 #pragma unroll
             for (int j = 0; j < 2; ++j)
@@ -534,7 +539,7 @@ __global__ void __launch_bounds__(kChThreads, 1)
                            "r"(o1[8 * j + 4]), "r"(o1[8 * j + 5]), "r"(o1[8 * j + 6]), "r"(o1[8 * j + 7])
                            : "memory");
           }
-        } else {
+        } else if (!p.fp_tma) {
           // g_y1 = (g_y W2^T) * F'(y1); padding slots and rows past the
           // segment end are zero (they feed the gb1 sums and GEMM2)
           const bool pad = orow < 0;
@@ -560,6 +565,63 @@ __global__ void __launch_bounds__(kChThreads, 1)
         mbar_wait(f_empty, feph ^ 1);
         mark(3);
         feph ^= 1;
+        uint8_t* const frow = sF + (cg >> 1) * kABytes + r * 128;
+        if (p.fp_tma) {
+          if constexpr (!BWD) {
+            // F' through the (now free) chunk buffer: one TMA store per
+            // 64-column box instead of per-row global stores
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int j0 = (cg & 1) * 4 + j;
+              *reinterpret_cast<uint4*>(frow + ((j0 ^ (r & 7)) << 4)) =
+                  make_uint4(o1[4 * j], o1[4 * j + 1], o1[4 * j + 2], o1[4 * j + 3]);
+            }
+            fence_async_smem();
+            named_bar_sync(4, 32 * kChEW);
+            if (elect) {
+              const int col = c * kChNC;
+              if (rows_here >= BM) {
+                tma_store_2d(&p.tmD, sF, col, qbase);
+                tma_store_2d(&p.tmD, sF + kABytes, col + 64, qbase);
+              } else {
+                for (int sl = 0; sl * 32 < rows_here; ++sl) {
+                  tma_store_2d(&p.tmDs, sF + sl * 4096, col, qbase + sl * 32);
+                  tma_store_2d(&p.tmDs, sF + kABytes + sl * 4096, col + 64, qbase + sl * 32);
+                }
+              }
+              bulk_commit();
+              asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            }
+            named_bar_sync(5, 32 * kChEW);
+          } else {
+            // F'(y1) chunk of this CTA's 128 rows into the chunk buffer (the
+            // rows past a segment end are loaded too and masked below)
+            if (elect) {
+              mbar_arrive_tx(fp_full, 2 * kABytes);
+              tma_2d(sF, &p.tmD, fp_full, c * kChNC, qbase);
+              tma_2d(sF + kABytes, &p.tmD, fp_full, c * kChNC + 64, qbase);
+            }
+            mbar_wait(fp_full, fpph);
+            fpph ^= 1;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int j0 = (cg & 1) * 4 + j;
+              dv[j] = *reinterpret_cast<const uint4*>(frow + ((j0 ^ (r & 7)) << 4));
+            }
+            const bool pad = orow < 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const __nv_bfloat162* yb = reinterpret_cast<const __nv_bfloat162*>(&dv[j]);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float2 g = f2_mul(make_float2(__uint_as_float(rr[8 * j + 2 * i]),
+                                                    __uint_as_float(rr[8 * j + 2 * i + 1])),
+                                        __bfloat1622float2(yb[i]));
+                o2[4 * j + i] = pad ? 0u : pack_bf16(g.x, g.y);
+              }
+            }
+          }
+        }
         {
           uint8_t* fa = sF + (cg >> 1) * kABytes + r * 128;
 #pragma unroll
@@ -783,6 +845,19 @@ hxm_status umma_chain(const ChainArgs& a, cudaStream_t st) {
     if (!make_map(&prm.tmF, a.chunk_out, 2, dims, strides, box) ||
         !make_map(&prm.tmFs, a.chunk_out, 2, dims, strides, box_s))
       return invalid_arg("chained layer GEMMs: cannot encode the stash map");
+    if (!make_map(&prm.tmD, a.dact, 2, dims, strides, box) ||
+        !make_map(&prm.tmDs, a.dact, 2, dims, strides, box_s))
+      return invalid_arg("chained layer GEMMs: cannot encode the F' stash map");
+  }
+  {
+    // F' by TMA through the chunk buffer: the backward's default (per-row
+    // loads of the stash throttle the LSU); the forward stores F' per row
+    // (faster there: the extra store / read-back barrier pair costs more)
+    static const int fpt = [] {
+      const char* e = std::getenv("HXM_CHAIN_FPT");
+      return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    prm.fp_tma = fpt >= 0 ? fpt : (a.bwd ? 1 : 0);
   }
   prm.dact = static_cast<__nv_bfloat16*>(a.dact);
   prm.b1 = a.bwd ? nullptr : a.b1;
