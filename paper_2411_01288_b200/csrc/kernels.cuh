@@ -178,7 +178,7 @@ hxm_status umma_wide_esmm(const EsmmArgs& a, cudaStream_t st);
 // stash, y += F W2 + b2), backward bwd_act -> gx (g_y1 = (g_y W2^T) F', gb1
 // column sums, g_x += g_y1 W1^T).  GEMM2's output width must be 384, GEMM1's
 // K a multiple of 192 up to 384; 256-row tiles; no shard-major weights, no
-// peer rows (HXM_CHAIN=0 disables).
+// peer rows.  Opt-in: HXM_CHAIN=1 (forward), HXM_CHAIN_BWD=1 (backward).
 struct ChainArgs {
   bool bwd;
   const void* a;   // GEMM1 A rows (bf16): x_s (forward) / g_y_s (backward)

@@ -488,6 +488,19 @@ __global__ void __launch_bounds__(kChThreads, 1)
       __nv_bfloat16* dact_row = p.dact + static_cast<int64_t>(qbase + r) * H + cg * 32;
       if (TR && p.trace) tmark = clock64();
       for (int c = 0; c < nC; ++c, ++gch) {
+        // backward: pull the next chunk's F'(y1) boxes into L2 (the in-place
+        // TMA load below then waits on an L2 hit, not on HBM)
+        if (BWD && p.fp_tma && elect) {
+          const bool more = c + 1 < nC;
+          if (more || nwl < total) {
+            const int pc = more ? (c + 1) * kChNC : 0;
+            const int pr = more ? qbase : p.tiles[nwl].begin + static_cast<int>(rank) * BM;
+            asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(&p.tmD),
+                         "r"(pc), "r"(pr) : "memory");
+            asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(&p.tmD),
+                         "r"(pc + 64), "r"(pr) : "memory");
+          }
+        }
         // next chunk's bias value (this tile's next chunk, or the next tile's first)
         float bnext = 0.f;
         const bool wr_bias = !BWD && lg == 0 && (c + 1 < nC || next_e >= 0);
@@ -783,12 +796,14 @@ unsigned long long* chain_trace_buf(bool bwd) {
   return g_chain_trace[bwd];
 }
 
-// HXM_CHAIN=0 disables the chained forward, HXM_CHAIN_BWD=1 enables the
-// chained backward (off by default until it beats bwd_act + gx; notes r2)
+// Opt-in (HXM_CHAIN=1 forward, HXM_CHAIN_BWD=1 backward): measured on c2
+// the chains are bit-identical but not faster than the two-kernel paths they
+// replace (forward -1 %, backward +2.5 % step time) -- the stash epilogues,
+// not HBM, bound these GEMMs (profiles/r2_notes.md 5-8)
 bool chain_on(bool bwd) {
   static const bool fwd_on = [] {
     const char* e = std::getenv("HXM_CHAIN");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   static const bool bwd_on = [] {
     const char* e = std::getenv("HXM_CHAIN_BWD");
