@@ -170,6 +170,21 @@ __device__ __forceinline__ float act_derivative(int act, float x) {
   return 1.f;
 }
 
+// F and F' with one tanh (the same expressions as act_value / act_derivative,
+// so the results are identical)
+__device__ __forceinline__ void act_both(int act, float x, float& f, float& df) {
+  if (act == HXM_ACT_GELU) {
+    const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
+    const float t = tanhf(u);
+    const float du = 0.7978845608028654f * (1.f + 3.f * 0.044715f * x * x);
+    f = 0.5f * x * (1.f + t);
+    df = 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * du;
+  } else {
+    f = act_value(act, x);
+    df = act_derivative(act, x);
+  }
+}
+
 // Row maps: padded-position p -> source row (or -1 for a padding slot).
 struct MapV64 {  // reference ReIndex v (int64 token ids, -1 pads)
   const int64_t* v;

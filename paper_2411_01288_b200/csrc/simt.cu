@@ -357,9 +357,230 @@ __global__ void zero_split_kernel(const SegTile* tiles, const int32_t* n_tiles,
     out[static_cast<int64_t>(t.expert) * slice + i] = 0.f;
 }
 
+// ---------------------------------------------------------------------------
+// Dense-operand fp32 kernels: the layer's fp32 path (c1) reads only
+// expert-sorted copies (x_s, the stash, g_y_s, g_y1_s), so no row map sits
+// between a tile and its operands.  A 3-stage cp.async ring (16-byte copies,
+// zero-filled past the ends) replaces the register-staged, transposing loads
+// of the mapped kernels above, whose per-k-step map-load -> data-load ->
+// store -> barrier chain left these small GEMMs latency-bound (~24 us each at
+// c1, IPC 1.5).  Same 64 x 64 tiles, K split and epilogues, same
+// summation order per output (k ascending within a split).
+constexpr int DS = 3;          // ring stages
+constexpr int APAD = BK + 4;   // k-contiguous rows: 80 B (16-B aligned, conflict-free reads)
+constexpr int BPAD = BN + 4;   // n-contiguous rows: 272 B
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool ok) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src),
+               "r"(ok ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// ESMM, dense A (rows tile.begin.. of a.a), B = W[e] (BT = 0: K x N rows,
+// n-contiguous) or W[e]^T use (BT = 1: W stored N x K, k-contiguous).
+// Thread (ty, tx) owns rows ty*4 + i and columns tx*4 + j (BT: tx + 16 j).
+template <bool BT>
+__global__ void __launch_bounds__(NT) esmm_dense_kernel(EsmmArgs a) {
+  const int ti = blockIdx.y;
+  if (ti >= *a.n_tiles) return;
+  const SegTile tile = a.tiles[ti];
+  const int n0 = blockIdx.x * BN;
+  const int64_t K = a.d1, N = a.d2;
+  const int64_t kper = ceil_div(ceil_div(K, BK), gridDim.z) * BK;
+  const int64_t kb = blockIdx.z * kper, ke = min(K, kb + kper);
+  const bool lead = blockIdx.z == 0;
+  __shared__ __align__(16) float As[DS][BM][APAD];
+  __shared__ __align__(16) float Bs[DS][BT ? BN : BK][BT ? APAD : BPAD];
+  const float* A = static_cast<const float*>(a.a);
+  const float* W = static_cast<const float*>(a.w) + static_cast<int64_t>(tile.expert) * K * N;
+  const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+  const int ar = tid / 4, ak = (tid % 4) * 4;
+  const int64_t arow = tile.begin + ar;
+  const bool arow_ok = arow < a.a_rows;
+  auto load = [&](int stg, int64_t k0) {
+    const bool aok = arow_ok && k0 + ak < ke;
+    cp_async16(&As[stg][ar][ak], aok ? A + arow * K + k0 + ak : A, aok);
+    if constexpr (!BT) {
+      const int kk = tid / 16, c4 = (tid % 16) * 4;
+      const bool ok = k0 + kk < ke && n0 + c4 < N;
+      cp_async16(&Bs[stg][kk][c4], ok ? W + (k0 + kk) * N + n0 + c4 : W, ok);
+    } else {
+      const int nn = tid / 4, k4 = (tid % 4) * 4;
+      const bool ok = n0 + nn < N && k0 + k4 < ke;
+      cp_async16(&Bs[stg][nn][k4], ok ? W + (n0 + nn) * K + k0 + k4 : W, ok);
+    }
+  };
+  const int nk = kb < ke ? static_cast<int>(ceil_div(ke - kb, BK)) : 0;
+  float acc[4][4] = {};
+#pragma unroll
+  for (int s = 0; s < DS - 1; ++s) {
+    if (s < nk) load(s, kb + s * BK);
+    cp_async_commit();
+  }
+  for (int it = 0; it < nk; ++it) {
+    cp_async_wait<DS - 2>();
+    __syncthreads();  // stage it complete for everyone; stage it - 1 free
+    if (it + DS - 1 < nk) load((it + DS - 1) % DS, kb + (it + DS - 1) * BK);
+    cp_async_commit();
+    const int stg = it % DS;
+#pragma unroll
+    for (int kq = 0; kq < BK / 4; ++kq) {
+      float4 av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = *reinterpret_cast<const float4*>(&As[stg][ty * 4 + i][kq * 4]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        bv[j] = BT ? *reinterpret_cast<const float4*>(&Bs[stg][tx + 16 * j][kq * 4])
+                   : *reinterpret_cast<const float4*>(&Bs[stg][kq * 4 + j][tx * 4]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float a4[4] = {av[i].x, av[i].y, av[i].z, av[i].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if constexpr (BT) {
+            acc[i][0] = fmaf(a4[q], (&bv[0].x)[q], acc[i][0]);
+            acc[i][1] = fmaf(a4[q], (&bv[1].x)[q], acc[i][1]);
+            acc[i][2] = fmaf(a4[q], (&bv[2].x)[q], acc[i][2]);
+            acc[i][3] = fmaf(a4[q], (&bv[3].x)[q], acc[i][3]);
+          } else {
+            acc[i][0] = fmaf(a4[q], bv[q].x, acc[i][0]);
+            acc[i][1] = fmaf(a4[q], bv[q].y, acc[i][1]);
+            acc[i][2] = fmaf(a4[q], bv[q].z, acc[i][2]);
+            acc[i][3] = fmaf(a4[q], bv[q].w, acc[i][3]);
+          }
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+  // epilogue (as esmm_simt_body)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = ty * 4 + i;
+    const int64_t p = tile.begin + r;
+    if (p >= tile.end) continue;
+    const int orow = a.omap(p);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t n = n0 + (BT ? tx + 16 * j : tx * 4 + j);
+      if (n >= N) continue;
+      const float bias =
+          (a.bias && lead) ? a.bias[static_cast<int64_t>(tile.expert) * N + n] : 0.f;
+      const float v = acc[i][j] + bias;
+      switch (a.epi) {
+        case EPI_WRITE:
+          if (orow >= 0) a.out_f32[static_cast<int64_t>(orow) * N + n] = v;
+          break;
+        case EPI_ACCUM:
+          if (orow >= 0) a.out_f32[static_cast<int64_t>(orow) * N + n] += v;
+          break;
+        case EPI_ATOMIC:
+          if (orow >= 0) atomicAdd(a.out_f32 + static_cast<int64_t>(orow) * N + n, v);
+          break;
+        case EPI_FWD_ACT: {
+          const bool pad = orow < 0;
+          float f, df;
+          act_both(a.act, v, f, df);
+          static_cast<float*>(a.out1)[p * N + n] = pad ? 0.f : df;
+          static_cast<float*>(a.out2)[p * N + n] = pad ? 0.f : f;
+          break;
+        }
+        default: {  // EPI_BWD_ACT: g_y1 = g_y2 * F'(y1)
+          const bool pad = orow < 0;
+          const float g = acc[i][j] * static_cast<const float*>(a.y1s)[p * N + n];
+          static_cast<float*>(a.out1)[p * N + n] = pad ? 0.f : g;
+          break;
+        }
+      }
+    }
+  }
+}
+
+// ESTMM, dense X1 / X2 rows (k = positions): 64 x 64 output tile over the
+// positions [pb, pe) of a chunk, both operands row-contiguous in m / n.
+__global__ void __launch_bounds__(NT) estmm_dense_kernel(EstmmArgs a) {
+  const int ti = blockIdx.y;
+  if (ti >= *a.n_tiles) return;
+  const SegTile tile = a.tiles[ti];
+  const int mt = static_cast<int>(ceil_div(a.d1, BM));
+  const int m0 = (blockIdx.x % mt) * BM, n0 = (blockIdx.x / mt) * BN;
+  const int64_t len = tile.end - tile.begin;
+  const int64_t per = ceil_div(ceil_div(len, BK), gridDim.z) * BK;
+  const int64_t pb = tile.begin + blockIdx.z * per,
+                pe = pb + per < tile.end ? pb + per : static_cast<int64_t>(tile.end);
+  const bool reduce = (tile.flags & 1) || gridDim.z > 1;
+  const int64_t D1 = a.d1, D2 = a.d2;
+  const float* X1 = static_cast<const float*>(a.x1);
+  const float* X2 = static_cast<const float*>(a.x2);
+  __shared__ __align__(16) float As[DS][BK][BPAD];
+  __shared__ __align__(16) float Bs[DS][BK][BPAD];
+  const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+  const int kk = tid / 16, c4 = (tid % 16) * 4;
+  auto load = [&](int stg, int64_t p0) {
+    const bool rok = p0 + kk < pe;
+    const bool okA = rok && m0 + c4 < D1, okB = rok && n0 + c4 < D2;
+    cp_async16(&As[stg][kk][c4], okA ? X1 + (p0 + kk) * D1 + m0 + c4 : X1, okA);
+    cp_async16(&Bs[stg][kk][c4], okB ? X2 + (p0 + kk) * D2 + n0 + c4 : X2, okB);
+  };
+  const int nk = pb < pe ? static_cast<int>(ceil_div(pe - pb, BK)) : 0;
+  float acc[4][4] = {};
+#pragma unroll
+  for (int s = 0; s < DS - 1; ++s) {
+    if (s < nk) load(s, pb + s * BK);
+    cp_async_commit();
+  }
+  for (int it = 0; it < nk; ++it) {
+    cp_async_wait<DS - 2>();
+    __syncthreads();
+    if (it + DS - 1 < nk) load((it + DS - 1) % DS, pb + (it + DS - 1) * BK);
+    cp_async_commit();
+    const int stg = it % DS;
+#pragma unroll
+    for (int k2 = 0; k2 < BK; ++k2) {
+      const float4 av = *reinterpret_cast<const float4*>(&As[stg][k2][ty * 4]);
+      const float4 bv = *reinterpret_cast<const float4*>(&Bs[stg][k2][tx * 4]);
+      const float a4[4] = {av.x, av.y, av.z, av.w}, b4[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a4[i], b4[j], acc[i][j]);
+    }
+  }
+  cp_async_wait<0>();
+  float* out = a.out + static_cast<int64_t>(tile.expert) * D1 * D2;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t m = m0 + ty * 4 + i;
+    if (m >= D1) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t n = n0 + tx * 4 + j;
+      if (n >= D2) continue;
+      if (reduce) atomicAdd(out + m * D2 + n, acc[i][j]);
+      else out[m * D2 + n] = acc[i][j];
+    }
+  }
+}
+
 }  // namespace
 
 bool vec_ok(const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; }
+// HXM_SIMT_DENSE=0: the mapped kernels for dense operands too (A/B)
+bool dense_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("HXM_SIMT_DENSE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 hxm_status simt_esmm(hxm_dtype dt, const EsmmArgs& a, cudaStream_t st) {
   if (a.max_tiles <= 0) return HXM_OK;
@@ -371,7 +592,10 @@ hxm_status simt_esmm(hxm_dtype dt, const EsmmArgs& a, cudaStream_t st) {
   }
   dim3 grid(static_cast<unsigned>(ceil_div(a.d2, BN)), static_cast<unsigned>(a.max_tiles), kz);
   const bool vec = dt == HXM_F32 && a.d1 % 4 == 0 && a.d2 % 4 == 0 && vec_ok(a.a) && vec_ok(a.w);
-  if (dt == HXM_BF16) esmm_simt_kernel<__nv_bfloat16, false><<<grid, NT, 0, st>>>(a);
+  if (vec && a.amap.kind == MAP_DENSE && dense_on()) {
+    if (a.w_trans) esmm_dense_kernel<true><<<grid, NT, 0, st>>>(a);
+    else esmm_dense_kernel<false><<<grid, NT, 0, st>>>(a);
+  } else if (dt == HXM_BF16) esmm_simt_kernel<__nv_bfloat16, false><<<grid, NT, 0, st>>>(a);
   else if (vec) esmm_simt_kernel<float, true><<<grid, NT, 0, st>>>(a);
   else esmm_simt_kernel<float, false><<<grid, NT, 0, st>>>(a);
   HXM_CHECK_LAUNCH();
@@ -388,7 +612,9 @@ hxm_status simt_estmm(hxm_dtype dt, const EstmmArgs& a, cudaStream_t st) {
   dim3 grid(static_cast<unsigned>(ceil_div(a.d1, BM) * ceil_div(a.d2, BN)),
             static_cast<unsigned>(a.max_tiles), kz);
   const bool vec = dt == HXM_F32 && a.d1 % 4 == 0 && a.d2 % 4 == 0 && vec_ok(a.x1) && vec_ok(a.x2);
-  if (dt == HXM_BF16) estmm_simt_kernel<__nv_bfloat16, false><<<grid, NT, 0, st>>>(a);
+  if (vec && a.m1.kind == MAP_DENSE && a.m2.kind == MAP_DENSE && dense_on())
+    estmm_dense_kernel<<<grid, NT, 0, st>>>(a);
+  else if (dt == HXM_BF16) estmm_simt_kernel<__nv_bfloat16, false><<<grid, NT, 0, st>>>(a);
   else if (vec) estmm_simt_kernel<float, true><<<grid, NT, 0, st>>>(a);
   else estmm_simt_kernel<float, false><<<grid, NT, 0, st>>>(a);
   HXM_CHECK_LAUNCH();
