@@ -466,7 +466,26 @@ hxm_status layer_backward(const hxm_layer_desc* d, const void* x, const void* w1
   t2.work = 2.0 * kn * H * Do;
   // y2 and the sorted g_y read, gW2 (fp32) written
   t2.bytes = kn * (H + Do) * esz + 4.0 * E * H * Do;
-  HXM_RETURN_IF(launch_estmm(dt, t2, st));
+  // HXM_BWD_CONC=1: gW2 (and later gb1 combine + gW1) on the side stream,
+  // beside bwd_act / gx on the main stream -- independent GEMMs whose
+  // persistent grids can then fill each other's tails (graph branches)
+  static const bool conc = [] {
+    const char* e = std::getenv("HXM_BWD_CONC");
+    return e && e[0] == '1';
+  }();
+  const bool use_conc = conc && w.colsum != nullptr;
+  std::unique_ptr<SideBranch> branch_gw2;  // joined on every return path
+  if (use_conc) {
+    const SideStream side = side_stream(st);
+    branch_gw2.reset(new SideBranch(st, side));
+    if (!branch_gw2->ok()) {
+      set_error("moe_backward: side-stream fork failed");
+      return HXM_ERR_CUDA;
+    }
+    HXM_RETURN_IF(launch_estmm(dt, t2, side.st));
+  } else {
+    HXM_RETURN_IF(launch_estmm(dt, t2, st));
+  }
   // (6,7) g_y1 = (g_y W2^T) * F'(y1)          (moe_layer.cpp:105-108)
   EsmmArgs b6{};
   b6.a = w.gys;
@@ -575,7 +594,11 @@ hxm_status layer_backward(const hxm_layer_desc* d, const void* x, const void* w1
   t1.label = "estmm_gw1";
   t1.work = 2.0 * kn * Di * H;
   t1.bytes = kn * (Di + H) * esz + 4.0 * E * Di * H;
-  HXM_RETURN_IF(launch_estmm(dt, t1, st));
+  if (use_conc && branch) {
+    HXM_RETURN_IF(launch_estmm(dt, t1, side_stream(st).st));
+  } else {
+    HXM_RETURN_IF(launch_estmm(dt, t1, st));
+  }
   // (10) gx += g_y1_i W1^T                    (moe_layer.cpp:118)
   EsmmArgs b10 = b6;
   b10.a = w.g1s;
@@ -597,6 +620,7 @@ hxm_status layer_backward(const hxm_layer_desc* d, const void* x, const void* w1
   b10.y1s = nullptr;
   if (!chain) HXM_RETURN_IF(launch_esmm(dt, b10, st));
   if (branch) HXM_TRY_CUDA(branch->join());
+  if (branch_gw2) HXM_TRY_CUDA(branch_gw2->join());
   return HXM_OK;
 }
 
