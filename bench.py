@@ -273,6 +273,7 @@ def _redundancy(args, r, D, Hd):
 
 
 def run_ours(args, cfg, rank, ws, local):
+    cap = 0  # conventional-baseline capacity rows (single mode)
     import numpy as np
     import torch
 
@@ -433,7 +434,7 @@ def run_ours(args, cfg, rank, ws, local):
             # D2H of step i-2 overlap on three streams (double-buffered)
             from paper_2411_01288_b200.moe_layer import MoeGrads
             from paper_2411_01288_b200.runner import HostPipeline
-            pipe = HostPipeline(run.p, N, k, D, D, dev, dtype)
+            pipe = HostPipeline(run.p, N, k, D, D, dev, dtype, capacity=cap)
             gh = None
             if full_grads:
                 g0 = run.grads

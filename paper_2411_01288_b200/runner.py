@@ -138,8 +138,9 @@ class HostPipeline:
     drain(): wait for everything enqueued."""
 
     def __init__(self, p: MoeLayerParams, n_tokens: int, k: int, d_in: int, d_out: int,
-                 device="cuda", dtype=torch.bfloat16):
-        self.runners = [LayerRunner(p, n_tokens, k, device, dtype) for _ in range(2)]
+                 device="cuda", dtype=torch.bfloat16, capacity: int = 0):
+        self.runners = [LayerRunner(p, n_tokens, k, device, dtype, capacity=capacity)
+                        for _ in range(2)]
         f = dict(device=device)
         self.x = [torch.empty(n_tokens, d_in, dtype=dtype, **f) for _ in range(2)]
         self.a = [torch.zeros(k, n_tokens, dtype=torch.int32, **f) for _ in range(2)]
