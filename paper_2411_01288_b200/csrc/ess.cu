@@ -139,9 +139,16 @@ __device__ __forceinline__ void ess_item_rows(const EssArgs& a, int ti) {
   for (int g = 0; g < GPL; ++g)
 #pragma unroll
     for (int i = 0; i < VEC; ++i) acc[g][i] = 0.f;
-  constexpr int U = 4;  // rows in flight per warp (x GPL groups per lane)
+  // rows in flight per warp (x GPL groups per lane); 16-byte vectors stay
+  // raw (4 registers, not VEC floats) until they are summed, so 8 rows fit
+  // the register budget of 4 converted ones: a 128-row item is two rounds of
+  // loads instead of four.  Each warp still sums rows warp, warp + W, ... in
+  // ascending order (the same partials as before).
+  constexpr bool kRaw = sizeof(T) * VEC == 16;
+  constexpr int U = kRaw ? 8 : 4;
   for (int r0 = warp; r0 < nrows; r0 += W * U) {
-    float v[U][GPL][VEC];
+    uint4 raw[kRaw ? U : 1][GPL];
+    float v[kRaw ? 1 : U][GPL][VEC];
     int rr[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -150,12 +157,17 @@ __device__ __forceinline__ void ess_item_rows(const EssArgs& a, int ti) {
 #pragma unroll
       for (int g = 0; g < GPL; ++g) {
         const int cg = lane + 32 * g;
-        if (rr[u] >= 0 && cg < col_groups)
-          load_vec<T, VEC>(X + static_cast<int64_t>(rr[u]) * D + static_cast<int64_t>(cg) * VEC,
-                           v[u][g]);
-        else
+        const bool ok = rr[u] >= 0 && cg < col_groups;
+        const T* src = X + static_cast<int64_t>(ok ? rr[u] : 0) * D + static_cast<int64_t>(cg) * VEC;
+        if constexpr (kRaw) {
+          raw[u][g] = ok ? __ldg(reinterpret_cast<const uint4*>(src)) : make_uint4(0u, 0u, 0u, 0u);
+        } else {
+          if (ok)
+            load_vec<T, VEC>(src, v[u][g]);
+          else
 #pragma unroll
-          for (int i = 0; i < VEC; ++i) v[u][g][i] = 0.f;
+            for (int i = 0; i < VEC; ++i) v[u][g][i] = 0.f;
+        }
       }
     }
 #pragma unroll
@@ -165,13 +177,20 @@ __device__ __forceinline__ void ess_item_rows(const EssArgs& a, int ti) {
       for (int g = 0; g < GPL; ++g) {
         const int cg = lane + 32 * g;
         if (cg >= col_groups) continue;
+        T* dst = a.copy_out ? static_cast<T*>(a.copy_out) +
+                                  (static_cast<int64_t>(tile.begin) + r0 + u * W) * D +
+                                  static_cast<int64_t>(cg) * VEC
+                            : nullptr;
+        if constexpr (kRaw) {
+          const T* e = reinterpret_cast<const T*>(&raw[u][g]);
 #pragma unroll
-        for (int i = 0; i < VEC; ++i) acc[g][i] += v[u][g][i];
-        if (a.copy_out)  // padding slots copy as zero rows
-          store_vec<T, VEC>(static_cast<T*>(a.copy_out) +
-                                (static_cast<int64_t>(tile.begin) + r0 + u * W) * D +
-                                static_cast<int64_t>(cg) * VEC,
-                            v[u][g]);
+          for (int i = 0; i < VEC; ++i) acc[g][i] += to_f32(e[i]);
+          if (dst) *reinterpret_cast<uint4*>(dst) = raw[u][g];  // padding slots copy as zero rows
+        } else {
+#pragma unroll
+          for (int i = 0; i < VEC; ++i) acc[g][i] += v[u][g][i];
+          if (dst) store_vec<T, VEC>(dst, v[u][g]);
+        }
       }
     }
   }
