@@ -59,6 +59,21 @@ inline hxm_status invalid_arg(const std::string& m) {
 
 int sm_count();  // cached per device
 bool pdl_on();   // programmatic dependent launch (HXM_PDL=0 disables)
+// Programmatic dependent launch, early trigger: every kernel of the layer
+// keeps all its CTAs resident from the start (persistent GEMM grids, fully
+// resident prologues), so it can release its dependent at once -- the next
+// kernel's CTAs then take SMs as this kernel's CTAs retire and run their
+// setup (barrier init, TMEM alloc, tensor-map prefetch) under the tail,
+// stopping at griddepcontrol.wait until this grid completes.
+// (-DHXM_PDL_TRIGGER=0: trigger only at completion.)
+#ifndef HXM_PDL_TRIGGER
+#define HXM_PDL_TRIGGER 1
+#endif
+__device__ __forceinline__ void pdl_trigger() {
+#if HXM_PDL_TRIGGER
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
 struct SideStream {
   cudaStream_t st = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;

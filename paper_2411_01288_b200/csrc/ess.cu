@@ -380,6 +380,7 @@ hxm_status gather_typed(const void* src, RowMap map, int64_t d, const IdxT* idx,
 template <class T, int VEC>
 __global__ void __launch_bounds__(NT) bwd_prologue(BwdPrologue b) {
   const EssArgs& a = b.es;
+  pdl_trigger();
   const int col_groups = static_cast<int>((a.d + VEC - 1) / VEC);
   const bool rows = VEC > 1 && col_groups <= 32 * 2 && a.d % VEC == 0;
   const int slabs = rows ? 1 : static_cast<int>(ceil_div(col_groups, 32));

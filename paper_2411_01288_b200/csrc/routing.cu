@@ -480,6 +480,7 @@ constexpr int kFastMaxGroups = 32;
 __global__ void __launch_bounds__(kThreads) fwd_prologue_1b(FwdPrologue a) {
   namespace cg = cooperative_groups;
   pro_ts(0);
+  pdl_trigger();
   cg::grid_group grid = cg::this_grid();
   const int E = a.E;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;

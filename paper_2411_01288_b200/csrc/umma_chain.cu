@@ -237,6 +237,7 @@ __global__ void __launch_bounds__(kChThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
   const uint32_t full_lead = mapa0(smem_u32(full));
   const uint32_t a1full_lead = mapa0(smem_u32(a1full));
   const uint32_t acc1e_lead = mapa0(smem_u32(acc1_empty));

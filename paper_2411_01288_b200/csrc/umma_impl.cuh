@@ -621,6 +621,7 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
   // the leader CTA's copies of the shared barriers (CG = 2)
   const uint32_t full_lead = CG == 2 ? mapa0(smem_u32(full)) : smem_u32(full);
   const uint32_t tempty_lead = CG == 2 ? mapa0(smem_u32(tempty)) : smem_u32(tempty);
@@ -891,6 +892,13 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
     constexpr int kYRing = C::kYRing;  // MODE 2: F'(y1) boxes in flight per group
     constexpr bool bwd = MODE == 2;
     constexpr bool dense_out = MODE == 1 || MODE == 2;
+    // MODE 1 with 16 epilogue warps (one output box per column group):
+    // per-warp staging slices and stores (HXM_PW_EPI=0 at build time: the
+    // column group's box is stored by one thread after a group barrier)
+#ifndef HXM_PW_EPI
+#define HXM_PW_EPI 1
+#endif
+    constexpr bool kPW = HXM_PW_EPI && MODE == 1 && C::kOutBufs == 1;
     constexpr int kNch = HB / 32;  // 32-column chunks per warp per tile
     const bool elect = ((warp - 2) & 3) == 0 && lane == 0;
     // this group's staging: kOutBufs output boxes, then (MODE 2) the F'(y1)
@@ -1078,13 +1086,20 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
             //     every thread is past the previous chunk's F'(y1) reads
             //     (MODE 2: the previous chunk's box is the slot the next F'
             //     load refills, so its store must have read it)
-            if (elect) {
-              if constexpr (C::kOutBufs == 2 && !bwd)
-                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-              else
-                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            if constexpr (kPW) {
+              // per-warp staging: this warp's 32-row slices of the group's
+              // boxes, stored by its own lane 0 -- no group barrier per chunk
+              if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+              __syncwarp();
+            } else {
+              if (elect) {
+                if constexpr (C::kOutBufs == 2 && !bwd)
+                  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                else
+                  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+              }
+              named_bar_sync(1 + half, 128);
             }
-            named_bar_sync(1 + half, 128);
             if (bwd && elect) y_issue_to(dchunk + kYRing);  // F'(y1) kYRing-1 chunks ahead
             uint4 dv[4];
             if (bwd) {  // this row's F'(y1) chunk from the staged box
@@ -1119,6 +1134,20 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
             // (2) box complete -> one TMA store per output (or per valid
             //     32-row slice at a segment end), one bulk group per chunk
             fence_async_smem();
+            if constexpr (kPW) {
+              __syncwarp();
+              if (lane == 0 && lg * 32 < rows_here && !(kDbg && (p.dbg_noload & 2))) {
+                const int row = qbase + lg * 32;
+                if (p.l2hint) {
+                  tma_store_2d_hint(&p.tmO1s, obox + lg * 2048, n, row, policy_evict_first());
+                  tma_store_2d_hint(&p.tmO2s, obox + 8192 + lg * 2048, n, row, policy_evict_last());
+                } else {
+                  tma_store_2d(&p.tmO1s, obox + lg * 2048, n, row);
+                  tma_store_2d(&p.tmO2s, obox + 8192 + lg * 2048, n, row);
+                }
+                bulk_commit();
+              }
+            } else {
             named_bar_sync(1 + half, 128);
             if (elect && !(kDbg && (p.dbg_noload & 2))) {
               if (rows_here >= BM) {
@@ -1144,6 +1173,7 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
               }
               bulk_commit();
             }
+            }  // !kPW
             if (bwd && p.colsum) {
               // fused gb1 (ESS of g_y1, es_ops.cpp:86-102): column sums of the
               // bf16 values this warp just staged (its own 32 rows, so only
@@ -1237,6 +1267,9 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
         }
         // every warp of the group is past this item's last bias read (the
         // last chunk's barrier): stage the next item's bias
+        if constexpr (kPW) {
+          if (bias_smem && has_nx) named_bar_sync(1 + half, 128);
+        }
         if (bias_smem && has_nx && lane < kBq) gbias[lg * kBq + lane] = bias_nx;
         t_cur = t_nx;
         orow_cur = orow_nx;

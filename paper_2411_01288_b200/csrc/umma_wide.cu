@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(kWideThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
   const uint32_t full_lead = mapa0(smem_u32(full));
   const uint32_t tlo_lead = mapa0(smem_u32(tempty_lo));
   const uint32_t thi_lead = mapa0(smem_u32(tempty_hi));
