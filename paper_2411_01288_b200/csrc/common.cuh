@@ -59,15 +59,14 @@ inline hxm_status invalid_arg(const std::string& m) {
 
 int sm_count();  // cached per device
 bool pdl_on();   // programmatic dependent launch (HXM_PDL=0 disables)
-// Programmatic dependent launch, early trigger: every kernel of the layer
-// keeps all its CTAs resident from the start (persistent GEMM grids, fully
-// resident prologues), so it can release its dependent at once -- the next
-// kernel's CTAs then take SMs as this kernel's CTAs retire and run their
-// setup (barrier init, TMEM alloc, tensor-map prefetch) under the tail,
-// stopping at griddepcontrol.wait until this grid completes.
-// (-DHXM_PDL_TRIGGER=0: trigger only at completion.)
+// Programmatic dependent launch, early trigger (build with
+// -DHXM_PDL_TRIGGER=1): every layer kernel keeps all its CTAs resident, so it
+// could release its dependent at once and let the next kernel's CTAs take SMs
+// as this kernel's retire, running their setup under the tail.  Measured
+// slower at c2 (0.3303 -> 0.3370 ms/step, profiles/r2_notes.md 11): off, the
+// dependent launches at completion.
 #ifndef HXM_PDL_TRIGGER
-#define HXM_PDL_TRIGGER 1
+#define HXM_PDL_TRIGGER 0
 #endif
 __device__ __forceinline__ void pdl_trigger() {
 #if HXM_PDL_TRIGGER
