@@ -90,6 +90,7 @@ struct EstmmArgs {
   const hxm_peer_rows* peer;  // tcgen05: reduce-scatter to H-shard owners (out unused)
   int peer_dim;               // 0: d1 (rows) is the split H extent, 1: d2 (columns)
   int skip_zero_split;  // split experts' slices already zeroed by the caller
+  int trans_out;        // tcgen05 whole-tile kernel: out[e] stored d2 x d1 (out = (X1^T X2)^T)
 };
 
 struct EssArgs {
@@ -173,6 +174,11 @@ hxm_status umma_estmm(const EstmmArgs& a, cudaStream_t st);
 // dense A, 256-row tiles, d2 == 384 (HXM_WIDE=0 disables)
 bool umma_wide_ok(const EsmmArgs& a);
 hxm_status umma_wide_esmm(const EsmmArgs& a, cudaStream_t st);
+// the same whole-tile scheme for ESTMM (umma_wide.cu): out[e] = X1^T X2 with
+// d2 == 384 owned whole by a CTA pair per 256 rows of d1 (A read once per
+// tile); trans_out writes the tile transposed (gW1 as (g_y1^T x_s)^T)
+bool umma_wide_estmm_ok(const EstmmArgs& a);
+hxm_status umma_wide_estmm(const EstmmArgs& a, cudaStream_t st);
 // Chained layer GEMMs (umma_chain.cu), one persistent CTA-pair kernel over
 // 128-column hidden chunks: forward fwd1 -> fwd2 (y1 = x W1 + b1, F / F'
 // stash, y += F W2 + b2), backward bwd_act -> gx (g_y1 = (g_y W2^T) F', gb1

@@ -594,6 +594,19 @@ hxm_status layer_backward(const hxm_layer_desc* d, const void* x, const void* w1
   t1.label = "estmm_gw1";
   t1.work = 2.0 * kn * Di * H;
   t1.bytes = kn * (Di + H) * esz + 4.0 * E * Di * H;
+  {
+    // D_i = 384 (c2): compute gW1 as (g_y1^T x_s)^T on the whole-tile kernel
+    // -- H on M (CTA pairs of 256 rows), the 384 columns of D_i in one
+    // accumulator, stored transposed (umma_wide.cu)
+    EstmmArgs sw = t1;
+    sw.x1 = w.g1s;
+    sw.x2 = w.xs;
+    sw.d1 = H;
+    sw.d2 = Di;
+    sw.trans_out = 1;
+    sw.peer_dim = 0;  // the owners' H spans are now rows of the computed tile
+    if (dt == HXM_BF16 && umma_wide_estmm_ok(sw)) t1 = sw;
+  }
   if (use_conc && branch) {
     HXM_RETURN_IF(launch_estmm(dt, t1, side_stream(st).st));
   } else {

@@ -57,6 +57,9 @@ hxm_status umma_esmm(const EsmmArgs& a, cudaStream_t st) {
 
 hxm_status umma_estmm(const EstmmArgs& a, cudaStream_t st) {
   if (a.max_tiles <= 0) return HXM_OK;
+  // 384-wide outputs (c2's gW2, and gW1 computed transposed): whole-tile pairs
+  if (umma_wide_estmm_ok(a)) return umma_wide_estmm(a, st);
+  if (a.trans_out) return invalid_arg("umma_estmm: transposed output needs the whole-tile kernel");
   const bool ga = a.m1.kind != MAP_DENSE, gb = a.m2.kind != MAP_DENSE;
   // CTA pairs (M = 256 output rows per pair) when both operands are dense
   // and the output rows tile evenly

@@ -476,6 +476,7 @@ struct UParams {
   int n_experts;
   int l2hint;  // MODE 1/2: L2 eviction-priority hints on the stash stores
   int reverse; // walk the work items last to first
+  int trans_out;         // whole-tile ESTMM: store out[e] transposed
   int n_peer;            // EPI_ATOMIC: > 0 -> row t reduces into peer[t / peer_rows]
   int peer_dim;          // ESTMM: 0 = output rows, 1 = output columns split over peers
   long long peer_rows;
