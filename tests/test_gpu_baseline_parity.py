@@ -103,3 +103,14 @@ def test_c5_skew_full_size_vs_oracle():
     # 8192-slot single-chunk ESTMM limit, 62 near-empty ones
     assert counts[0] > 8192 and counts[1] > 8192
     assert counts[2:].max() < 200
+
+
+def test_c2_dims_skew_vs_oracle():
+    """c2's dims (d 384: the whole-tile 256 x 384 kernels for fwd2 / gx and
+    for gW2 / gW1, the latter stored transposed) under bench.py's skew90
+    routing: two hot experts above the 8192-slot chunk limit, so the
+    whole-tile ESTMM runs split chunks that reduce with red.add into the
+    zeroed slices, and 30 near-empty experts."""
+    a = _run("c5", 32, 2, 384, 1536, 16384, 6)
+    counts = np.bincount(a.ravel(), minlength=32)
+    assert counts[0] > 8192 and counts[1] > 8192
