@@ -551,10 +551,17 @@ struct Cfg {
   static constexpr int kStaging = kGroups * kGroupBytes;
   // MODE 1: the item's bias columns (BN floats), shared by a column group's warps
   static constexpr int kBias = MODE == 1 ? BN * 4 : 0;
-  static constexpr int kBudget = 232448 - 1024 - 256 - kStaging - kBias;
+  // MODE 2 with 16 warps: per-warp F'(y1) slices and barriers (HXM_PW_EPI)
+#ifndef HXM_PW_EPI
+#define HXM_PW_EPI 1
+#endif
+  static constexpr bool kPW2 = HXM_PW_EPI && MODE == 2 && EW == 16;
+  static constexpr int kDbars = (kPW2 ? kEW : kGroups) * kYRing;
+  static constexpr int kBars = kPW2 ? 512 : 256;
+  static constexpr int kBudget = 232448 - 1024 - kBars - kStaging - kBias;
   static constexpr int kStages = kBudget / kStage > 8 ? 8 : kBudget / kStage;
   static constexpr int kSmem =
-      kStages * kStage + kStaging + kBias + 1024 /*align*/ + 256 /*barriers*/;
+      kStages * kStage + kStaging + kBias + 1024 /*align*/ + kBars /*barriers*/;
 };
 
 // MODE: 0 = ESMM, fp32 write / accumulate / reduce epilogue; 1 = ESMM with
@@ -590,7 +597,7 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + 2;
   uint64_t* dbar = tempty + 2;  // MODE 2: F'(y1) box loads, [group][ring slot]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dbar + C::kGroups * C::kYRing);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dbar + C::kDbars);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
@@ -602,7 +609,7 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], C::kEW * CG);
     }
-    for (int b = 0; b < C::kGroups * C::kYRing; ++b) mbar_init(&dbar[b], 1);
+    for (int b = 0; b < C::kDbars; ++b) mbar_init(&dbar[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -895,11 +902,12 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
     constexpr bool dense_out = MODE == 1 || MODE == 2;
     // MODE 1 with 16 epilogue warps (one output box per column group):
     // per-warp staging slices and stores (HXM_PW_EPI=0 at build time: the
-    // column group's box is stored by one thread after a group barrier)
-#ifndef HXM_PW_EPI
-#define HXM_PW_EPI 1
-#endif
+    // column group's box is stored by one thread after a group barrier).
+    // MODE 2 with 16 warps (kPW2): each warp also loads its own 32-row
+    // slices of the F'(y1) boxes (own barriers), so the g_y1 chunk needs no
+    // group barrier either.
     constexpr bool kPW = HXM_PW_EPI && MODE == 1 && C::kOutBufs == 1;
+    constexpr bool kPW2 = C::kPW2;
     constexpr int kNch = HB / 32;  // 32-column chunks per warp per tile
     const bool elect = ((warp - 2) & 3) == 0 && lane == 0;
     // this group's staging: kOutBufs output boxes, then (MODE 2) the F'(y1)
@@ -969,7 +977,9 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
         const int qbase = t.begin + static_cast<int>(rank) * BM;  // row 0 of the box
         const int rows_here = t.end - qbase;
         auto ybox = [&](int gchunk) { return hstage + (gchunk % kYRing) * 8192; };
-        auto ybar = [&](int gchunk) { return &dbar[half * kYRing + gchunk % kYRing]; };
+        auto ybar = [&](int gchunk) {
+          return &dbar[(kPW2 ? warp - 2 : half) * kYRing + gchunk % kYRing];
+        };
         // F'(y1) boxes stream kYRing - 1 chunks ahead of the math, across the
         // item boundary (the next item's first boxes load during this item's
         // last chunk); a box goes into the slot of the chunk before the one
@@ -982,11 +992,17 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
             const bool nx = c >= kNch;
             const int col = (nx ? (w_nx % per_item) * BN + half * HB : n0) + 32 * (nx ? c - kNch : c);
             const int row = (nx ? t_nx.begin : t.begin) + static_cast<int>(rank) * BM;
-            mbar_arrive_tx(ybar(y_iss), 8192);
-            tma_2d(ybox(y_iss), &p.tmY, ybar(y_iss), col, row);
+            if constexpr (kPW2) {  // this warp's 32 rows (tmO2s: the F' stash, 32 x 32)
+              mbar_arrive_tx(ybar(y_iss), 2048);
+              tma_2d(ybox(y_iss) + lg * 2048, &p.tmO2s, ybar(y_iss), col, row + lg * 32);
+            } else {
+              mbar_arrive_tx(ybar(y_iss), 8192);
+              tma_2d(ybox(y_iss), &p.tmY, ybar(y_iss), col, row);
+            }
           }
         };
-        if (bwd && elect) y_issue_to(chunk0 + (kNch < kYRing - 1 ? kNch : kYRing - 1));
+        const bool y_issuer = kPW2 ? lane == 0 : elect;
+        if (bwd && y_issuer) y_issue_to(chunk0 + (kNch < kYRing - 1 ? kNch : kYRing - 1));
         // MODE 0 bias of this warp's HB columns: every lane reads the same 32
         // floats per chunk (uniform-address LDG.128, one broadcast transaction
         // each, L1-resident) and adds them in f32x2 (MODE 1: from smem, below)
@@ -1087,7 +1103,7 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
             //     every thread is past the previous chunk's F'(y1) reads
             //     (MODE 2: the previous chunk's box is the slot the next F'
             //     load refills, so its store must have read it)
-            if constexpr (kPW) {
+            if constexpr (kPW || kPW2) {
               // per-warp staging: this warp's 32-row slices of the group's
               // boxes, stored by its own lane 0 -- no group barrier per chunk
               if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -1101,7 +1117,7 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
               }
               named_bar_sync(1 + half, 128);
             }
-            if (bwd && elect) y_issue_to(dchunk + kYRing);  // F'(y1) kYRing-1 chunks ahead
+            if (bwd && y_issuer) y_issue_to(dchunk + kYRing);  // F'(y1) kYRing-1 chunks ahead
             uint4 dv[4];
             if (bwd) {  // this row's F'(y1) chunk from the staged box
               mbar_wait(ybar(dchunk), (dchunk / kYRing) & 1);
@@ -1135,7 +1151,17 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
             // (2) box complete -> one TMA store per output (or per valid
             //     32-row slice at a segment end), one bulk group per chunk
             fence_async_smem();
-            if constexpr (kPW) {
+            if constexpr (kPW2) {
+              __syncwarp();
+              if (lane == 0 && lg * 32 < rows_here && !(kDbg && (p.dbg_noload & 2))) {
+                if (p.l2hint)
+                  tma_store_2d_hint(&p.tmO1s, obox + lg * 2048, n, qbase + lg * 32,
+                                    policy_evict_last());
+                else
+                  tma_store_2d(&p.tmO1s, obox + lg * 2048, n, qbase + lg * 32);
+                bulk_commit();
+              }
+            } else if constexpr (kPW) {
               __syncwarp();
               if (lane == 0 && lg * 32 < rows_here && !(kDbg && (p.dbg_noload & 2))) {
                 const int row = qbase + lg * 32;
@@ -1680,8 +1706,9 @@ hxm_status prep_esmm(const EsmmArgs& a, const int CG, const int bn, UParams& prm
     if (a.epi == EPI_FWD_ACT)
       ok = ok && make_map(&prm.tmO2, a.out2, 2, dims, strides, box, sw) &&
            make_map(&prm.tmO2s, a.out2, 2, dims, strides, box_s, sw);
-    else
-      ok = ok && make_map(&prm.tmY, a.y1s, 2, dims, strides, box, sw);
+    else  // MODE 2: the F'(y1) stash, 32 x 128 boxes (and 32 x 32 per-warp slices in tmO2s)
+      ok = ok && make_map(&prm.tmY, a.y1s, 2, dims, strides, box, sw) &&
+           make_map(&prm.tmO2s, a.y1s, 2, dims, strides, box_s, sw);
     if (!ok) return invalid_arg("umma_esmm: cannot encode the stash tensor maps");
   }
   return HXM_OK;
