@@ -528,6 +528,25 @@ __device__ __forceinline__ void load_w_box(const UParams& p, void* sb, uint64_t*
   }
 }
 
+// Division by a kernel-uniform divisor without the ~25-instruction integer
+// division sequence (work item -> tile, column block), as CUTLASS FastDivmod:
+// q = umulhi(n, m) >> s for n < 2^31.
+struct FastDiv {
+  uint32_t d, m, s;
+  __device__ __forceinline__ explicit FastDiv(uint32_t div) : d(div), m(0), s(0) {
+    if (div > 1) {
+      const uint32_t l = 32 - __clz(div - 1);  // ceil(log2(div))
+      const uint32_t pw = 31 + l;
+      m = static_cast<uint32_t>(((1ull << pw) + div - 1) / div);
+      s = pw - 32;
+    }
+  }
+  __device__ __forceinline__ int div(int n) const {
+    return d == 1 ? n : static_cast<int>(__umulhi(static_cast<uint32_t>(n), m) >> s);
+  }
+  __device__ __forceinline__ int mod(int n) const { return n - div(n) * static_cast<int>(d); }
+};
+
 // CG = CTAs per UMMA (cta_group): with CG = 2 a CTA pair runs M = 256 tiles,
 // each CTA holding 128 rows of A / D and half (BN/2) of the B columns.
 template <int BN, int CG = 1, int MODE = 0, int EW = 8>
@@ -640,6 +659,7 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
   const int n_items = *p.n_tiles;
   const int per_item = ESTMM ? p.n_mt * p.n_nt : p.n_nt;
   const int total = n_items * per_item;
+  const FastDiv fdi(static_cast<uint32_t>(per_item));  // work item -> (tile, rem)
   // p.reverse: walk the items last to first, so a kernel that consumes the
   // previous kernel's output starts on the rows written last (L2-resident)
   auto wmap = [&](int wl) { return p.reverse ? total - 1 - wl : wl; };
@@ -690,8 +710,8 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
       const Unit u = unit_at(ui);
       if (!u.ok) break;
       const int w = wmap(u.wl);
-      const SegTile t = p.tiles[w / per_item];
-      const int rem = w % per_item;
+      const SegTile t = p.tiles[fdi.div(w)];
+      const int rem = fdi.mod(w);
       if (!ESTMM) {
         const int n0 = rem * BN;
         const int nk = u.hi;
@@ -845,7 +865,7 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
         const Unit u = unit_at(ui);
         if (!u.ok) break;
         const int w = wmap(u.wl);
-        const int nk = ESTMM ? (p.tiles[w / per_item].end - p.tiles[w / per_item].begin + BK - 1) / BK
+        const int nk = ESTMM ? (p.tiles[fdi.div(w)].end - p.tiles[fdi.div(w)].begin + BK - 1) / BK
                              : u.hi;
         if (lane == 0) TRACE(it_, 0);
         if constexpr (CG == 2) mbar_wait_cl(&tempty[acc], aph ^ 1);
@@ -916,7 +936,7 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
     // ESMM: the next work item's tile and this lane's output row are loaded
     // one item ahead, so an epilogue that finds its accumulator already full
     // does not wait on the tile table / index latency.
-    auto tile_at = [&](int wi) { return wi < total ? p.tiles[wi / per_item] : SegTile{0, 0, 0, 0}; };
+    auto tile_at = [&](int wi) { return wi < total ? p.tiles[fdi.div(wi)] : SegTile{0, 0, 0, 0}; };
     // MODE 0: this lane's token-order output row.  MODE 1/2 only need to
     // know pads, which the layer's tile flags carry (no index load).
     auto orow_of = [&](const SegTile& tt) {
@@ -945,7 +965,7 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
     float* gbias = bias_s + half * HB;
     const bool bias_smem = MODE == 1 && p.bias != nullptr;
     auto bias_at = [&](const SegTile& tt, int ww) {
-      const int col = (ww % per_item) * BN + half * HB + lg * kBq + lane;
+      const int col = fdi.mod(ww) * BN + half * HB + lg * kBq + lane;
       const int hb = p.bias_shard_h;
       return __ldg(p.bias + (hb == 0 ? static_cast<int64_t>(tt.expert) * p.N + col
                                      : (static_cast<int64_t>(col / hb) * p.n_experts + tt.expert) *
@@ -957,8 +977,8 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
       const Unit u = unit_at(ui);
       if (!u.ok) break;
       const int w = wmap(u.wl);
-      const SegTile t = ESTMM ? p.tiles[w / per_item] : t_cur;
-      const int rem = w % per_item;
+      const SegTile t = ESTMM ? p.tiles[fdi.div(w)] : t_cur;
+      const int rem = fdi.mod(w);
       if (!ESTMM) {
         const Unit u_nx = unit_at(ui + 1);
         const bool has_nx = u_nx.ok;
@@ -990,7 +1010,7 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
           for (; y_iss < limit; ++y_iss) {
             const int c = y_iss - chunk0;
             const bool nx = c >= kNch;
-            const int col = (nx ? (w_nx % per_item) * BN + half * HB : n0) + 32 * (nx ? c - kNch : c);
+            const int col = (nx ? fdi.mod(w_nx) * BN + half * HB : n0) + 32 * (nx ? c - kNch : c);
             const int row = (nx ? t_nx.begin : t.begin) + static_cast<int>(rank) * BM;
             if constexpr (kPW2) {  // this warp's 32 rows (tmO2s: the F' stash, 32 x 32)
               mbar_arrive_tx(ybar(y_iss), 2048);
@@ -1232,7 +1252,7 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
                   cs[k].y += __shfl_xor_sync(0xffffffffu, cs[k].y, o);
                 }
               if (lane < 4) {
-                float* dst = p.colsum + ((static_cast<int64_t>(w / per_item) * CG + rank) * 4 + lg) * N +
+                float* dst = p.colsum + ((static_cast<int64_t>(fdi.div(w)) * CG + rank) * 4 + lg) * N +
                              n + cq * 8;
                 reinterpret_cast<float4*>(dst)[0] = make_float4(cs[0].x, cs[0].y, cs[1].x, cs[1].y);
                 reinterpret_cast<float4*>(dst)[1] = make_float4(cs[2].x, cs[2].y, cs[3].x, cs[3].y);
