@@ -403,14 +403,17 @@ def run_ours(args, cfg, rank, ws, local):
     launches0 = L.hxm_launch_count()
     clocks = ClockSampler(local, period=0.005)
     with clocks:
-        total_ms = max_over_ranks(timed(step_fn, not use_graph), ws)
+        # the value pass never carries per-kernel events (eager modes too)
+        total_ms = max_over_ranks(timed(step_fn, False), ws)
         launches = L.hxm_launch_count() - launches0
-        prof_ms = None
         if use_graph:
             launches = graph_kernels * args.steps  # each replay runs the captured kernels
             # second pass: the profiled graph (its event nodes hold the last
             # replay's per-kernel durations)
             prof_ms = max_over_ranks(timed(g_prof.replay, False), ws)
+        else:
+            # second pass of the eager step with an event pair per launch
+            prof_ms = max_over_ranks(timed(step_fn, True), ws)
     prof = _lib.profile_read()
     L.hxm_profile_reset()
     value = N * ws * args.steps / (total_ms / 1000.0)
@@ -544,7 +547,8 @@ def run_ours(args, cfg, rank, ws, local):
                    else "expert-specific (no padding, no dropping)",
                    "cuda_graph": use_graph,
                    "kernel_times": "second K-step pass of the same step captured with per-kernel "
-                                   "event nodes" if use_graph else "events around each launch",
+                                   "event nodes" if use_graph else
+                                   "second K-step pass with events around each launch",
                    "l2": "flushed between steps (256 MiB write, outside the timed events)"},
         "ms_per_step_profiled": (prof_ms / args.steps) if prof_ms else None,
         "layer_tflops": flop_step * args.steps * ws / (total_ms / 1e3) / 1e12,
