@@ -295,6 +295,11 @@ def test_layer_c1_fp32_full_size():
     (4, 2, 12, 20, 6, 50, "gelu", "uniform"),          # unaligned dims
     (8, 2, 640, 512, 640, 512, "gelu", "uniform"),     # K > 512: 8-warp stash epilogues
     (8, 2, 128, 256, 256, 300, "relu", "uniform"),     # K <= 512: 16-warp stash epilogues
+    # d = 384 with H a multiple of 256: the whole-tile kernels (fwd2 / gx and
+    # gW2 / transposed gW1, umma_wide.cu), incl. empty experts and top-1
+    (12, 2, 384, 256, 384, 300, "gelu", "uniform"),
+    (40, 1, 384, 512, 384, 200, "relu", "uniform"),
+    (6, 2, 384, 768, 384, 900, "identity", "zipf:1.3"),
 ])
 def test_layer_bf16_vs_oracle(E, k, din, hid, dout, n, act, dist):
     p, x, r, gy = _layer_case(E, k, din, hid, dout, n, act, torch.bfloat16, E + n, dist)
@@ -401,6 +406,8 @@ def test_layer_c4_full_size_properties():
     (2, 1, 8, 16, 0, torch.float32),        # no tokens
     (2, 1, 64, 64, 0, torch.bfloat16),
     (5, 2, 64, 256, 130, torch.bfloat16),   # segments straddling 64/128/256 rows
+    (1, 1, 384, 256, 3, torch.bfloat16),    # whole-tile kernels, 3 tokens
+    (3, 2, 384, 512, 0, torch.bfloat16),    # whole-tile kernels, no tokens
 ])
 def test_layer_edge_cases(E, k, D, Hd, N, dtype):
     H = hx()
