@@ -639,8 +639,10 @@ bool umma_wide_estmm_ok(const EstmmArgs& a) {
   }();
   const char* cp = std::getenv("HXM_CTA_PAIR");
   const bool pair_ok = !(cp && cp[0] == '0');
-  return on && pair_ok && a.m1.kind == MAP_DENSE && a.m2.kind == MAP_DENSE && a.d2 == kWideN &&
-         a.d1 % (BM * 2) == 0 && a.d1 > 0;
+  // peer shards: a warp's 32 rows must belong to one owner (row-major out)
+  const bool peer_ok = !a.peer || a.trans_out || a.peer->rows_per_rank % 32 == 0;
+  return on && pair_ok && peer_ok && a.m1.kind == MAP_DENSE && a.m2.kind == MAP_DENSE &&
+         a.d2 == kWideN && a.d1 % (BM * 2) == 0 && a.d1 > 0;
 }
 
 hxm_status umma_wide_estmm(const EstmmArgs& a, cudaStream_t st) {

@@ -113,14 +113,16 @@ def test_fused_reduce_scatter_two_processes_ipc():
 
 
 @pytest.mark.skipif(not torch.cuda.is_available(), reason="no CUDA device")
-@pytest.mark.parametrize("P", [1, 2, 4])
-def test_fused_grad_reduce_scatter_simulated_ranks(P):
+@pytest.mark.parametrize("P,Dm", [(1, 128), (2, 128), (4, 128), (2, 384), (3, 384)])
+def test_fused_grad_reduce_scatter_simulated_ranks(P, Dm):
     """Data-centric: each simulated rank runs the full layer on its own tokens
     and reduces gW1 / gW2 into the H-shard owners' buffers; the shards must
-    equal the H-slices of the summed single-GPU gradients."""
+    equal the H-slices of the summed single-GPU gradients.  Dm = 384: the
+    whole-tile ESTMM kernels (gW2 rows and the transposed gW1 reduced into the
+    owners' H spans)."""
     import paper_2411_01288_b200 as H
     from paper_2411_01288_b200 import dist as D
-    E, k, Dm, Hd, n = 8, 2, 128, 256 * P, 256
+    E, k, Hd, n = 8, 2, 256 * P, 256
     p, _ = H.make_random_params(E, Dm, Hd, Dm, "gelu", seed=9, n_tokens=0)
     span = Hd // P
     gw1s = [torch.zeros(E, Dm, span, device="cuda") for _ in range(P)]
