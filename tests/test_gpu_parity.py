@@ -201,6 +201,7 @@ def test_operators_vs_reference_fixtures(golden_dir, dtype, rtol):
     (32, 4096, 1536, 384, 8),    # c2 second GEMM shape
     (8, 1000, 128, 256, 3),      # ragged segments, odd blk
     (64, 3000, 64, 192, 8),      # many experts, some empty
+    (4, 20000, 512, 384, 8),     # whole-tile ESTMM with split (> 8192-slot) experts
 ])
 def test_bf16_operators_at_scale(E, n, d1, d2, blk):
     H = hx()
