@@ -1,7 +1,9 @@
 """Run under compute-sanitizer by tests/test_gpu_sanitizer.py: one small
-layer forward + backward on each device path (bf16 tcgen05 CTA pairs,
-bf16 single-CTA tiles, fp32 SIMT) and the operator API, so memcheck /
-racecheck / synccheck see every kernel family of the library."""
+layer forward + backward on each device path (bf16 tcgen05 CTA pairs, the
+whole-tile d 384 kernels -- and, with HXM_CHAIN=1 / HXM_CHAIN_BWD=1 in the
+environment, the chained kernels -- bf16 single-CTA tiles, fp32 SIMT) and
+the operator API, so memcheck / racecheck / synccheck see every kernel
+family of the library."""
 import os
 import sys
 
@@ -40,6 +42,7 @@ def ops(dtype):
 if __name__ == "__main__":
     torch.cuda.set_device(0)
     layer(8, 2, 128, 256, 300, torch.bfloat16)   # CTA-pair tcgen05 path
+    layer(6, 2, 384, 512, 300, torch.bfloat16)   # whole-tile fwd2 / gx / gW2 / gW1 (d 384)
     layer(4, 2, 64, 192, 150, torch.bfloat16)    # single-CTA / fallback tiles
     layer(4, 1, 96, 384, 200, torch.float32)     # fp32 SIMT path
     ops(torch.bfloat16)

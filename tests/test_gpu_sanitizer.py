@@ -55,6 +55,13 @@ def test_sanitizer_clean(tool):
     assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
 
 
+def test_memcheck_chained_kernels_clean():
+    """The opt-in chained fwd1 -> fwd2 / bwd_act -> gx kernels (umma_chain.cu)."""
+    rc, out = _run("memcheck", {"HXM_CHAIN": "1", "HXM_CHAIN_BWD": "1"})
+    assert rc == 0, out[-6000:]
+    assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
+
+
 def test_racecheck_single_cta_clean():
     rc, out = _run("racecheck", {"HXM_CTA_PAIR": "0"})
     assert rc == 0, out[-6000:]
