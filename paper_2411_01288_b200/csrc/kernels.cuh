@@ -165,6 +165,8 @@ hxm_status launch_ess(hxm_dtype dt, const EssArgs& a, cudaStream_t st);
 
 // fp32 FMA kernels (simt.cu)
 hxm_status simt_esmm(hxm_dtype dt, const EsmmArgs& a, cudaStream_t st);
+// the dense-operand fp32 ESMM (the one that can fuse gb1 column sums) applies
+bool simt_dense_esmm_ok(hxm_dtype dt, const EsmmArgs& a);
 hxm_status simt_estmm(hxm_dtype dt, const EstmmArgs& a, cudaStream_t st);
 // tcgen05 kernels (umma.cu); return HXM_ERR_UNSUPPORTED for shapes they
 // do not cover (d1/d2 not multiples of 64), which the caller reports.

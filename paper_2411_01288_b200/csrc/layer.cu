@@ -60,6 +60,8 @@ struct LayerWs {
 };
 
 size_t esize(int32_t dt) { return dt == HXM_BF16 ? 2 : 4; }
+// partial rows of the fused gb1 column sums per tile
+int colsum_parts(int rows_a) { return rows_a >= kUmmaRows ? (rows_a / kUmmaRows) * 4 : 1; }
 
 LayerWs carve(Arena& ar, const hxm_layer_desc& d) {
   LayerWs w{};
@@ -109,9 +111,13 @@ LayerWs carve(Arena& ar, const hxm_layer_desc& d) {
   w.y2s = ar.take<char>(stash);
   w.g1s = ar.take<char>(stash);
   const char* fuse = std::getenv("HXM_FUSE_GB1");  // 0: separate ESS pass for gb1
-  if (w.rows_a >= kUmmaRows && !(fuse && fuse[0] == '0'))
+  // fused gb1 column sums: tcgen05 (per tile, CTA and TMEM lane group) or the
+  // dense fp32 SIMT kernel (one partial row per 64-row tile)
+  const bool simt_cs = w.rows_a == kSimtRows && dt == HXM_F32 && d.hidden % 4 == 0 &&
+                       d.d_out % 4 == 0;
+  if ((w.rows_a >= kUmmaRows || simt_cs) && !(fuse && fuse[0] == '0'))
     w.colsum = ar.take<float>(static_cast<size_t>(max_tiles(w.bound, d.n_experts, w.rows_a)) *
-                              (w.rows_a / kUmmaRows) * 4 * d.hidden);
+                              colsum_parts(w.rows_a) * d.hidden);
   return w;
 }
 
@@ -515,6 +521,8 @@ hxm_status layer_backward(const hxm_layer_desc* d, const void* x, const void* w1
   // tcgen05 path: fused into the g_y1 epilogue (column sums of the stored
   // bf16 tile per (tile, CTA)), then a deterministic per-expert combine
   b6.colsum = w.colsum;
+  // fp32: the fused sums need the dense SIMT kernel (aligned, 4-wide rows)
+  if (b6.colsum && w.rows_a < kUmmaRows && !simt_dense_esmm_ok(dt, b6)) b6.colsum = nullptr;
   // (6,7) + (10) chained (umma_chain.cu): the g_y1 chunks feed the g_x GEMM
   // from shared memory; g_y1 is still stashed for gW1 and its gb1 column sums
   // are fused as above
@@ -550,12 +558,12 @@ hxm_status layer_backward(const hxm_layer_desc* d, const void* x, const void* w1
   std::unique_ptr<SideBranch> branch;  // joined on every return path
   const char* se = std::getenv("HXM_SIDE");
   const bool use_side = !(se && se[0] == '0');
-  if (w.colsum && !use_side) {
-    const int parts = (w.rows_a / kUmmaRows) * 4;
+  if (b6.colsum && !use_side) {
+    const int parts = colsum_parts(w.rows_a);
     HXM_RETURN_IF(launch_colsum_combine(
         w.colsum, w.tiles_a_off, static_cast<int>(E), parts, H, gb1, st, "gb1_combine",
         (static_cast<double>(max_tiles(w.bound, E, w.rows_a)) * parts + E) * H * 4.0));
-  } else if (w.colsum) {
+  } else if (b6.colsum) {
     // the gb1 combine is independent of gW1 / gx: it runs on the side
     // stream beside them (a parallel branch of the captured graph)
     const SideStream side = side_stream(st);
@@ -564,7 +572,7 @@ hxm_status layer_backward(const hxm_layer_desc* d, const void* x, const void* w1
       set_error("moe_backward: side-stream fork failed");
       return HXM_ERR_CUDA;
     }
-    const int parts = (w.rows_a / kUmmaRows) * 4;  // per tile: CTAs x TMEM lane groups
+    const int parts = colsum_parts(w.rows_a);  // per tile: CTAs x TMEM lane groups (tcgen05)
     HXM_RETURN_IF(launch_colsum_combine(
         w.colsum, w.tiles_a_off, static_cast<int>(E), parts, H, gb1, side.st, "gb1_combine",
         (static_cast<double>(max_tiles(w.bound, E, w.rows_a)) * parts + E) * H * 4.0));

@@ -461,7 +461,10 @@ __global__ void __launch_bounds__(NT) esmm_dense_kernel(EsmmArgs a) {
     }
   }
   cp_async_wait<0>();
-  // epilogue (as esmm_simt_body)
+  // epilogue (as esmm_simt_body); EPI_BWD_ACT with a.colsum also sums this
+  // CTA's g_y1 columns over its 64 rows (fused gb1: one deterministic
+  // partial row per tile, combined per expert by colsum_combine)
+  float colacc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int r = ty * 4 + i;
@@ -497,9 +500,23 @@ __global__ void __launch_bounds__(NT) esmm_dense_kernel(EsmmArgs a) {
           const bool pad = orow < 0;
           const float g = acc[i][j] * static_cast<const float*>(a.y1s)[p * N + n];
           static_cast<float*>(a.out1)[p * N + n] = pad ? 0.f : g;
+          colacc[j] += pad ? 0.f : g;
           break;
         }
       }
+    }
+  }
+  if (a.epi == EPI_BWD_ACT && a.colsum) {
+    __shared__ float red[NT / 16][BN];
+    __syncthreads();  // (the operand ring is no longer read)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) red[ty][BT ? tx + 16 * j : tx * 4 + j] = colacc[j];
+    __syncthreads();
+    if (tid < BN && n0 + tid < N) {
+      float sum = 0.f;
+#pragma unroll
+      for (int t = 0; t < NT / 16; ++t) sum += red[t][tid];  // fixed order: deterministic
+      a.colsum[static_cast<int64_t>(ti) * N + n0 + tid] = sum;
     }
   }
 }
@@ -582,6 +599,11 @@ bool dense_on() {
   return on;
 }
 
+bool simt_dense_esmm_ok(hxm_dtype dt, const EsmmArgs& a) {
+  return dt == HXM_F32 && a.d1 % 4 == 0 && a.d2 % 4 == 0 && vec_ok(a.a) && vec_ok(a.w) &&
+         a.amap.kind == MAP_DENSE && dense_on();
+}
+
 hxm_status simt_esmm(hxm_dtype dt, const EsmmArgs& a, cudaStream_t st) {
   if (a.max_tiles <= 0) return HXM_OK;
   // split K for the reduction epilogue when the grid would not fill the GPU
@@ -592,6 +614,8 @@ hxm_status simt_esmm(hxm_dtype dt, const EsmmArgs& a, cudaStream_t st) {
   }
   dim3 grid(static_cast<unsigned>(ceil_div(a.d2, BN)), static_cast<unsigned>(a.max_tiles), kz);
   const bool vec = dt == HXM_F32 && a.d1 % 4 == 0 && a.d2 % 4 == 0 && vec_ok(a.a) && vec_ok(a.w);
+  if (a.colsum && !(vec && a.amap.kind == MAP_DENSE && dense_on()))
+    return invalid_arg("esmm: fused column sums need the dense fp32 kernel");
   if (vec && a.amap.kind == MAP_DENSE && dense_on()) {
     if (a.w_trans) esmm_dense_kernel<true><<<grid, NT, 0, st>>>(a);
     else esmm_dense_kernel<false><<<grid, NT, 0, st>>>(a);
