@@ -618,7 +618,12 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
   uint64_t* dbar = tempty + 2;  // MODE 2: F'(y1) box loads, [group][ring slot]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dbar + C::kDbars);
 
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // warp index broadcast from lane 0: ptxas then knows it is warp-uniform and
+  // keeps what derives from it (roles, TMEM lane group, column group, staging
+  // slices, TMA-store coordinates) in uniform registers (CUTLASS's
+  // canonical_warp_idx_sync)
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x / 32), 0);
+  const int lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full[s], 1);  // CG = 2: the leader's producer expects both CTAs' bytes
