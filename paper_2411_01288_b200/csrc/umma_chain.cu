@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(kChThreads, 1)
     // floats of the NEXT chunk (slot (gch + 1) & 1) between the chunk's two
     // barriers; everyone reads the current slot before the first barrier
     auto bias_val = [&](int e, int c) {
-      return BWD ? 0.f : __ldg(p.b1 + static_cast<int64_t>(e) * H + c * kChNC + cg * 32 + lane);
+      return BWD ? 0.f : ldg_nc(p.b1 + static_cast<int64_t>(e) * H + c * kChNC + cg * 32 + lane);
     };
     {
       const int wl0 = cluster;
@@ -711,16 +711,17 @@ __global__ void __launch_bounds__(kChThreads, 1)
       tc_fence_after();
       if (elect) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       named_bar_sync(3, 32 * kChEW);  // F buffer free: staging for the fp32 rows
-      const float* bias2 = p.b2 ? p.b2 + static_cast<int64_t>(t.expert) * kChN2 : nullptr;
+      // (the backward's g_x has no bias: compiled out, not just skipped)
+      const float* bias2 = (!BWD && p.b2) ? p.b2 + static_cast<int64_t>(t.expert) * kChN2 : nullptr;
       auto emit = [&](const uint32_t (&q)[32], const int gcol) {
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(q[i]);
-        if (bias2) {
+        if (!BWD && bias2) {
           const float4* b4 = reinterpret_cast<const float4*>(bias2 + gcol);
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
-            const float4 b = __ldg(b4 + i / 4);
+            const float4 b = ldg_nc_v4(b4 + i / 4);
             v[i] += b.x; v[i + 1] += b.y; v[i + 2] += b.z; v[i + 3] += b.w;
           }
         }

@@ -422,6 +422,21 @@ __device__ __forceinline__ float2 f2_mul(float2 a, float2 b) {
   return *reinterpret_cast<float2*>(&d);
 }
 __device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+// Read-only loads of optional operands (bias pointers that may be null):
+// asm volatile so the compiler cannot speculate them above the null check
+// (an __ldg was hoisted above `if (bias)` in one build: a fault at address 0)
+__device__ __forceinline__ float4 ldg_nc_v4(const float4* ptr) {
+  float4 r;
+  asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(ptr));
+  return r;
+}
+__device__ __forceinline__ float ldg_nc(const float* ptr) {
+  float r;
+  asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(r) : "l"(ptr));
+  return r;
+}
 __device__ __forceinline__ float tanh_approx(float u) {
   float t;
   asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
@@ -972,7 +987,7 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
     auto bias_at = [&](const SegTile& tt, int ww) {
       const int col = fdi.mod(ww) * BN + half * HB + lg * kBq + lane;
       const int hb = p.bias_shard_h;
-      return __ldg(p.bias + (hb == 0 ? static_cast<int64_t>(tt.expert) * p.N + col
+      return ldg_nc(p.bias + (hb == 0 ? static_cast<int64_t>(tt.expert) * p.N + col
                                      : (static_cast<int64_t>(col / hb) * p.n_experts + tt.expert) *
                                                hb + col % hb));
     };
@@ -1091,7 +1106,7 @@ __device__ __forceinline__ void umma_body(const UParams& p, const int cluster,
           if (has_bias) {
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
-              const float4 b = __ldg(bias4 + (c0 + i) / 4);
+              const float4 b = ldg_nc_v4(bias4 + (c0 + i) / 4);
               const float2 lo = f2_fma(make_float2(v[i], v[i + 1]), f2(1.f), make_float2(b.x, b.y));
               const float2 hi = f2_fma(make_float2(v[i + 2], v[i + 3]), f2(1.f), make_float2(b.z, b.w));
               v[i] = lo.x; v[i + 1] = lo.y; v[i + 2] = hi.x; v[i + 3] = hi.y;

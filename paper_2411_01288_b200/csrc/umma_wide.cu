@@ -109,7 +109,8 @@ __global__ void __launch_bounds__(kWideThreads, 1)
   uint64_t* tempty_lo = tfull + 2;         // [1] the N = 256 accumulator
   uint64_t* tempty_hi = tempty_lo + 1;     // [2] the two N = 128 slots
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_hi + 2);
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x / 32), 0);  // warp-uniform
+  const int lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kWideStages; ++s) {
       mbar_init(&full[s], 1);
@@ -242,7 +243,7 @@ __global__ void __launch_bounds__(kWideThreads, 1)
           const float4* b4 = reinterpret_cast<const float4*>(bias + gcol);
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
-            const float4 b = __ldg(b4 + i / 4);
+            const float4 b = ldg_nc_v4(b4 + i / 4);
             v[i] += b.x; v[i + 1] += b.y; v[i + 2] += b.z; v[i + 3] += b.w;
           }
         }
@@ -397,7 +398,8 @@ __global__ void __launch_bounds__(kWideThreads, 1)
   uint64_t* tempty_lo = tfull + 2;         // [1] the N = 256 accumulator
   uint64_t* tempty_hi = tempty_lo + 1;     // [2] the two N = 128 slots
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_hi + 2);
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x / 32), 0);  // warp-uniform
+  const int lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kWideStages; ++s) {
       mbar_init(&full[s], 1);
